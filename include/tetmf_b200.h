@@ -1,0 +1,159 @@
+/* tetmf_b200.h -- C ABI of the B200-native matrix-free operator apply.
+ *
+ * Drop-in boundary for the reference's hot path. Plain
+ * pointers and sizes only; no C++ exceptions cross this boundary.
+ *
+ * Reference interfaces replaced:
+ *   tetmf_ctx_create / tetmf_ctx_create_dist
+ *       FormSystem(Form, const MacroMesh&, int level) inputs
+ *       (forms.hpp:46; mesh_by_name mesh.cpp:177-181)
+ *   tetmf_fn_*
+ *       FieldVector (fespace.hpp:69-77) as level-indexed, per-macro lattice
+ *       storage on the device; tetmf_fn_import_ref / _export_ref convert
+ *       from / to the reference's global numbering with ND1 signs
+ *       (DoFIndexer::build fespace.cpp:182-307, fill_map :320-376)
+ *   tetmf_fn_fill_coefficient
+ *       interpolate(indexer, f) for the BASELINE coefficients
+ *       (fespace.cpp:494-506)
+ *   tetmf_op_create
+ *       FormSystem(Form, ...) + coefficient binding (forms.cpp:43-67)
+ *   tetmf_apply (update = TETMF_REPLACE)
+ *       FieldVector FormSystem::apply(v, coeffs, rule) const
+ *       (forms.hpp:65-66, forms.cpp:195-255): w = A v, exact integration
+ *   tetmf_apply (update = TETMF_ADD)
+ *       generated kernel_apply(v, w, c0, c1, ..., jp, tab), w += A v
+ *       (ir.cpp:732-734)
+ *   tetmf_apply_ref_host
+ *       FormSystem::apply with host FieldVectors in reference numbering
+ *       (H2D, permute, apply, permute, D2H)
+ *
+ * Conventions: return 0 on success, else a TETMF_E* code with a message in
+ * tetmf_last_error() (thread-local). The library owns device memory; host
+ * pointers are borrowed for the duration of a call. Calls are ordered on the
+ * context's CUDA stream; tetmf_apply does not synchronize. One host process
+ * per GPU; multi-rank contexts exchange interface sums over NCCL.
+ */
+#ifndef TETMF_B200_H
+#define TETMF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef struct tetmf_ctx tetmf_ctx;
+typedef struct tetmf_fn tetmf_fn;
+typedef struct tetmf_op tetmf_op;
+
+enum {
+  TETMF_OK = 0,
+  TETMF_EINVAL = 1,    /* std::invalid_argument class (forms.cpp:58-67) */
+  TETMF_EINTERNAL = 2, /* std::logic_error class (fespace.cpp:330,400) */
+  TETMF_EDEVICE = 3,   /* CUDA failure */
+  TETMF_ECOMM = 4      /* NCCL failure */
+};
+
+/* spaces: reference enum Space (fespace.hpp:15) */
+enum { TETMF_SPACE_P1 = 0, TETMF_SPACE_P2 = 1, TETMF_SPACE_ND1 = 2 };
+/* forms: reference enum Form (forms.hpp:16) + config 2's P1 -div(k grad) */
+enum { TETMF_FORM_P1 = 0, TETMF_FORM_P2V = 1, TETMF_FORM_N1 = 2, TETMF_FORM_P1K = 3 };
+enum { TETMF_REPLACE = 0, TETMF_ADD = 1 };
+/* coefficients of the BASELINE configs (nodal P1 interpolation) */
+enum { TETMF_COEFF_ALPHA = 0, TETMF_COEFF_BETA = 1, TETMF_COEFF_K = 2, TETMF_COEFF_CONST = 3 };
+
+const char* tetmf_last_error(void);
+const char* tetmf_version(void);
+
+/* mesh_desc: "single-tet", "cube6", "cubes<K>", "cubes<Kx>x<Ky>x<Kz>" or a
+ * reference-format mesh file path. device < 0 creates a planning-only
+ * context (host index machinery, no CUDA calls). */
+int tetmf_ctx_create(const char* mesh_desc, int device, tetmf_ctx** out);
+/* One rank of a multi-GPU context: macros are partitioned contiguously by
+ * id; nccl_unique_id (128 bytes from tetmf_nccl_unique_id) may be NULL for
+ * nranks == 1 or planning-only contexts. */
+int tetmf_ctx_create_dist(const char* mesh_desc, int device, int rank, int nranks,
+                          const void* nccl_unique_id, tetmf_ctx** out);
+int tetmf_ctx_destroy(tetmf_ctx* ctx);
+int tetmf_ctx_set_stream(tetmf_ctx* ctx, void* cuda_stream); /* NULL -> own stream */
+int tetmf_ctx_synchronize(tetmf_ctx* ctx);
+int tetmf_ctx_num_macros(const tetmf_ctx* ctx, int* global_count, int* local_count);
+int tetmf_ctx_local_macros(const tetmf_ctx* ctx, int* out /* local_count */);
+int tetmf_nccl_unique_id(void* out128);
+
+int tetmf_fn_create(tetmf_ctx* ctx, int space, tetmf_fn** out);
+int tetmf_fn_destroy(tetmf_fn* fn);
+/* storage entries on this rank at a level (allocates the level) */
+int tetmf_fn_size(tetmf_fn* fn, int level, int64_t* entries);
+int tetmf_fn_device_ptr(tetmf_fn* fn, int level, double** ptr);
+/* layout-independent seeded values; dirichlet_zero zeroes
+ * carriers on the domain boundary (interior() == 0, fespace.hpp:95-96) */
+int tetmf_fn_fill_seeded(tetmf_fn* fn, int level, uint64_t seed, int dirichlet_zero);
+int tetmf_fn_fill_coefficient(tetmf_fn* fn, int level, int which, double value);
+/* raw storage (this library's layout) <-> host */
+int tetmf_fn_upload(tetmf_fn* fn, int level, const double* host, int64_t entries);
+int tetmf_fn_download(tetmf_fn* fn, int level, double* host, int64_t entries);
+/* reference global numbering (FieldVector order, ND1 key-ascending signs) */
+int tetmf_fn_num_ref_dofs(tetmf_fn* fn, int level, int64_t* count);
+int tetmf_fn_import_ref(tetmf_fn* fn, int level, const double* host_ref);
+int tetmf_fn_export_ref(tetmf_fn* fn, int level, double* host_ref);
+
+int tetmf_op_create(tetmf_ctx* ctx, int form, tetmf_fn* const* coeffs, int ncoeffs, tetmf_op** out);
+int tetmf_op_destroy(tetmf_op* op);
+int tetmf_apply(tetmf_op* op, const tetmf_fn* src, tetmf_fn* dst, int level, int update);
+/* Drop-in for FormSystem::apply: host vectors in reference numbering. src
+ * and dst are scratch functions of the operator's space (contents
+ * overwritten); synchronizes before returning. */
+int tetmf_apply_ref_host(tetmf_op* op, tetmf_fn* src, tetmf_fn* dst, int level, const double* host_v,
+                         double* host_w);
+
+/* pinned host memory for the end-to-end path */
+int tetmf_host_alloc(void** ptr, int64_t bytes);
+int tetmf_host_free(void* ptr);
+
+/* ---- host-side planning hooks (no GPU needed; used by CPU tests) ---- */
+/* reference numbering map of the stored macros (layout entries) */
+int tetmf_plan_ref_map(tetmf_ctx* ctx, int space, int level, int64_t* out, int64_t entries,
+                       int64_t* num_ref_dofs);
+int tetmf_plan_layout(tetmf_ctx* ctx, int space, int level, int64_t* macro_stride, int64_t* class_stride);
+/* rank-local interface groups: sizes, then CSR arrays */
+int tetmf_plan_local_groups(tetmf_ctx* ctx, int space, int level, int64_t* ngroups, int64_t* ncopies,
+                            int64_t* offsets, int64_t* copies);
+/* cross-rank exchange plan: sizes, then arrays (any pointer may be NULL) */
+int tetmf_plan_exchange(tetmf_ctx* ctx, int space, int level, int* npeers, int64_t* nsend, int64_t* nrecv,
+                        int64_t* ngroups, int64_t* nentries, int* peers, int64_t* send_offsets,
+                        int64_t* recv_offsets, int64_t* send_index, int64_t* group_offsets,
+                        int64_t* group_entries);
+/* the product's pack / combine / local-sum bodies run on host arrays */
+int tetmf_host_local_sum(const int64_t* offsets, const int64_t* copies, int64_t ngroups, double* y);
+int tetmf_host_pack(const double* y, const int64_t* send_index, int64_t nsend, double* send);
+int tetmf_host_combine(double* y, const double* recv, const int64_t* group_offsets,
+                       const int64_t* group_entries, int64_t ngroups);
+
+/* element matrix (nloc x nloc, local basis in reference orientation, row =
+ * test) assembled from this library's per-orientation tables; coefficient
+ * vertex values c0/c1 (alpha/beta for N1, k for P1K) -- checks the tables
+ * against FormSystem::local_matrix (forms.cpp:133-177) */
+int tetmf_plan_local_matrix(tetmf_ctx* ctx, int form, int level, int macro, int orientation,
+                            const double* c0, const double* c1, double* out);
+
+/* P1 15-point stencil variants of a macro: 16 point types x 15 weights */
+int tetmf_plan_stencil(tetmf_ctx* ctx, int level, int macro, double* out);
+
+/* FP64 DFMA-chain peak probe: returns the sustained FP64 TFLOP/s measured
+ * on the context's device (bench.py roofline denominator). */
+int tetmf_measure_fp64_peak(tetmf_ctx* ctx, double seconds, double* tflops);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TETMF_B200_H */

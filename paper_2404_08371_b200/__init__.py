@@ -1,0 +1,372 @@
+"""paper_2404_08371_b200 -- B200-native matrix-free FE operator apply.
+
+Python binding (ctypes) over the C ABI in include/tetmf_b200.h. The compute
+path is the CUDA library ``_lib/libtetmf_b200.so`` (sm_100a); there is no CPU
+fallback: importing this package without the built library raises.
+
+Object model (mirrors the reference's FormSystem API, forms.hpp:41-89):
+    ctx = Context("cube6", device=0)
+    x = Function(ctx, SPACE_P1); y = Function(ctx, SPACE_P1)
+    op = Operator(ctx, FORM_P1)
+    x.fill_seeded(level, seed=42)
+    op.apply(x, y, level)            # FormSystem::apply (Replace semantics)
+    w = y.export_ref(level)          # reference global numbering
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libtetmf_b200.so")
+
+SPACE_P1, SPACE_P2, SPACE_ND1 = 0, 1, 2
+FORM_P1, FORM_P2V, FORM_N1, FORM_P1K = 0, 1, 2, 3
+REPLACE, ADD = 0, 1
+COEFF_ALPHA, COEFF_BETA, COEFF_K, COEFF_CONST = 0, 1, 2, 3
+FORM_SPACE = {FORM_P1: SPACE_P1, FORM_P1K: SPACE_P1, FORM_N1: SPACE_ND1, FORM_P2V: SPACE_P2}
+
+EINVAL, EINTERNAL, EDEVICE, ECOMM = 1, 2, 3, 4
+
+
+class TetmfError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"tetmf error {code}: {msg}")
+        self.code = code
+
+
+class InvalidArgument(TetmfError, ValueError):
+    pass
+
+
+_lib: Optional[ctypes.CDLL] = None
+
+_c_i64p = ctypes.POINTER(ctypes.c_int64)
+_c_dp = ctypes.POINTER(ctypes.c_double)
+_c_ip = ctypes.POINTER(ctypes.c_int)
+_c_vp = ctypes.c_void_p
+
+_SIGS = {
+    "tetmf_last_error": (ctypes.c_char_p, []),
+    "tetmf_version": (ctypes.c_char_p, []),
+    "tetmf_ctx_create": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(_c_vp)]),
+    "tetmf_ctx_create_dist": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_vp,
+                                             ctypes.POINTER(_c_vp)]),
+    "tetmf_ctx_destroy": (ctypes.c_int, [_c_vp]),
+    "tetmf_ctx_set_stream": (ctypes.c_int, [_c_vp, _c_vp]),
+    "tetmf_ctx_synchronize": (ctypes.c_int, [_c_vp]),
+    "tetmf_ctx_num_macros": (ctypes.c_int, [_c_vp, _c_ip, _c_ip]),
+    "tetmf_ctx_local_macros": (ctypes.c_int, [_c_vp, _c_ip]),
+    "tetmf_nccl_unique_id": (ctypes.c_int, [_c_vp]),
+    "tetmf_fn_create": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.POINTER(_c_vp)]),
+    "tetmf_fn_destroy": (ctypes.c_int, [_c_vp]),
+    "tetmf_fn_size": (ctypes.c_int, [_c_vp, ctypes.c_int, _c_i64p]),
+    "tetmf_fn_device_ptr": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.POINTER(_c_dp)]),
+    "tetmf_fn_fill_seeded": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_int]),
+    "tetmf_fn_fill_coefficient": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_double]),
+    "tetmf_fn_upload": (ctypes.c_int, [_c_vp, ctypes.c_int, _c_dp, ctypes.c_int64]),
+    "tetmf_fn_download": (ctypes.c_int, [_c_vp, ctypes.c_int, _c_dp, ctypes.c_int64]),
+    "tetmf_fn_num_ref_dofs": (ctypes.c_int, [_c_vp, ctypes.c_int, _c_i64p]),
+    "tetmf_fn_import_ref": (ctypes.c_int, [_c_vp, ctypes.c_int, _c_dp]),
+    "tetmf_fn_export_ref": (ctypes.c_int, [_c_vp, ctypes.c_int, _c_dp]),
+    "tetmf_op_create": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.POINTER(_c_vp), ctypes.c_int,
+                                       ctypes.POINTER(_c_vp)]),
+    "tetmf_op_destroy": (ctypes.c_int, [_c_vp]),
+    "tetmf_apply": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, ctypes.c_int, ctypes.c_int]),
+    "tetmf_apply_ref_host": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, ctypes.c_int, _c_dp, _c_dp]),
+    "tetmf_host_alloc": (ctypes.c_int, [ctypes.POINTER(_c_vp), ctypes.c_int64]),
+    "tetmf_host_free": (ctypes.c_int, [_c_vp]),
+    "tetmf_plan_ref_map": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, _c_i64p, ctypes.c_int64, _c_i64p]),
+    "tetmf_plan_layout": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, _c_i64p, _c_i64p]),
+    "tetmf_plan_local_groups": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, _c_i64p, _c_i64p, _c_i64p,
+                                               _c_i64p]),
+    "tetmf_plan_exchange": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, _c_ip, _c_i64p, _c_i64p, _c_i64p,
+                                           _c_i64p, _c_ip, _c_i64p, _c_i64p, _c_i64p, _c_i64p, _c_i64p]),
+    "tetmf_host_local_sum": (ctypes.c_int, [_c_i64p, _c_i64p, ctypes.c_int64, _c_dp]),
+    "tetmf_host_pack": (ctypes.c_int, [_c_dp, _c_i64p, ctypes.c_int64, _c_dp]),
+    "tetmf_host_combine": (ctypes.c_int, [_c_dp, _c_dp, _c_i64p, _c_i64p, ctypes.c_int64]),
+    "tetmf_measure_fp64_peak": (ctypes.c_int, [_c_vp, ctypes.c_double, _c_dp]),
+    "tetmf_plan_local_matrix": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                               _c_dp, _c_dp, _c_dp]),
+    "tetmf_plan_stencil": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, _c_dp]),
+}
+
+
+def lib() -> ctypes.CDLL:
+    """Loads the CUDA library; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"tetmf CUDA library missing: {LIB_PATH} (run __graft_entry__.build())")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = lib().tetmf_last_error().decode()
+        if rc == EINVAL:
+            raise InvalidArgument(rc, msg)
+        raise TetmfError(rc, msg)
+
+
+def _dptr(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_c_dp)
+
+
+def _iptr(a: np.ndarray):
+    assert a.dtype == np.int64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_c_i64p)
+
+
+class Context:
+    """Mesh + topology + device + rank partition (FormSystem's inputs)."""
+
+    def __init__(self, mesh: str, device: int = 0, rank: int = 0, nranks: int = 1,
+                 nccl_id: Optional[bytes] = None):
+        h = _c_vp()
+        idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        _check(lib().tetmf_ctx_create_dist(mesh.encode(), device, rank, nranks,
+                                           ctypes.cast(idbuf, _c_vp) if idbuf is not None else None,
+                                           ctypes.byref(h)))
+        self._h = h
+        self.mesh = mesh
+        self.device = device
+        self.rank = rank
+        self.nranks = nranks
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tetmf_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_ptr: int):
+        _check(lib().tetmf_ctx_set_stream(self._h, _c_vp(stream_ptr)))
+
+    def synchronize(self):
+        _check(lib().tetmf_ctx_synchronize(self._h))
+
+    def num_macros(self):
+        g, l = ctypes.c_int(), ctypes.c_int()
+        _check(lib().tetmf_ctx_num_macros(self._h, ctypes.byref(g), ctypes.byref(l)))
+        return g.value, l.value
+
+    def local_macros(self):
+        _, l = self.num_macros()
+        out = (ctypes.c_int * max(l, 1))()
+        _check(lib().tetmf_ctx_local_macros(self._h, out))
+        return list(out)[:l]
+
+    # ---- planning hooks (no GPU needed)
+    def layout(self, space: int, level: int):
+        ms, cs = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().tetmf_plan_layout(self._h, space, level, ctypes.byref(ms), ctypes.byref(cs)))
+        return ms.value, cs.value
+
+    def ref_map(self, space: int, level: int) -> tuple[np.ndarray, int]:
+        ms, _ = self.layout(space, level)
+        total = ms * len(self.local_macros())
+        out = np.empty(total, dtype=np.int64)
+        nd = ctypes.c_int64()
+        _check(lib().tetmf_plan_ref_map(self._h, space, level, _iptr(out), total, ctypes.byref(nd)))
+        return out, nd.value
+
+    def local_groups(self, space: int, level: int):
+        ng, nc = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().tetmf_plan_local_groups(self._h, space, level, ctypes.byref(ng), ctypes.byref(nc), None, None))
+        off = np.empty(ng.value + 1, dtype=np.int64)
+        cp = np.empty(max(nc.value, 1), dtype=np.int64)
+        _check(lib().tetmf_plan_local_groups(self._h, space, level, None, None, _iptr(off), _iptr(cp)))
+        return off, cp[: nc.value]
+
+    def exchange_plan(self, space: int, level: int) -> dict:
+        npeers = ctypes.c_int()
+        ns, nr, ng, ne = (ctypes.c_int64() for _ in range(4))
+        L = lib()
+        _check(L.tetmf_plan_exchange(self._h, space, level, ctypes.byref(npeers), ctypes.byref(ns), ctypes.byref(nr),
+                                     ctypes.byref(ng), ctypes.byref(ne), None, None, None, None, None, None))
+        peers = (ctypes.c_int * max(npeers.value, 1))()
+        so = np.empty(npeers.value + 1, dtype=np.int64)
+        ro = np.empty(npeers.value + 1, dtype=np.int64)
+        si = np.empty(max(ns.value, 1), dtype=np.int64)
+        go = np.empty(ng.value + 1, dtype=np.int64)
+        ge = np.empty(max(ne.value, 1), dtype=np.int64)
+        _check(L.tetmf_plan_exchange(self._h, space, level, None, None, None, None, None, peers, _iptr(so),
+                                     _iptr(ro), _iptr(si), _iptr(go), _iptr(ge)))
+        return {"peers": list(peers)[: npeers.value], "send_offsets": so, "recv_offsets": ro,
+                "send_index": si[: ns.value], "group_offsets": go, "group_entries": ge[: ne.value]}
+
+    def local_matrix(self, form: int, level: int, macro: int, orientation: int, c0=None, c1=None) -> np.ndarray:
+        nloc = 6 if form == FORM_N1 else 4
+        out = np.empty(nloc * nloc)
+        a = None if c0 is None else np.ascontiguousarray(c0, dtype=np.float64)
+        b = None if c1 is None else np.ascontiguousarray(c1, dtype=np.float64)
+        _check(lib().tetmf_plan_local_matrix(self._h, form, level, macro, orientation,
+                                             _dptr(a) if a is not None else None,
+                                             _dptr(b) if b is not None else None, _dptr(out)))
+        return out.reshape(nloc, nloc)
+
+    def stencil(self, level: int, macro: int) -> np.ndarray:
+        out = np.empty(16 * 15)
+        _check(lib().tetmf_plan_stencil(self._h, level, macro, _dptr(out)))
+        return out.reshape(16, 15)
+
+    def fp64_peak(self, seconds: float = 1.0) -> float:
+        tf = ctypes.c_double()
+        _check(lib().tetmf_measure_fp64_peak(self._h, seconds, ctypes.byref(tf)))
+        return tf.value
+
+
+class Function:
+    """Level-indexed per-macro lattice storage of one space (device)."""
+
+    def __init__(self, ctx: Context, space: int):
+        h = _c_vp()
+        _check(lib().tetmf_fn_create(ctx.handle, space, ctypes.byref(h)))
+        self._h = h
+        self.ctx = ctx
+        self.space = space
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tetmf_fn_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def size(self, level: int) -> int:
+        n = ctypes.c_int64()
+        _check(lib().tetmf_fn_size(self._h, level, ctypes.byref(n)))
+        return n.value
+
+    def device_ptr(self, level: int) -> int:
+        p = _c_dp()
+        _check(lib().tetmf_fn_device_ptr(self._h, level, ctypes.byref(p)))
+        return ctypes.cast(p, _c_vp).value
+
+    def fill_seeded(self, level: int, seed: int, dirichlet_zero: bool = False):
+        _check(lib().tetmf_fn_fill_seeded(self._h, level, seed, int(dirichlet_zero)))
+
+    def fill_coefficient(self, level: int, which: int, value: float = 0.0):
+        _check(lib().tetmf_fn_fill_coefficient(self._h, level, which, value))
+
+    def upload(self, level: int, data: np.ndarray):
+        data = np.ascontiguousarray(data, dtype=np.float64)
+        _check(lib().tetmf_fn_upload(self._h, level, _dptr(data), data.size))
+
+    def download(self, level: int) -> np.ndarray:
+        out = np.empty(self.size(level), dtype=np.float64)
+        _check(lib().tetmf_fn_download(self._h, level, _dptr(out), out.size))
+        return out
+
+    def num_ref_dofs(self, level: int) -> int:
+        n = ctypes.c_int64()
+        _check(lib().tetmf_fn_num_ref_dofs(self._h, level, ctypes.byref(n)))
+        return n.value
+
+    def import_ref(self, level: int, v: np.ndarray):
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        if v.size != self.num_ref_dofs(level):
+            raise InvalidArgument(EINVAL, "import_ref: vector length does not match num_ref_dofs")
+        _check(lib().tetmf_fn_import_ref(self._h, level, _dptr(v)))
+
+    def export_ref(self, level: int) -> np.ndarray:
+        out = np.empty(self.num_ref_dofs(level), dtype=np.float64)
+        _check(lib().tetmf_fn_export_ref(self._h, level, _dptr(out)))
+        return out
+
+
+class Operator:
+    """Form + coefficient functions (FormSystem + coefficient binding)."""
+
+    def __init__(self, ctx: Context, form: int, coeffs: Sequence[Function] = ()):
+        arr = (_c_vp * max(len(coeffs), 1))(*[c.handle for c in coeffs])
+        h = _c_vp()
+        _check(lib().tetmf_op_create(ctx.handle, form, arr, len(coeffs), ctypes.byref(h)))
+        self._h = h
+        self.ctx = ctx
+        self.form = form
+        self._coeffs = list(coeffs)  # keep alive (borrowed by the library)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tetmf_op_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def apply(self, src: Function, dst: Function, level: int, update: int = REPLACE):
+        _check(lib().tetmf_apply(self._h, src.handle, dst.handle, level, update))
+
+    def apply_ref_host(self, src: Function, dst: Function, level: int, v: np.ndarray, w: np.ndarray):
+        _check(lib().tetmf_apply_ref_host(self._h, src.handle, dst.handle, level, _dptr(v), _dptr(w)))
+
+
+def host_local_sum(offsets, copies, y):
+    _check(lib().tetmf_host_local_sum(_iptr(offsets), _iptr(copies), offsets.size - 1, _dptr(y)))
+
+
+def host_pack(y, send_index):
+    out = np.empty(send_index.size, dtype=np.float64)
+    if send_index.size:
+        _check(lib().tetmf_host_pack(_dptr(y), _iptr(send_index), send_index.size, _dptr(out)))
+    return out
+
+
+def host_combine(y, recv, group_offsets, group_entries):
+    recv = np.ascontiguousarray(recv, dtype=np.float64)
+    if recv.size == 0:
+        recv = np.zeros(1)
+    _check(lib().tetmf_host_combine(_dptr(y), _dptr(recv), _iptr(group_offsets), _iptr(group_entries),
+                                    group_offsets.size - 1))
+
+
+def host_alloc(nbytes: int) -> int:
+    p = _c_vp()
+    _check(lib().tetmf_host_alloc(ctypes.byref(p), nbytes))
+    return p.value
+
+
+def host_free(ptr: int):
+    _check(lib().tetmf_host_free(_c_vp(ptr)))
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().tetmf_nccl_unique_id(buf))
+    return buf.raw

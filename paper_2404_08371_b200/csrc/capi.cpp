@@ -1,0 +1,470 @@
+// capi.cpp -- extern "C" boundary (include/tetmf_b200.h).
+//
+// Exceptions never cross the ABI: std::invalid_argument -> TETMF_EINVAL,
+// std::logic_error -> TETMF_EINTERNAL, DeviceError -> TETMF_EDEVICE,
+// CommError -> TETMF_ECOMM, anything else -> TETMF_EINTERNAL.
+#include "../../include/tetmf_b200.h"
+
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "common.hpp"
+#include "exchange.hpp"
+#include "runtime.hpp"
+#include "runtime_check.hpp"
+
+namespace tetmf {
+void nccl_get_unique_id(void* out);
+void* nccl_comm_create(int nranks, const void* unique_id, int rank);
+void nccl_comm_destroy(void* comm);
+} // namespace tetmf
+
+using namespace tetmf;
+
+struct tetmf_ctx {
+  std::unique_ptr<Context> impl;
+};
+struct tetmf_fn {
+  std::unique_ptr<Function> impl;
+};
+struct tetmf_op {
+  std::unique_ptr<Operator> impl;
+};
+
+namespace {
+
+thread_local std::string g_error;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return TETMF_OK;
+  } catch (const std::invalid_argument& e) {
+    g_error = e.what();
+    return TETMF_EINVAL;
+  } catch (const DeviceError& e) {
+    g_error = e.what();
+    return TETMF_EDEVICE;
+  } catch (const CommError& e) {
+    g_error = e.what();
+    return TETMF_ECOMM;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return TETMF_EINTERNAL;
+  } catch (...) {
+    g_error = "unknown error";
+    return TETMF_EINTERNAL;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) fail_arg(std::string("null argument: ") + what);
+}
+
+Space space_of(int s) {
+  if (s < 0 || s > 2) fail_arg("unknown space id " + std::to_string(s));
+  return static_cast<Space>(s);
+}
+
+std::vector<int> rank_of(const Context& c) {
+  std::vector<int> r(c.mesh().num_tets(), 0);
+  for (int k = 0; k < c.nranks(); ++k)
+    for (int m : partition_macros(c.mesh().num_tets(), k, c.nranks())) r[m] = k;
+  return r;
+}
+
+} // namespace
+
+extern "C" {
+
+const char* tetmf_last_error(void) { return g_error.c_str(); }
+const char* tetmf_version(void) { return "tetmf-b200 0.1 (sm_100a)"; }
+
+int tetmf_ctx_create(const char* mesh_desc, int device, tetmf_ctx** out) {
+  return tetmf_ctx_create_dist(mesh_desc, device, 0, 1, nullptr, out);
+}
+
+int tetmf_ctx_create_dist(const char* mesh_desc, int device, int rank, int nranks, const void* nccl_unique_id,
+                          tetmf_ctx** out) {
+  return guard([&] {
+    need(mesh_desc, "mesh_desc");
+    need(out, "out");
+    if (nranks < 1 || rank < 0 || rank >= nranks) fail_arg("bad rank / world size");
+    auto c = std::make_unique<tetmf_ctx>();
+    const int nm = mesh_by_name(mesh_desc).num_tets();
+    c->impl = std::make_unique<Context>(mesh_desc, device, rank, nranks, partition_macros(nm, rank, nranks));
+    if (nranks > 1 && device >= 0) {
+      need(nccl_unique_id, "nccl_unique_id");
+      void* comm = nccl_comm_create(nranks, nccl_unique_id, rank);
+      c->impl->attach_exchange_backend(std::shared_ptr<void>(comm, nccl_comm_destroy));
+    }
+    *out = c.release();
+  });
+}
+
+int tetmf_ctx_destroy(tetmf_ctx* ctx) {
+  return guard([&] { delete ctx; });
+}
+
+int tetmf_ctx_set_stream(tetmf_ctx* ctx, void* cuda_stream) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->impl->set_stream(static_cast<cudaStream_t>(cuda_stream));
+  });
+}
+
+int tetmf_ctx_synchronize(tetmf_ctx* ctx) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->impl->synchronize();
+  });
+}
+
+int tetmf_ctx_num_macros(const tetmf_ctx* ctx, int* global_count, int* local_count) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (global_count) *global_count = ctx->impl->mesh().num_tets();
+    if (local_count) *local_count = static_cast<int>(ctx->impl->macros().size());
+  });
+}
+
+int tetmf_ctx_local_macros(const tetmf_ctx* ctx, int* out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    const auto& m = ctx->impl->macros();
+    std::memcpy(out, m.data(), m.size() * sizeof(int));
+  });
+}
+
+int tetmf_nccl_unique_id(void* out128) {
+  return guard([&] {
+    need(out128, "out");
+    nccl_get_unique_id(out128);
+  });
+}
+
+int tetmf_fn_create(tetmf_ctx* ctx, int space, tetmf_fn** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    const Space s = space_of(space);
+    if (s == Space::P2) fail_arg("P2 functions are not implemented (SURVEY.md 8(f) next item)");
+    auto f = std::make_unique<tetmf_fn>();
+    f->impl = std::make_unique<Function>(*ctx->impl, s);
+    *out = f.release();
+  });
+}
+
+int tetmf_fn_destroy(tetmf_fn* fn) {
+  return guard([&] { delete fn; });
+}
+
+int tetmf_fn_size(tetmf_fn* fn, int level, int64_t* entries) {
+  return guard([&] {
+    need(fn, "fn");
+    need(entries, "entries");
+    fn->impl->data(level);
+    *entries = fn->impl->size(level);
+  });
+}
+
+int tetmf_fn_device_ptr(tetmf_fn* fn, int level, double** ptr) {
+  return guard([&] {
+    need(fn, "fn");
+    need(ptr, "ptr");
+    *ptr = fn->impl->data(level);
+  });
+}
+
+int tetmf_fn_fill_seeded(tetmf_fn* fn, int level, uint64_t seed, int dirichlet_zero) {
+  return guard([&] {
+    need(fn, "fn");
+    fn->impl->fill_seeded(level, seed, dirichlet_zero != 0);
+  });
+}
+
+int tetmf_fn_fill_coefficient(tetmf_fn* fn, int level, int which, double value) {
+  return guard([&] {
+    need(fn, "fn");
+    fn->impl->fill_coefficient(level, CoeffSpec{which, value});
+  });
+}
+
+int tetmf_fn_upload(tetmf_fn* fn, int level, const double* host, int64_t entries) {
+  return guard([&] {
+    need(fn, "fn");
+    need(host, "host");
+    double* d = fn->impl->data(level);
+    if (entries != fn->impl->size(level)) fail_arg("upload: entry count does not match the layout");
+    Context& c = fn->impl->ctx();
+    TETMF_CUDA(cudaMemcpyAsync(d, host, entries * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
+    c.synchronize();
+  });
+}
+
+int tetmf_fn_download(tetmf_fn* fn, int level, double* host, int64_t entries) {
+  return guard([&] {
+    need(fn, "fn");
+    need(host, "host");
+    double* d = fn->impl->data(level);
+    if (entries != fn->impl->size(level)) fail_arg("download: entry count does not match the layout");
+    Context& c = fn->impl->ctx();
+    TETMF_CUDA(cudaMemcpyAsync(host, d, entries * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
+    c.synchronize();
+  });
+}
+
+int tetmf_fn_num_ref_dofs(tetmf_fn* fn, int level, int64_t* count) {
+  return guard([&] {
+    need(fn, "fn");
+    need(count, "count");
+    *count = fn->impl->num_ref_dofs(level);
+  });
+}
+
+int tetmf_fn_import_ref(tetmf_fn* fn, int level, const double* host_ref) {
+  return guard([&] {
+    need(fn, "fn");
+    need(host_ref, "host_ref");
+    fn->impl->import_ref(level, host_ref);
+  });
+}
+
+int tetmf_fn_export_ref(tetmf_fn* fn, int level, double* host_ref) {
+  return guard([&] {
+    need(fn, "fn");
+    need(host_ref, "host_ref");
+    fn->impl->export_ref(level, host_ref);
+  });
+}
+
+int tetmf_op_create(tetmf_ctx* ctx, int form, tetmf_fn* const* coeffs, int ncoeffs, tetmf_op** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    if (ncoeffs < 0 || (ncoeffs > 0 && !coeffs)) fail_arg("bad coefficient list");
+    std::vector<const Function*> cf;
+    for (int i = 0; i < ncoeffs; ++i) cf.push_back(coeffs[i] ? coeffs[i]->impl.get() : nullptr);
+    if (form < 0 || form > 3) fail_arg("unknown form id " + std::to_string(form));
+    auto o = std::make_unique<tetmf_op>();
+    o->impl = std::make_unique<Operator>(*ctx->impl, static_cast<Form>(form), std::move(cf));
+    *out = o.release();
+  });
+}
+
+int tetmf_op_destroy(tetmf_op* op) {
+  return guard([&] { delete op; });
+}
+
+int tetmf_apply(tetmf_op* op, const tetmf_fn* src, tetmf_fn* dst, int level, int update) {
+  return guard([&] {
+    need(op, "op");
+    need(src, "src");
+    need(dst, "dst");
+    if (update != TETMF_REPLACE && update != TETMF_ADD) fail_arg("unknown update type");
+    op->impl->apply(*src->impl, *dst->impl, level, static_cast<Update>(update));
+  });
+}
+
+int tetmf_apply_ref_host(tetmf_op* op, tetmf_fn* src, tetmf_fn* dst, int level, const double* host_v,
+                         double* host_w) {
+  return guard([&] {
+    need(op, "op");
+    need(src, "src");
+    need(dst, "dst");
+    need(host_v, "host_v");
+    need(host_w, "host_w");
+    Function& s = *src->impl;
+    Function& d = *dst->impl;
+    Context& c = s.ctx();
+    if (c.nranks() > 1) fail_arg("apply_ref_host: single-rank contexts only");
+    const i64 nd = s.num_ref_dofs(level);
+    if (d.num_ref_dofs(level) != nd) fail_arg("apply_ref_host: src/dst space mismatch");
+    static thread_local DeviceBuffer<double> ref;
+    if (ref.size() < static_cast<std::size_t>(nd)) ref.reset(static_cast<std::size_t>(nd));
+    TETMF_CUDA(cudaMemcpyAsync(ref.get(), host_v, nd * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
+    s.import_ref_device(level, ref.get());
+    op->impl->apply(s, d, level, Update::Replace);
+    d.export_ref_device(level, ref.get());
+    TETMF_CUDA(cudaMemcpyAsync(host_w, ref.get(), nd * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
+    c.synchronize();
+  });
+}
+
+int tetmf_host_alloc(void** ptr, int64_t bytes) {
+  return guard([&] {
+    need(ptr, "ptr");
+    TETMF_CUDA(cudaMallocHost(ptr, static_cast<std::size_t>(bytes)));
+  });
+}
+
+int tetmf_host_free(void* ptr) {
+  return guard([&] { TETMF_CUDA(cudaFreeHost(ptr)); });
+}
+
+// ------------------------------------------------------------ planning hooks
+int tetmf_plan_layout(tetmf_ctx* ctx, int space, int level, int64_t* macro_stride, int64_t* class_stride) {
+  return guard([&] {
+    need(ctx, "ctx");
+    const Context& c = *ctx->impl;
+    const auto lay = LevelLayout::make(space_of(space), level, c.mesh().num_tets(), c.macros());
+    if (macro_stride) *macro_stride = lay.macro_stride;
+    if (class_stride) *class_stride = lay.class_stride;
+  });
+}
+
+int tetmf_plan_ref_map(tetmf_ctx* ctx, int space, int level, int64_t* out, int64_t entries,
+                       int64_t* num_ref_dofs) {
+  return guard([&] {
+    need(ctx, "ctx");
+    const Context& c = *ctx->impl;
+    const auto lay = LevelLayout::make(space_of(space), level, c.mesh().num_tets(), c.macros());
+    if (out && entries != lay.total()) fail_arg("plan_ref_map: entry count does not match the layout");
+    const auto rn = build_ref_numbering(c.mesh(), c.topo(), lay);
+    if (out) std::memcpy(out, rn.map.data(), rn.map.size() * sizeof(int64_t));
+    if (num_ref_dofs) *num_ref_dofs = rn.num_dofs;
+  });
+}
+
+int tetmf_plan_local_groups(tetmf_ctx* ctx, int space, int level, int64_t* ngroups, int64_t* ncopies,
+                            int64_t* offsets, int64_t* copies) {
+  return guard([&] {
+    need(ctx, "ctx");
+    const Context& c = *ctx->impl;
+    const auto lay = LevelLayout::make(space_of(space), level, c.mesh().num_tets(), c.macros());
+    const auto g = local_groups_only(c.mesh(), c.topo(), lay, rank_of(c), c.rank());
+    if (ngroups) *ngroups = g.num_groups();
+    if (ncopies) *ncopies = static_cast<int64_t>(g.copies.size());
+    if (offsets) std::memcpy(offsets, g.offsets.data(), g.offsets.size() * sizeof(int64_t));
+    if (copies) std::memcpy(copies, g.copies.data(), g.copies.size() * sizeof(int64_t));
+  });
+}
+
+int tetmf_plan_exchange(tetmf_ctx* ctx, int space, int level, int* npeers, int64_t* nsend, int64_t* nrecv,
+                        int64_t* ngroups, int64_t* nentries, int* peers, int64_t* send_offsets,
+                        int64_t* recv_offsets, int64_t* send_index, int64_t* group_offsets,
+                        int64_t* group_entries) {
+  return guard([&] {
+    need(ctx, "ctx");
+    const Context& c = *ctx->impl;
+    const auto lay = LevelLayout::make(space_of(space), level, c.mesh().num_tets(), c.macros());
+    const auto p = build_exchange_plan(c.mesh(), c.topo(), lay, rank_of(c), c.rank());
+    if (npeers) *npeers = static_cast<int>(p.peers.size());
+    if (nsend) *nsend = p.send_total();
+    if (nrecv) *nrecv = p.recv_total();
+    if (ngroups) *ngroups = p.num_groups();
+    if (nentries) *nentries = static_cast<int64_t>(p.group_entries.size());
+    auto cp = [](auto* dst, const auto& v) {
+      if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+    };
+    cp(peers, p.peers);
+    cp(send_offsets, p.send_offsets);
+    cp(recv_offsets, p.recv_offsets);
+    cp(send_index, p.send_index);
+    cp(group_offsets, p.group_offsets);
+    cp(group_entries, p.group_entries);
+  });
+}
+
+int tetmf_host_local_sum(const int64_t* offsets, const int64_t* copies, int64_t ngroups, double* y) {
+  return guard([&] {
+    for (int64_t g = 0; g < ngroups; ++g) interface_sum_one(y, offsets, copies, g);
+  });
+}
+
+int tetmf_host_pack(const double* y, const int64_t* send_index, int64_t nsend, double* send) {
+  return guard([&] {
+    for (int64_t i = 0; i < nsend; ++i) exchange_pack_one(y, send_index, send, i);
+  });
+}
+
+int tetmf_host_combine(double* y, const double* recv, const int64_t* group_offsets, const int64_t* group_entries,
+                       int64_t ngroups) {
+  return guard([&] {
+    for (int64_t g = 0; g < ngroups; ++g) exchange_combine_one(y, recv, group_offsets, group_entries, g);
+  });
+}
+
+int tetmf_plan_local_matrix(tetmf_ctx* ctx, int form, int level, int macro, int orientation, const double* c0,
+                            const double* c1, double* out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    const Context& c = *ctx->impl;
+    if (orientation < 0 || orientation > 5) fail_arg("orientation out of range");
+    if (form == TETMF_FORM_N1) {
+      need(c0, "alpha");
+      need(c1, "beta");
+      const N1DeviceTable t = pack_n1(n1_tables(c.mesh(), macro, level));
+      double s[6];
+      for (int e = 0; e < 6; ++e) s[e] = local_edge_ref(orientation, e).flipped ? -1.0 : 1.0;
+      const double sa = c0[0] + c0[1] + c0[2] + c0[3];
+      for (int j = 0; j < 6; ++j)
+        for (int i = 0; i < 6; ++i) {
+          const int q = sym6(i, j);
+          double a = sa * t.e[orientation][0][q];
+          for (int m = 0; m < 4; ++m) a += c1[m] * t.e[orientation][1 + m][q];
+          out[j * 6 + i] = s[i] * s[j] * a;
+        }
+    } else if (form == TETMF_FORM_P1 || form == TETMF_FORM_P1K) {
+      const P1DeviceTable t = pack_p1(p1_tables(c.mesh(), macro, level));
+      double kb = 1.0;
+      if (form == TETMF_FORM_P1K) {
+        need(c0, "k");
+        kb = 0.25 * (c0[0] + c0[1] + c0[2] + c0[3]);
+      }
+      for (int j = 0; j < 4; ++j)
+        for (int i = 0; i < 4; ++i) out[j * 4 + i] = kb * t.K[orientation][sym4(i, j)];
+    } else {
+      fail_arg("plan_local_matrix: unsupported form");
+    }
+  });
+}
+
+int tetmf_plan_stencil(tetmf_ctx* ctx, int level, int macro, double* out /* 16 x 15 */) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    const P1Tables t = p1_tables(ctx->impl->mesh(), macro, level);
+    std::memcpy(out, t.stencil, sizeof(t.stencil));
+  });
+}
+
+int tetmf_measure_fp64_peak(tetmf_ctx* ctx, double seconds, double* tflops) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(tflops, "tflops");
+    Context& c = *ctx->impl;
+    if (c.device() < 0) fail_arg("measure_fp64_peak: planning-only context");
+    int sms = 0;
+    TETMF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device()));
+    DeviceBuffer<double> out(1);
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    cudaEvent_t e0, e1;
+    TETMF_CUDA(cudaEventCreate(&e0));
+    TETMF_CUDA(cudaEventCreate(&e1));
+    launch_fp64_peak(out.get(), blocks, threads, 64, c.stream());  // warm-up
+    double best = 0.0;
+    const auto t0 = std::chrono::steady_clock::now();
+    do {
+      TETMF_CUDA(cudaEventRecord(e0, c.stream()));
+      launch_fp64_peak(out.get(), blocks, threads, iters, c.stream());
+      TETMF_CUDA(cudaEventRecord(e1, c.stream()));
+      TETMF_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      TETMF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      const double flops = 2.0 * 8.0 * 16.0 * double(iters) * double(blocks) * double(threads);
+      const double tf = flops / (ms * 1e-3) / 1e12;
+      if (tf > best) best = tf;
+    } while (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() < seconds);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *tflops = best;
+  });
+}
+
+} // extern "C"

@@ -1,0 +1,55 @@
+// device.hpp -- device-side descriptors and kernel launchers (sm_100a).
+//
+// Kernels:
+//   K1 p1_stencil     P1 -Laplace via the assembled 15-point stencil
+//   K2 p1k_cubes      P1 -div(k grad), k in P1, cube-wise element loop
+//   K3 n1_cubes       N1 alpha curl curl + beta, cube-wise element loop
+//   K4 interface_sum  sum of macro copies of shared carriers, write-back
+//   fill / permute    seeded inputs, coefficients, reference numbering I/O
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "lattice.hpp"
+#include "tables.hpp"
+
+namespace tetmf {
+
+// One stored macro as the kernels see it.
+struct MacroDesc {
+  int group;         // geometry group (index into the table array)
+  int bface;         // bit v: face opposite local vertex v is domain boundary
+  i64 V0[3];         // integer world coords (scaled by n * D) of local vertex 0
+  i64 E[3][3];       // integer edge vectors v_{c+1} - v_0 (scaled by D), E[c][r]
+  double X0[3];      // world coords of local vertex 0
+  double dX[3][3];   // world edge vectors, dX[c][r]
+};
+
+struct CoeffSpec {
+  int which;         // 0 alpha = 1+x^2+y^2, 1 beta = 2+sin(pi z), 2 k, 3 constant
+  double value;      // for which == 3
+};
+
+void launch_fill_seeded(double* out, const MacroDesc* d_macros, int nmacros, i64 macro_stride, int n,
+                        bool nd1, i64 class_stride, std::uint64_t seed, bool dirichlet, cudaStream_t s);
+void launch_fill_coeff(double* out, const MacroDesc* d_macros, int nmacros, i64 macro_stride, int n,
+                       CoeffSpec spec, cudaStream_t s);
+void launch_import_ref(double* lat, const i64* map, i64 total, const double* ref, cudaStream_t s);
+void launch_export_ref(const double* lat, const i64* map, i64 total, double* ref, cudaStream_t s);
+void launch_interface_sum(double* y, const i64* offsets, const i64* copies, i64 ngroups, cudaStream_t s);
+void launch_axpy(double* y, const double* x, double a, i64 count, cudaStream_t s);
+
+void launch_p1_stencil(const double* x, double* y, const MacroDesc* d_macros, int nmacros, i64 macro_stride,
+                       int n, const P1DeviceTable* d_tables, cudaStream_t s);
+void launch_p1k_cubes(const double* x, const double* k, double* y, const MacroDesc* d_macros, int nmacros,
+                      i64 macro_stride, int n, const P1DeviceTable* d_tables, cudaStream_t s);
+void launch_n1_cubes(const double* x, const double* alpha, const double* beta, double* y,
+                     const MacroDesc* d_macros, int nmacros, i64 macro_stride, i64 class_stride,
+                     i64 coeff_stride, int n, const N1DeviceTable* d_tables, cudaStream_t s);
+
+// FP64 DFMA-chain peak probe (used by bench.py to measure the FP64 roof).
+void launch_fp64_peak(double* out, int blocks, int threads, int iters, cudaStream_t s);
+
+} // namespace tetmf

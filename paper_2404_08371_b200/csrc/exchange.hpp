@@ -1,0 +1,110 @@
+// exchange.hpp -- cross-rank interface exchange (the path's one collective).
+//
+// After the element kernels, every rank holds macro-local partial sums on
+// the carriers its macros share with macros of other ranks. The exchange is
+// a sparse neighbour SUM-exchange (not an all-reduce):
+//   1. pack:    send[p][k] = +-y[local copy]      (owner orientation)
+//   2. NCCL grouped send/recv with every peer rank over NVLink
+//   3. combine: per shared carrier, sum ALL copies in ascending global macro
+//               id order (local values or receive-buffer entries), write the
+//               total back to the local copies.
+// Summation order depends only on global macro ids, so every rank (and the
+// single-rank run) produces bitwise-identical totals.
+//
+// The pack / combine bodies are __host__ __device__ so the exact product code
+// also runs on the CPU for the world_size-2 gloo tests (tests/test_dist.py).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "lattice.hpp"
+#include "layout.hpp"
+#include "mesh.hpp"
+
+namespace tetmf {
+
+struct ExchangePlan {
+  // peers and per-peer send / receive counts (entries of doubles)
+  std::vector<int> peers;
+  std::vector<i64> send_offsets;  // size peers+1
+  std::vector<i64> recv_offsets;  // size peers+1
+  // send entries: (storage index << 1) | negative
+  std::vector<i64> send_index;
+  // combine CSR over cross-rank carriers; entry = (v << 2) | (remote << 1) | negative
+  // v = storage index (local) or position in the concatenated receive buffer
+  std::vector<i64> group_offsets;
+  std::vector<i64> group_entries;
+  i64 num_groups() const { return static_cast<i64>(group_offsets.size()) - 1; }
+  i64 send_total() const { return send_offsets.empty() ? 0 : send_offsets.back(); }
+  i64 recv_total() const { return recv_offsets.empty() ? 0 : recv_offsets.back(); }
+};
+
+// rank_of[m] = rank storing macro m. Local-only groups are excluded here
+// (they are summed by the interface kernel, K4).
+ExchangePlan build_exchange_plan(const MacroMesh& mesh, const Topology& topo, const LevelLayout& lay,
+                                 const std::vector<int>& rank_of, int rank);
+
+// Interface groups whose copies are all on this rank.
+InterfaceGroups local_groups_only(const MacroMesh& mesh, const Topology& topo, const LevelLayout& lay,
+                                  const std::vector<int>& rank_of, int rank);
+
+TM_HD void exchange_pack_one(const double* y, const i64* send_index, double* send, i64 i) {
+  const i64 e = send_index[i];
+  const double v = y[e >> 1];
+  send[i] = (e & 1) ? -v : v;
+}
+
+TM_HD void exchange_combine_one(double* y, const double* recv, const i64* offsets, const i64* entries, i64 g) {
+  const i64 b = offsets[g], e = offsets[g + 1];
+  double s = 0.0;
+  for (i64 k = b; k < e; ++k) {
+    const i64 c = entries[k];
+    const double v = (c & 2) ? recv[c >> 2] : y[c >> 2];
+    s += (c & 1) ? -v : v;
+  }
+  for (i64 k = b; k < e; ++k) {
+    const i64 c = entries[k];
+    if (c & 2) continue;
+    y[c >> 2] = (c & 1) ? -s : s;
+  }
+}
+
+// K4 body for rank-local groups (same arithmetic as interface_sum_kernel)
+TM_HD void interface_sum_one(double* y, const i64* offsets, const i64* copies, i64 g) {
+  const i64 b = offsets[g], e = offsets[g + 1];
+  double s = 0.0;
+  for (i64 k = b; k < e; ++k) {
+    const i64 c = copies[k];
+    const double v = y[c >> 1];
+    s += (c & 1) ? -v : v;
+  }
+  for (i64 k = b; k < e; ++k) {
+    const i64 c = copies[k];
+    y[c >> 1] = (c & 1) ? -s : s;
+  }
+}
+
+// Device side of one level's plan + the NCCL transport.
+class Exchange {
+public:
+  Exchange(ExchangePlan plan, void* nccl_comm);
+  ~Exchange();
+  // pack -> send/recv -> combine on `stream`
+  void run(double* y, cudaStream_t stream);
+  const ExchangePlan& plan() const { return plan_; }
+
+private:
+  ExchangePlan plan_;
+  void* comm_;
+  i64* d_send_index_ = nullptr;
+  i64* d_group_offsets_ = nullptr;
+  i64* d_group_entries_ = nullptr;
+  double* d_send_ = nullptr;
+  double* d_recv_ = nullptr;
+};
+
+} // namespace tetmf

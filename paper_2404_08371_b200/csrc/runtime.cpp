@@ -1,0 +1,315 @@
+// runtime.cpp -- Context / Function / Operator (host C++).
+#include "runtime.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+#include "common.hpp"
+#include "exchange.hpp"
+#include "runtime_check.hpp"
+
+namespace tetmf {
+
+void* nccl_comm_create(int nranks, const void* unique_id, int rank);  // exchange_nccl.cu
+void nccl_comm_destroy(void* comm);
+
+// ---------------------------------------------------------------- buffers
+template <typename T>
+void DeviceBuffer<T>::reset(std::size_t count) {
+  release();
+  if (count == 0) return;
+  TETMF_CUDA(cudaMalloc(&p_, count * sizeof(T)));
+  n_ = count;
+}
+template <typename T>
+void DeviceBuffer<T>::release() {
+  if (p_) cudaFree(p_);
+  p_ = nullptr;
+  n_ = 0;
+}
+template <typename T>
+void DeviceBuffer<T>::upload(const T* host, std::size_t count, cudaStream_t s) {
+  reset(count);
+  if (count) {
+    TETMF_CUDA(cudaMemcpyAsync(p_, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    TETMF_CUDA(cudaStreamSynchronize(s));
+  }
+}
+template class DeviceBuffer<double>;
+template class DeviceBuffer<i64>;
+template class DeviceBuffer<MacroDesc>;
+template class DeviceBuffer<P1DeviceTable>;
+template class DeviceBuffer<N1DeviceTable>;
+
+// ---------------------------------------------------------------- forms
+const FormInfo& form_info(Form f) {
+  // the reference's kForms (forms.cpp:10-14) plus config 2's P1 -div(k grad)
+  static const FormInfo kInfo[4] = {
+      {Form::P1Diffusion, "P1", Space::P1, {}},
+      {Form::P2VDiffusion, "P2V", Space::P2, {Space::P2}},
+      {Form::N1CurlCurlMass, "N1", Space::ND1, {Space::P1, Space::P1}},
+      {Form::P1KDiffusion, "P1K", Space::P1, {Space::P1}},
+  };
+  const int i = static_cast<int>(f);
+  if (i < 0 || i > 3) fail_arg("unknown form id " + std::to_string(i));
+  return kInfo[i];
+}
+
+std::vector<int> partition_macros(int num_macros, int rank, int nranks) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) fail_arg("partition: bad rank / world size");
+  std::vector<int> out;
+  const long long b = static_cast<long long>(num_macros) * rank / nranks;
+  const long long e = static_cast<long long>(num_macros) * (rank + 1) / nranks;
+  for (long long m = b; m < e; ++m) out.push_back(static_cast<int>(m));
+  return out;
+}
+
+// ---------------------------------------------------------------- context
+Context::Context(const std::string& mesh_desc, int device, int rank, int nranks, std::vector<int> macros)
+    : mesh_(mesh_by_name(mesh_desc)), topo_(mesh_), device_(device), rank_(rank), nranks_(nranks) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) fail_arg("context: bad rank / world size");
+  macros_ = macros.empty() && nranks == 1 ? partition_macros(mesh_.num_tets(), 0, 1) : std::move(macros);
+  std::sort(macros_.begin(), macros_.end());
+  for (int m : macros_)
+    if (m < 0 || m >= mesh_.num_tets()) fail_arg("context: macro id out of range");
+  group_ = geometry_groups(mesh_, macros_, &ngroups_);
+  if (device_ >= 0) {
+    TETMF_CUDA(cudaSetDevice(device_));
+    TETMF_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
+    stream_ = own_stream_;
+  }
+}
+
+Context::~Context() {
+  levels_.clear();
+  if (own_stream_) cudaStreamDestroy(own_stream_);
+}
+
+void Context::synchronize() const {
+  if (device_ >= 0) TETMF_CUDA(cudaStreamSynchronize(stream_));
+}
+
+Context::LevelData& Context::level(Space s, int level) {
+  const auto key = std::make_pair(static_cast<int>(s), level);
+  auto it = levels_.find(key);
+  if (it != levels_.end()) return *it->second;
+  if (device_ < 0) fail_arg("context has no device (planning-only context)");
+  auto ld = std::make_unique<LevelData>();
+  ld->lay = LevelLayout::make(s, level, mesh_.num_tets(), macros_);
+  const int n = ld->lay.n;
+  std::vector<MacroDesc> descs(macros_.size());
+  for (std::size_t li = 0; li < macros_.size(); ++li) {
+    const int m = macros_[li];
+    const auto& t = mesh_.tets[m];
+    MacroDesc& d = descs[li];
+    std::memset(&d, 0, sizeof(d));
+    d.group = group_[li];
+    d.bface = 0;
+    for (int v = 0; v < 4; ++v)
+      if (topo_.boundary_face[m][v]) d.bface |= 1 << v;
+    for (int r = 0; r < 3; ++r) {
+      d.V0[r] = static_cast<i64>(n) * topo_.int_vertices[t[0]][r];
+      d.X0[r] = mesh_.vertices[t[0]][r];
+      for (int c = 0; c < 3; ++c) {
+        d.E[c][r] = topo_.int_vertices[t[c + 1]][r] - topo_.int_vertices[t[0]][r];
+        d.dX[c][r] = mesh_.vertices[t[c + 1]][r] - mesh_.vertices[t[0]][r];
+      }
+    }
+  }
+  ld->macros.upload(descs.data(), descs.size(), stream_);
+  std::vector<int> rank_of(mesh_.num_tets(), -1);
+  if (nranks_ == 1) {
+    std::fill(rank_of.begin(), rank_of.end(), 0);
+  } else {
+    for (int r = 0; r < nranks_; ++r)
+      for (int m : partition_macros(mesh_.num_tets(), r, nranks_)) rank_of[m] = r;
+    for (int m : macros_)
+      if (rank_of[m] != rank_) fail_arg("context: multi-rank contexts use the default partition");
+  }
+  ld->groups = local_groups_only(mesh_, topo_, ld->lay, rank_of, rank_);
+  ld->group_offsets.upload(ld->groups.offsets.data(), ld->groups.offsets.size(), stream_);
+  ld->group_copies.upload(ld->groups.copies.data(), ld->groups.copies.size(), stream_);
+  if (nranks_ > 1)
+    ld->exchange = std::make_unique<Exchange>(build_exchange_plan(mesh_, topo_, ld->lay, rank_of, rank_),
+                                              comm_backend_.get());
+  auto& ref = *ld;
+  levels_.emplace(key, std::move(ld));
+  return ref;
+}
+
+Context::LevelData& Context::ref_level(Space s, int level) {
+  LevelData& ld = this->level(s, level);
+  if (!ld.ref) {
+    ld.ref = std::make_unique<RefNumbering>(build_ref_numbering(mesh_, topo_, ld.lay));
+    ld.ref_map.upload(ld.ref->map.data(), ld.ref->map.size(), stream_);
+  }
+  return ld;
+}
+
+// ---------------------------------------------------------------- function
+double* Function::data(int level) {
+  auto it = data_.find(level);
+  if (it != data_.end()) return it->second.get();
+  auto& ld = ctx_->level(space_, level);
+  DeviceBuffer<double> buf(static_cast<std::size_t>(ld.lay.total()));
+  if (buf.get()) TETMF_CUDA(cudaMemsetAsync(buf.get(), 0, buf.size() * sizeof(double), ctx_->stream()));
+  double* p = buf.get();
+  data_.emplace(level, std::move(buf));
+  return p;
+}
+
+const double* Function::data(int level) const {
+  auto it = data_.find(level);
+  if (it == data_.end()) fail_arg("function has no data at level " + std::to_string(level));
+  return it->second.get();
+}
+
+i64 Function::size(int level) const { return ctx_->level(space_, level).lay.total(); }
+
+void Function::fill_seeded(int level, std::uint64_t seed, bool dirichlet_zero) {
+  if (ctx_->topo().coord_scale == 0) fail_arg("fill_seeded: mesh vertices are not on a dyadic grid");
+  auto& ld = ctx_->level(space_, level);
+  double* p = data(level);
+  if (ld.lay.macros.empty()) return;
+  launch_fill_seeded(p, ld.macros.get(), static_cast<int>(ld.lay.macros.size()), ld.lay.macro_stride, ld.lay.n,
+                     space_ == Space::ND1, ld.lay.class_stride, seed, dirichlet_zero, ctx_->stream());
+}
+
+void Function::fill_coefficient(int level, CoeffSpec spec) {
+  if (space_ != Space::P1) fail_arg("fill_coefficient: coefficient functions live in P1");
+  if (spec.which < 0 || spec.which > 3) fail_arg("fill_coefficient: unknown coefficient");
+  auto& ld = ctx_->level(space_, level);
+  double* p = data(level);
+  if (ld.lay.macros.empty()) return;
+  launch_fill_coeff(p, ld.macros.get(), static_cast<int>(ld.lay.macros.size()), ld.lay.macro_stride, ld.lay.n, spec,
+                    ctx_->stream());
+}
+
+i64 Function::num_ref_dofs(int level) { return ctx_->ref_level(space_, level).ref->num_dofs; }
+
+void Function::import_ref_device(int level, const double* dev_ref) {
+  auto& ld = ctx_->ref_level(space_, level);
+  launch_import_ref(data(level), ld.ref_map.get(), ld.lay.total(), dev_ref, ctx_->stream());
+}
+
+void Function::export_ref_device(int level, double* dev_ref) {
+  auto& ld = ctx_->ref_level(space_, level);
+  launch_export_ref(data(level), ld.ref_map.get(), ld.lay.total(), dev_ref, ctx_->stream());
+}
+
+void Function::import_ref(int level, const double* host_ref) {
+  const i64 nd = num_ref_dofs(level);
+  DeviceBuffer<double> tmp(static_cast<std::size_t>(nd));
+  TETMF_CUDA(cudaMemcpyAsync(tmp.get(), host_ref, nd * sizeof(double), cudaMemcpyHostToDevice, ctx_->stream()));
+  import_ref_device(level, tmp.get());
+  ctx_->synchronize();
+}
+
+void Function::export_ref(int level, double* host_ref) {
+  if (ctx_->nranks() > 1) fail_arg("export_ref: single-rank contexts only (gather on the caller side)");
+  const i64 nd = num_ref_dofs(level);
+  DeviceBuffer<double> tmp(static_cast<std::size_t>(nd));
+  export_ref_device(level, tmp.get());
+  TETMF_CUDA(cudaMemcpyAsync(host_ref, tmp.get(), nd * sizeof(double), cudaMemcpyDeviceToHost, ctx_->stream()));
+  ctx_->synchronize();
+}
+
+// ---------------------------------------------------------------- operator
+Operator::Operator(Context& ctx, Form form, std::vector<const Function*> coeffs)
+    : ctx_(&ctx), form_(form), coeffs_(std::move(coeffs)) {
+  const FormInfo& fi = form_info(form);
+  if (form == Form::P2VDiffusion) fail_arg("form P2V is not implemented (SURVEY.md 8(f) next item)");
+  if (coeffs_.size() != fi.coeffSpaces.size())
+    fail_arg(std::string("form ") + fi.name + " expects " + std::to_string(fi.coeffSpaces.size()) +
+             " coefficient field(s)");
+  for (std::size_t c = 0; c < coeffs_.size(); ++c) {
+    if (!coeffs_[c]) fail_arg("missing coefficient field");
+    if (&coeffs_[c]->ctx() != ctx_) fail_arg("coefficient field belongs to another context");
+    if (coeffs_[c]->space() != fi.coeffSpaces[c]) fail_arg("coefficient field has wrong space or level");
+  }
+}
+
+Operator::LevelTables& Operator::tables(int level) {
+  auto it = tables_.find(level);
+  if (it != tables_.end()) return *it->second;
+  auto lt = std::make_unique<LevelTables>();
+  const int ng = ctx_->num_geometry_groups();
+  const auto& macros = ctx_->macros();
+  const auto& grp = ctx_->geometry_group();
+  if (form_ == Form::N1CurlCurlMass) {
+    std::vector<N1DeviceTable> t(ng);
+    std::vector<bool> done(ng, false);
+    for (std::size_t li = 0; li < macros.size(); ++li)
+      if (!done[grp[li]]) {
+        t[grp[li]] = pack_n1(n1_tables(ctx_->mesh(), macros[li], level));
+        done[grp[li]] = true;
+      }
+    lt->n1.upload(t.data(), t.size(), ctx_->stream());
+  } else {
+    std::vector<P1DeviceTable> t(ng);
+    std::vector<bool> done(ng, false);
+    for (std::size_t li = 0; li < macros.size(); ++li)
+      if (!done[grp[li]]) {
+        t[grp[li]] = pack_p1(p1_tables(ctx_->mesh(), macros[li], level));
+        done[grp[li]] = true;
+      }
+    lt->p1.upload(t.data(), t.size(), ctx_->stream());
+  }
+  auto& ref = *lt;
+  tables_.emplace(level, std::move(lt));
+  return ref;
+}
+
+void Operator::check(const Function& src, const Function& dst, int level) const {
+  const FormInfo& fi = info();
+  if (&src.ctx() != ctx_ || &dst.ctx() != ctx_) fail_arg("apply: functions belong to another context");
+  if (src.space() != fi.trial || dst.space() != fi.trial || !src.has_level(level))
+    fail_arg("apply: field shape mismatch");
+  if (&src == &dst) fail_arg("apply: src and dst must be different functions");
+  if ((form_ == Form::N1CurlCurlMass) && level < 1) fail_arg("apply: N1 requires level >= 1");
+  for (const Function* c : coeffs_)
+    if (!c->has_level(level)) fail_arg("coefficient field has wrong space or level");
+}
+
+void Operator::kernel_apply(const double* x, double* y, int level) {
+  auto& ld = ctx_->level(info().trial, level);
+  const int nm = static_cast<int>(ld.lay.macros.size());
+  if (nm == 0) return;
+  auto& t = tables(level);
+  const cudaStream_t s = ctx_->stream();
+  switch (form_) {
+    case Form::P1Diffusion:
+      launch_p1_stencil(x, y, ld.macros.get(), nm, ld.lay.macro_stride, ld.lay.n, t.p1.get(), s);
+      break;
+    case Form::P1KDiffusion:
+      launch_p1k_cubes(x, coeffs_[0]->data(level), y, ld.macros.get(), nm, ld.lay.macro_stride, ld.lay.n,
+                       t.p1.get(), s);
+      break;
+    case Form::N1CurlCurlMass: {
+      auto& cl = ctx_->level(Space::P1, level);
+      launch_n1_cubes(x, coeffs_[0]->data(level), coeffs_[1]->data(level), y, ld.macros.get(), nm,
+                      ld.lay.macro_stride, ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, t.n1.get(), s);
+      break;
+    }
+    default:
+      fail_internal("kernel_apply: unsupported form");
+  }
+  launch_interface_sum(y, ld.group_offsets.get(), ld.group_copies.get(), ld.groups.num_groups(), s);
+  if (ld.exchange) ld.exchange->run(y, s);
+}
+
+void Operator::apply(const Function& src, Function& dst, int level, Update upd) {
+  check(src, dst, level);
+  const double* x = src.data(level);
+  if (upd == Update::Replace) {
+    kernel_apply(x, dst.data(level), level);
+    return;
+  }
+  auto it = scratch_.find(level);
+  if (it == scratch_.end())
+    it = scratch_.emplace(level, DeviceBuffer<double>(static_cast<std::size_t>(dst.size(level)))).first;
+  kernel_apply(x, it->second.get(), level);
+  launch_axpy(dst.data(level), it->second.get(), 1.0, dst.size(level), ctx_->stream());
+}
+
+} // namespace tetmf

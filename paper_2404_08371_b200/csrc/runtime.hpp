@@ -1,0 +1,170 @@
+// runtime.hpp -- host C++ operator / function API over the CUDA kernels.
+//
+// Mirrors the reference's operator API (FormSystem, forms.hpp:41-89) in the
+// level-indexed, macro-primitive form the north star asks for:
+//
+//   Context    mesh + topology + device + rank partition  (FormSystem ctor
+//              inputs: MacroMesh, level; forms.cpp:43-56)
+//   Function   level-indexed per-macro lattice storage     (FieldVector,
+//              fespace.hpp:69-77, but device-resident and per macro)
+//   Operator   form + coefficient functions + tables        (FormSystem +
+//              StarTables, forms.cpp:33-41, 69-131)
+//   Operator::apply(src, dst, level, update)                (FormSystem::apply
+//              forms.cpp:195-255: REPLACE; generated kernel_apply ir.cpp:732:
+//              ADD)
+//
+// Errors: std::invalid_argument for wrong space/level/coefficients (as the
+// reference), std::logic_error for internal inconsistency, DeviceError /
+// CommError for CUDA / NCCL failures. Not thread-safe per object (the
+// reference's const methods mutate caches too, forms.hpp:86-87).
+#pragma once
+
+#include <array>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "device.hpp"
+#include "layout.hpp"
+#include "mesh.hpp"
+#include "tables.hpp"
+
+namespace tetmf {
+
+template <typename T>
+class DeviceBuffer {
+public:
+  DeviceBuffer() = default;
+  explicit DeviceBuffer(std::size_t count) { reset(count); }
+  ~DeviceBuffer() { release(); }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    if (this != &o) { release(); p_ = o.p_; n_ = o.n_; o.p_ = nullptr; o.n_ = 0; }
+    return *this;
+  }
+  void reset(std::size_t count);
+  void release();
+  void upload(const T* host, std::size_t count, cudaStream_t s);
+  T* get() const { return p_; }
+  std::size_t size() const { return n_; }
+
+private:
+  T* p_ = nullptr;
+  std::size_t n_ = 0;
+};
+
+enum class Form : int { P1Diffusion = 0, P2VDiffusion = 1, N1CurlCurlMass = 2, P1KDiffusion = 3 };
+enum class Update : int { Replace = 0, Add = 1 };
+
+struct FormInfo {
+  Form id;
+  const char* name;
+  Space trial;
+  std::vector<Space> coeffSpaces;
+};
+const FormInfo& form_info(Form f);
+
+class Exchange;  // multi-rank interface exchange (exchange.hpp)
+
+class Context {
+public:
+  // macros: the macro ids this rank stores (empty = all, single rank)
+  Context(const std::string& mesh_desc, int device, int rank, int nranks, std::vector<int> macros);
+  ~Context();
+
+  const MacroMesh& mesh() const { return mesh_; }
+  const Topology& topo() const { return topo_; }
+  int device() const { return device_; }
+  int rank() const { return rank_; }
+  int nranks() const { return nranks_; }
+  const std::vector<int>& macros() const { return macros_; }
+  const std::vector<int>& geometry_group() const { return group_; }  // per local macro
+  int num_geometry_groups() const { return ngroups_; }
+  cudaStream_t stream() const { return stream_; }
+  void set_stream(cudaStream_t s) { stream_ = s; }
+  void synchronize() const;
+
+  struct LevelData {
+    LevelLayout lay;
+    DeviceBuffer<MacroDesc> macros;
+    InterfaceGroups groups;
+    DeviceBuffer<i64> group_offsets, group_copies;
+    std::unique_ptr<RefNumbering> ref;  // lazily, import/export only
+    DeviceBuffer<i64> ref_map;
+    std::unique_ptr<Exchange> exchange; // nranks > 1
+  };
+  LevelData& level(Space s, int level);
+  LevelData& ref_level(Space s, int level);  // level() + reference numbering
+
+  void attach_exchange_backend(std::shared_ptr<void> backend) { comm_backend_ = std::move(backend); }
+  const std::shared_ptr<void>& comm_backend() const { return comm_backend_; }
+
+private:
+  MacroMesh mesh_;
+  Topology topo_;
+  int device_, rank_, nranks_;
+  std::vector<int> macros_;
+  std::vector<int> group_;
+  int ngroups_ = 0;
+  cudaStream_t stream_ = nullptr;
+  cudaStream_t own_stream_ = nullptr;
+  std::map<std::pair<int, int>, std::unique_ptr<LevelData>> levels_;
+  std::shared_ptr<void> comm_backend_;
+};
+
+class Function {
+public:
+  Function(Context& ctx, Space s) : ctx_(&ctx), space_(s) {}
+  Context& ctx() const { return *ctx_; }
+  Space space() const { return space_; }
+  double* data(int level);              // allocates (zeroed) on first use
+  const double* data(int level) const;  // throws if never allocated
+  bool has_level(int level) const { return data_.count(level) > 0; }
+  i64 size(int level) const;            // storage entries on this rank
+
+  void fill_seeded(int level, std::uint64_t seed, bool dirichlet_zero);
+  void fill_coefficient(int level, CoeffSpec spec);
+  void import_ref(int level, const double* host_ref);  // reference numbering in
+  void export_ref(int level, double* host_ref);        // reference numbering out
+  void import_ref_device(int level, const double* dev_ref);
+  void export_ref_device(int level, double* dev_ref);
+  i64 num_ref_dofs(int level);
+
+private:
+  Context* ctx_;
+  Space space_;
+  std::map<int, DeviceBuffer<double>> data_;
+};
+
+class Operator {
+public:
+  Operator(Context& ctx, Form form, std::vector<const Function*> coeffs);
+  Form form() const { return form_; }
+  const FormInfo& info() const { return form_info(form_); }
+  void apply(const Function& src, Function& dst, int level, Update upd);
+
+private:
+  struct LevelTables {
+    DeviceBuffer<P1DeviceTable> p1;
+    DeviceBuffer<N1DeviceTable> n1;
+  };
+  LevelTables& tables(int level);
+  void check(const Function& src, const Function& dst, int level) const;
+  void kernel_apply(const double* x, double* y, int level);
+
+  Context* ctx_;
+  Form form_;
+  std::vector<const Function*> coeffs_;
+  std::map<int, std::unique_ptr<LevelTables>> tables_;
+  std::map<int, DeviceBuffer<double>> scratch_;
+};
+
+// default contiguous partition of macro ids over ranks
+std::vector<int> partition_macros(int num_macros, int rank, int nranks);
+
+} // namespace tetmf

@@ -1,0 +1,85 @@
+// tables.hpp -- per (macro, level, orientation) micro-invariant tables.
+//
+// This is the paper's tabulation "T" plus loop-invariant hoisting "I"
+// (PAPER.md:884-903), evaluated once per macro on the host:
+//  * micro Jacobian J = A * D * 2^-L, det = detA * detD * 2^-3L
+//    (micro_jacobian mesh.cpp:243-262)
+//  * P1 stiffness K_o[i][j] = vol * (J^-T grad_i) . (J^-T grad_j) -- the
+//    reference's starA summed over an exact rule (forms.cpp:110-116)
+//  * P1 15-point stencil variants: per lattice-point type (which of the four
+//    macro faces the point lies on) the sum of K_o over the incident micro
+//    elements that belong to the macro
+//  * N1: Kc_o = s_i s_j vol/4 curl_i.curl_j and T_o[m] = s_i s_j
+//    int lambda_m phi_i.phi_j (exact), so that
+//      A_e = (sum_m alpha_m) Kc_o + sum_m beta_m T_o[m]
+//    equals the reference's starA/starB contraction (forms.cpp:93-108,
+//    233-243) for P1 coefficients; s_i = -1 where the local edge runs
+//    against its class direction (ND1 signs folded into the table).
+#pragma once
+
+#include <array>
+#include <vector>
+
+#include "lattice.hpp"
+#include "mesh.hpp"
+
+namespace tetmf {
+
+struct OrientGeom {
+  double J[3][3];
+  double det;
+  double JinvT[3][3];
+  double vol;  // |det| / 6
+};
+
+OrientGeom orient_geometry(const MacroMesh& mesh, int macro, int level, int o);
+
+// 15-point stencil offsets: 0 = centre, 2c+1 = +dir_c, 2c+2 = -dir_c
+TM_HD Off3 stencil_offset(int k) {
+  if (k == 0) return {0, 0, 0};
+  const int c = (k - 1) >> 1;
+  const int s = (k & 1) ? 1 : -1;
+  const Off3 d = edge_dir(c);
+  return {s * d.x, s * d.y, s * d.z};
+}
+
+struct P1Tables {
+  double K[6][4][4];        // per orientation local stiffness
+  double stencil[16][15];   // per point type (bit0 x=0, bit1 y=0, bit2 z=0, bit3 x+y+z=n)
+};
+P1Tables p1_tables(const MacroMesh& mesh, int macro, int level);
+
+struct N1Tables {
+  double Kc[6][6][6];       // [o][j][i] curl-curl / 4, signs folded
+  double T[6][4][6][6];     // [o][m][j][i] mass moments, signs folded
+};
+N1Tables n1_tables(const MacroMesh& mesh, int macro, int level);
+
+// Device table image of one distinct macro geometry, as consumed by the
+// kernels (packed symmetric storage, see kernels_*.cu).
+struct P1DeviceTable {
+  double stencil[16][16];   // 16 slots per type (last unused) for alignment
+  double K[6][10];          // packed upper triangle (i<=j) of K_o
+};
+struct N1DeviceTable {
+  // per orientation: 21 packed entries of Kc, then 4 x 21 of T[m]
+  double e[6][5][21];
+};
+P1DeviceTable pack_p1(const P1Tables& t);
+N1DeviceTable pack_n1(const N1Tables& t);
+
+// packed index of (i, j), i <= j < 6 (row-major upper triangle)
+TM_HD int sym6(int i, int j) {
+  if (i > j) { const int t = i; i = j; j = t; }
+  return i * 6 - i * (i - 1) / 2 + (j - i);
+}
+TM_HD int sym4(int i, int j) {
+  if (i > j) { const int t = i; i = j; j = t; }
+  return i * 4 - i * (i - 1) / 2 + (j - i);
+}
+
+// Groups macros with bitwise-identical tables (translated copies, e.g. all
+// cubes of a Kuhn mesh share six geometries). Returns per-macro group id.
+std::vector<int> geometry_groups(const MacroMesh& mesh, const std::vector<int>& macros, int* num_groups);
+
+} // namespace tetmf
