@@ -1,0 +1,437 @@
+#!/usr/bin/env python
+"""bench.py -- GDoF/s per FP64 operator apply on B200 (BASELINE.json metric).
+
+Default workload (N=1): BASELINE config 5, the largest single-GPU config:
+alpha curl curl + beta (N1) on the 2x2x2 Kuhn cube mesh (48 macro-tets),
+L = 8, 941,884,928 edge DoFs, weak-scaled with N (48 macros per GPU:
+N=2 2x2x4, N=4 2x4x4, N=8 4x4x4 = 384 macros). The other configs
+(c1..c4) run with --config; c4 (P1 -Laplace, cube6 L8) is strong-scaled.
+
+A "step" = one operator apply y = A x (element kernel + interface sum +
+cross-rank exchange) over the whole mesh, inputs resident in HBM. Inputs of
+every config exceed L2 except c1-c3 (latency-bound parity configs), which
+flush L2 between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5]
+  python bench.py --impl reference ...   # the reference's CPU apply
+
+Timing: W untimed warm-up steps, then K steps bracketed by barrier +
+torch.cuda.synchronize(), CUDA events on the stream the kernels run on, max
+over ranks. e2e: the same metric through the public C-ABI drop-in
+(tetmf_apply_ref_host: host vectors in reference numbering, H2D + apply +
+D2H every step, pinned buffers) at N=1; per-rank upload/apply/download of
+the local storage for N>1.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GDoF/s per operator apply (FP64) at 1/2/4/8 B200; fraction of roofline"
+
+# F = flop per element of the cheapest exact formulation counted with
+# DFMA = 2; M = compulsory bytes per DoF.
+CONFIGS = {
+    "c1": dict(name="P1 -Laplace single-tet L6 (config 1)", mesh="single-tet", form="P1", level=6, dirichlet=True),
+    "c2": dict(name="P1 -div(k grad) single-tet L7 (config 2)", mesh="single-tet", form="P1K", level=7),
+    "c3": dict(name="N1 alpha curl curl + beta single-tet L6 (config 3)", mesh="single-tet", form="N1", level=6),
+    "c4": dict(name="P1 -Laplace cube6 L8 (config 4, strong scaling)", mesh="cube6", form="P1", level=8),
+    "c5": dict(name="N1 alpha curl curl + beta, 48 macros/GPU L8 (config 5, weak scaling)", mesh=None,
+               form="N1", level=8),
+}
+WEAK_MESH = {1: "cubes2x2x2", 2: "cubes2x2x4", 4: "cubes2x4x4", 8: "cubes4x4x4"}
+CPU_SAMPLE = {  # bounded sample of each workload for the CPU reference leg
+    "c1": ("single-tet", 6), "c2": ("single-tet", 6), "c3": ("single-tet", 5),
+    "c4": ("cube6", 6), "c5": ("cubes2x2x2", 4),
+}
+FLOP_PER_ELEM = {"P1": None, "P1K": None, "N1": 264.0}
+
+
+def lattice_counts(mesh_macros: int, level: int, form: str):
+    n = 1 << level
+    tet = lambda k: (k + 1) * (k + 2) * (k + 3) // 6 if k >= 0 else 0
+    return dict(elements=mesh_macros * n ** 3, p1_points=mesh_macros * tet(n),
+                nd1_edges=mesh_macros * (6 * tet(n - 1) + tet(n - 2)))
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([s.strip() for s in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ CPU legs
+def cpu_reference_sample(cfg_key: str, seconds: float = 12.0, verbatim: bool = True):
+    """Times the reference's own FormSystem::apply (oracle/_ref, compiled from
+    the reference sources) single-threaded on a bounded sample of the
+    workload. Returns (GDoF/s, sample description, dofs, seconds/apply)."""
+    from oracle.refapi import RefSystem
+    cfg = CONFIGS[cfg_key]
+    mesh, level = CPU_SAMPLE[cfg_key]
+    r = RefSystem(mesh, cfg["form"], level, fixed=not verbatim)
+    x = r.seeded_input(42)
+    c0, c1 = r.coefficients()
+    # same rule class as the GPU: exact, cheapest (P1: 2, N1: 3)
+    degree = 3 if cfg["form"] == "N1" else 2
+    r.apply(x, c0, c1, degree)  # warm-up fills the star / map caches
+    times = []
+    t_end = time.time() + seconds
+    while time.time() < t_end or len(times) < 3:
+        _, t = r.apply(x, c0, c1, degree)
+        times.append(t)
+    t = float(np.median(times))
+    return r.num_dofs / t / 1e9, f"{mesh} L{level} {cfg['form']} ({r.num_dofs} DoFs, degree-{degree} rule, " \
+                                 f"median of {len(times)} applies)", r.num_dofs, t
+
+
+def _replica(args):
+    cfg_key, seconds = args
+    g, _, dofs, t = cpu_reference_sample(cfg_key, seconds)
+    return dofs, t
+
+
+def run_reference_arm(a):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = CONFIGS[a.config]
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        pass
+    mesh, level = CPU_SAMPLE[a.config]
+    # the reference is single-threaded and not thread-safe (mutable caches,
+    # forms.hpp:86-87): one replica process per host core, aggregate DoF/s
+    nrep = max(1, min(cores, int(os.environ.get("TETMF_REF_REPLICAS", "64"))))
+    per_step = []
+    with mp.get_context("fork").Pool(nrep) as pool:
+        for _ in range(a.warmup):
+            pool.map(_replica, [(a.config, 0.0)] * nrep)
+        for _ in range(a.steps):
+            t0 = time.time()
+            res = pool.map(_replica, [(a.config, 0.0)] * nrep)
+            per_step.append(sum(d for d, _ in res) / max(t for _, t in res) / 1e9)
+    v = float(np.median(per_step))
+    sample = f"{nrep} concurrent single-thread replicas of the verbatim reference FormSystem::apply on " \
+             f"{mesh} L{level} {cfg['form']}"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GDoF/s", "n_gpus": ws, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "weak" if a.config == "c5" else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded uniform[-1,1] x, nodal coefficients)",
+        "config": {"workload": cfg["name"], "cpu_sample": f"{mesh} L{level}", "level": cfg["level"]},
+        "cpu_baseline": {"value": v, "unit": "GDoF/s", "cores": nrep, "kind": "reference", "sample": sample},
+        "e2e": {"value": v, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ------------------------------------------------------------------ GPU leg
+def run_gpu(a):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2404_08371_b200 as tm
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = dict(CONFIGS[a.config])
+    if cfg["mesh"] is None:
+        if ws not in WEAK_MESH:
+            raise SystemExit(f"config c5 supports 1/2/4/8 GPUs, got {ws}")
+        cfg["mesh"] = WEAK_MESH[ws]
+    level, form = cfg["level"], cfg["form"]
+    fid = {"P1": tm.FORM_P1, "P1K": tm.FORM_P1K, "N1": tm.FORM_N1}[form]
+    sid = tm.FORM_SPACE[fid]
+
+    nccl_id = None
+    if ws > 1:
+        obj = [tm.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    t_setup = time.time()
+    ctx = tm.Context(cfg["mesh"], device=local, rank=rank, nranks=ws, nccl_id=nccl_id)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    nmac_global, nmac_local = ctx.num_macros()
+    x, y = tm.Function(ctx, sid), tm.Function(ctx, sid)
+    coeffs = []
+    if form == "N1":
+        al, be = tm.Function(ctx, tm.SPACE_P1), tm.Function(ctx, tm.SPACE_P1)
+        al.fill_coefficient(level, tm.COEFF_ALPHA)
+        be.fill_coefficient(level, tm.COEFF_BETA)
+        coeffs = [al, be]
+    elif form == "P1K":
+        k = tm.Function(ctx, tm.SPACE_P1)
+        k.fill_coefficient(level, tm.COEFF_K)
+        coeffs = [k]
+    op = tm.Operator(ctx, fid, coeffs)
+    x.fill_seeded(level, 42, cfg.get("dirichlet", False))
+    y.size(level)
+    torch.cuda.synchronize()
+    t_setup = time.time() - t_setup
+
+    counts = lattice_counts(nmac_global, level, form)
+    n_unique = None
+    # unique DoFs of the whole mesh (reference numbering count)
+    if rank == 0 and ws == 1:
+        n_unique = x.num_ref_dofs(level)
+    if n_unique is None:
+        n_unique = unique_dofs(cfg["mesh"], form, level)
+
+    small = counts["elements"] < 50_000_000
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda") if small else None
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    for _ in range(a.warmup):
+        if flush is not None:
+            flush.zero_()
+        op.apply(x, y, level)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    lc0 = tm.launch_count()
+    op.profile(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    with ClockSampler(local) as clk:
+        for i in range(a.steps):
+            if flush is not None:
+                flush.zero_()  # L2 flush outside the timed interval of each step
+            ev[i][0].record(stream)
+            op.apply(x, y, level)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    launches = tm.launch_count() - lc0
+    kern_ms, kern_n = op.kernel_stats()
+    op.profile(False)
+    step_ms = [s.elapsed_time(e) for s, e in ev]
+    t_total = sum(step_ms)
+    if ws > 1:
+        tt = torch.tensor([t_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_total = float(tt.item())
+    ms_per_step = t_total / a.steps
+    value = n_unique / (ms_per_step * 1e-3) / 1e9
+
+    # ---------------- roofline of the dominant (element) kernel
+    kern_avg_ms = kern_ms / max(kern_n, 1)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    local_counts = lattice_counts(nmac_local, level, form)
+    if form == "N1":
+        nd1_local = local_counts["nd1_edges"]
+        p1_local = local_counts["p1_points"]
+        flops = FLOP_PER_ELEM["N1"] * local_counts["elements"]
+        fp64_peak = ctx.fp64_peak(1.0) if a.fp64_peak else None
+        bytes_alg = 8.0 * (2 * nd1_local + 2 * p1_local)
+        roof = {"bound": "fp64", "achieved": flops / (kern_avg_ms * 1e-3) / 1e12,
+                "peak": fp64_peak, "unit": "TFLOP/s", "traffic": None,
+                "frac": (flops / (kern_avg_ms * 1e-3) / 1e12) / fp64_peak if fp64_peak else None,
+                "flop_per_launch": flops, "flop_per_element": FLOP_PER_ELEM["N1"],
+                "peak_source": "measured FP64 DFMA-chain probe (tetmf_measure_fp64_peak) on this GPU",
+                "hbm": {"achieved": bytes_alg / (kern_avg_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                        "bytes_per_launch": bytes_alg}}
+    else:
+        p1_local = local_counts["p1_points"]
+        nbytes = 8.0 * p1_local * (3 if form == "P1K" else 2)
+        roof = {"bound": "hbm", "achieved": nbytes / (kern_avg_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                "frac": nbytes / (kern_avg_ms * 1e-3) / 1e9 / hbm_peak, "traffic": None,
+                "bytes_per_launch": nbytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+    roof["kernel_ms"] = kern_avg_ms
+    roof["kernel_share_of_step"] = kern_avg_ms / ms_per_step
+
+    # ---------------- end to end through the public API (host buffers)
+    e2e = None
+    if a.e2e:
+        e2e = run_e2e(a, tm, torch, dist, ctx, op, x, y, level, ws, rank, n_unique, barrier)
+
+    cpu = None
+    if rank == 0 and ws == 1 and a.cpu_baseline:
+        try:
+            g, sample, _, _ = cpu_reference_sample(a.config, seconds=a.cpu_seconds)
+            cpu = {"value": g, "unit": "GDoF/s", "cores": 1, "kind": "reference",
+                   "sample": "verbatim reference FormSystem::apply (oracle/_ref, -O3), 1 host core, " + sample}
+        except Exception as e:  # the reference lib is built here and ships with the snapshot
+            cpu = {"value": None, "unit": "GDoF/s", "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": ws, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak" if a.config == "c5" else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: x seeded uniform[-1,1] by canonical DoF key (SURVEY 8(d)); nodal P1 coefficients",
+            "config": {"workload": cfg["name"], "mesh": cfg["mesh"], "level": level, "form": form,
+                       "macros": nmac_global, "dofs": n_unique, "elements": counts["elements"],
+                       "parallelism": f"macro partition over {ws} GPU(s)",
+                       "l2": "inputs > 126 MB L2" if flush is None else "L2 flushed between steps",
+                       "setup_s": round(t_setup, 2)},
+            "roofline": roof, "clocks": clk.summary(), "gpu_launches": launches,
+            "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def unique_dofs(mesh: str, form: str, level: int) -> int:
+    """Unique DoFs of a Kuhn cube mesh / built-in mesh (closed forms,
+    SURVEY.md Appendix B): P1 (N+1)^3 vertices; ND1 7N^3 + 9N^2 + 3N edges."""
+    import re
+    n = 1 << level
+    if mesh == "single-tet":
+        tet = lambda k: (k + 1) * (k + 2) * (k + 3) // 6
+        return tet(n) if form != "N1" else 6 * tet(n - 1) + tet(n - 2)
+    m = re.fullmatch(r"cubes(\d+)x(\d+)x(\d+)", mesh) or re.fullmatch(r"cubes(\d+)", mesh)
+    k = [int(g) for g in m.groups()] if m else [1, 1, 1]
+    if len(k) == 1:
+        k = k * 3
+    N = [ki * n for ki in k]
+    if form != "N1":
+        return (N[0] + 1) * (N[1] + 1) * (N[2] + 1)
+    X, Y, Z = N
+    # edges: axis (3), face diagonals (3), body diagonal (1) of every cube
+    axis = X * (Y + 1) * (Z + 1) + (X + 1) * Y * (Z + 1) + (X + 1) * (Y + 1) * Z
+    faces = X * Y * (Z + 1) + X * (Y + 1) * Z + (X + 1) * Y * Z
+    return axis + faces + X * Y * Z
+
+
+def run_e2e(a, tm, torch, dist, ctx, op, x, y, level, ws, rank, n_unique, barrier):
+    steps = max(1, min(a.steps, a.e2e_steps))
+    if ws == 1:
+        nd = x.num_ref_dofs(level)
+        hv = tm.host_alloc(nd * 8)
+        hw = tm.host_alloc(nd * 8)
+        try:
+            # host input vector in reference numbering (the FieldVector a caller holds)
+            x.export_ref(level)  # builds the numbering maps (setup, untimed)
+            arr = np.ctypeslib.as_array((ctypes_double_p(hv)), shape=(nd,))
+            arr[:] = x.export_ref(level)
+            src, dst = tm.Function(ctx, x.space), tm.Function(ctx, x.space)
+            op.apply_ref_host(src, dst, level, hv, hw)  # warm-up
+            t = []
+            for _ in range(steps):
+                t0 = time.perf_counter()
+                op.apply_ref_host(src, dst, level, hv, hw)
+                t.append(time.perf_counter() - t0)
+            sec = float(np.median(t))
+            return {"value": n_unique / sec / 1e9, "unit": "GDoF/s", "h2d_bytes_per_step": nd * 8,
+                    "d2h_bytes_per_step": nd * 8, "ms_per_step": sec * 1e3, "steps": steps,
+                    "path": "tetmf_apply_ref_host: pinned host FieldVector (reference numbering) -> H2D -> "
+                            "permute -> apply -> permute -> D2H"}
+        finally:
+            tm.host_free(hv)
+            tm.host_free(hw)
+    n_loc = x.size(level)
+    host = np.zeros(n_loc)
+    x.download(level)
+    t = []
+    for _ in range(steps):
+        barrier()
+        t0 = time.perf_counter()
+        x.upload(level, host)
+        op.apply(x, y, level)
+        out = y.download(level)
+        t.append(time.perf_counter() - t0)
+    tt = torch.tensor([float(np.median(t))], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    sec = float(tt.item())
+    return {"value": n_unique / sec / 1e9, "unit": "GDoF/s", "h2d_bytes_per_step": n_loc * 8,
+            "d2h_bytes_per_step": out.size * 8, "ms_per_step": sec * 1e3, "steps": steps,
+            "path": "tetmf_fn_upload + tetmf_apply + tetmf_fn_download of the local storage per rank"}
+
+
+def ctypes_double_p(addr):
+    import ctypes
+    return ctypes.cast(ctypes.c_void_p(addr), ctypes.POINTER(ctypes.c_double))
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", choices=sorted(CONFIGS), default="c5")
+    p.add_argument("--no-e2e", dest="e2e", action="store_false")
+    p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--no-fp64-peak", dest="fp64_peak", action="store_false")
+    a = p.parse_args()
+    a.warmup = max(a.warmup, 3)
+    if a.impl == "reference":
+        run_reference_arm(a)
+    else:
+        run_gpu(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -111,6 +111,13 @@ int tetmf_apply(tetmf_op* op, const tetmf_fn* src, tetmf_fn* dst, int level, int
 int tetmf_apply_ref_host(tetmf_op* op, tetmf_fn* src, tetmf_fn* dst, int level, const double* host_v,
                          double* host_w);
 
+/* instrumentation: CUDA events around the element kernel of every apply on
+ * the context stream (enable resets the totals); stats synchronize. */
+int tetmf_op_profile(tetmf_op* op, int enable);
+int tetmf_op_kernel_stats(tetmf_op* op, double* total_ms, int64_t* launches);
+/* kernels launched by this library so far (process-wide) */
+int tetmf_launch_count(int64_t* count);
+
 /* pinned host memory for the end-to-end path */
 int tetmf_host_alloc(void** ptr, int64_t bytes);
 int tetmf_host_free(void* ptr);

@@ -92,7 +92,16 @@ _SIGS = {
     "tetmf_plan_local_matrix": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                _c_dp, _c_dp, _c_dp]),
     "tetmf_plan_stencil": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, _c_dp]),
+    "tetmf_op_profile": (ctypes.c_int, [_c_vp, ctypes.c_int]),
+    "tetmf_op_kernel_stats": (ctypes.c_int, [_c_vp, _c_dp, _c_i64p]),
+    "tetmf_launch_count": (ctypes.c_int, [_c_i64p]),
 }
+
+
+def launch_count() -> int:
+    n = ctypes.c_int64()
+    _check(lib().tetmf_launch_count(ctypes.byref(n)))
+    return n.value
 
 
 def lib() -> ctypes.CDLL:
@@ -333,8 +342,20 @@ class Operator:
     def apply(self, src: Function, dst: Function, level: int, update: int = REPLACE):
         _check(lib().tetmf_apply(self._h, src.handle, dst.handle, level, update))
 
-    def apply_ref_host(self, src: Function, dst: Function, level: int, v: np.ndarray, w: np.ndarray):
-        _check(lib().tetmf_apply_ref_host(self._h, src.handle, dst.handle, level, _dptr(v), _dptr(w)))
+    def apply_ref_host(self, src: Function, dst: Function, level: int, v, w):
+        """v, w: float64 numpy arrays or raw (pinned) host pointers (int)."""
+        pv = _dptr(v) if isinstance(v, np.ndarray) else ctypes.cast(_c_vp(v), _c_dp)
+        pw = _dptr(w) if isinstance(w, np.ndarray) else ctypes.cast(_c_vp(w), _c_dp)
+        _check(lib().tetmf_apply_ref_host(self._h, src.handle, dst.handle, level, pv, pw))
+
+    def profile(self, enable: bool = True):
+        _check(lib().tetmf_op_profile(self._h, int(enable)))
+
+    def kernel_stats(self):
+        ms = ctypes.c_double()
+        n = ctypes.c_int64()
+        _check(lib().tetmf_op_kernel_stats(self._h, ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
 
 
 def host_local_sum(offsets, copies, y):

@@ -284,14 +284,36 @@ int tetmf_apply_ref_host(tetmf_op* op, tetmf_fn* src, tetmf_fn* dst, int level, 
     if (c.nranks() > 1) fail_arg("apply_ref_host: single-rank contexts only");
     const i64 nd = s.num_ref_dofs(level);
     if (d.num_ref_dofs(level) != nd) fail_arg("apply_ref_host: src/dst space mismatch");
-    static thread_local DeviceBuffer<double> ref;
-    if (ref.size() < static_cast<std::size_t>(nd)) ref.reset(static_cast<std::size_t>(nd));
-    TETMF_CUDA(cudaMemcpyAsync(ref.get(), host_v, nd * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
-    s.import_ref_device(level, ref.get());
+    double* ref = op->impl->ref_scratch(nd);
+    TETMF_CUDA(cudaMemcpyAsync(ref, host_v, nd * sizeof(double), cudaMemcpyHostToDevice, c.stream()));
+    s.import_ref_device(level, ref);
     op->impl->apply(s, d, level, Update::Replace);
-    d.export_ref_device(level, ref.get());
-    TETMF_CUDA(cudaMemcpyAsync(host_w, ref.get(), nd * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
+    d.export_ref_device(level, ref);
+    TETMF_CUDA(cudaMemcpyAsync(host_w, ref, nd * sizeof(double), cudaMemcpyDeviceToHost, c.stream()));
     c.synchronize();
+  });
+}
+
+int tetmf_op_profile(tetmf_op* op, int enable) {
+  return guard([&] {
+    need(op, "op");
+    op->impl->set_profiling(enable != 0);
+  });
+}
+
+int tetmf_op_kernel_stats(tetmf_op* op, double* total_ms, int64_t* launches) {
+  return guard([&] {
+    need(op, "op");
+    i64 l = 0;
+    op->impl->kernel_stats(total_ms, &l);
+    if (launches) *launches = l;
+  });
+}
+
+int tetmf_launch_count(int64_t* count) {
+  return guard([&] {
+    need(count, "count");
+    *count = launch_count();
   });
 }
 

@@ -2,6 +2,7 @@
 #include "runtime.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 
 #include "common.hpp"
@@ -10,8 +11,11 @@
 
 namespace tetmf {
 
-void* nccl_comm_create(int nranks, const void* unique_id, int rank);  // exchange_nccl.cu
-void nccl_comm_destroy(void* comm);
+namespace {
+std::atomic<i64> g_launches{0};
+}
+void count_launch(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+i64 launch_count() { return g_launches.load(); }
 
 // ---------------------------------------------------------------- buffers
 template <typename T>
@@ -277,6 +281,18 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
   if (nm == 0) return;
   auto& t = tables(level);
   const cudaStream_t s = ctx_->stream();
+  cudaEvent_t ev_stop = nullptr;
+  if (profiling_) {
+    if (events_used_ == events_.size()) {
+      cudaEvent_t a, b;
+      TETMF_CUDA(cudaEventCreate(&a));
+      TETMF_CUDA(cudaEventCreate(&b));
+      events_.emplace_back(a, b);
+    }
+    TETMF_CUDA(cudaEventRecord(events_[events_used_].first, s));
+    ev_stop = events_[events_used_].second;
+    ++events_used_;
+  }
   switch (form_) {
     case Form::P1Diffusion:
       launch_p1_stencil(x, y, ld.macros.get(), nm, ld.lay.macro_stride, ld.lay.n, t.p1.get(), s);
@@ -294,8 +310,43 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
     default:
       fail_internal("kernel_apply: unsupported form");
   }
+  if (ev_stop) TETMF_CUDA(cudaEventRecord(ev_stop, s));
   launch_interface_sum(y, ld.group_offsets.get(), ld.group_copies.get(), ld.groups.num_groups(), s);
   if (ld.exchange) ld.exchange->run(y, s);
+}
+
+Operator::~Operator() {
+  for (auto& e : events_) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+}
+
+void Operator::set_profiling(bool on) {
+  if (on && !profiling_) {
+    prof_ms_ = 0.0;
+    prof_launches_ = 0;
+    events_used_ = 0;
+  }
+  profiling_ = on;
+}
+
+void Operator::kernel_stats(double* total_ms, i64* launches) {
+  for (std::size_t i = 0; i < events_used_; ++i) {
+    TETMF_CUDA(cudaEventSynchronize(events_[i].second));
+    float ms = 0.f;
+    TETMF_CUDA(cudaEventElapsedTime(&ms, events_[i].first, events_[i].second));
+    prof_ms_ += ms;
+    ++prof_launches_;
+  }
+  events_used_ = 0;
+  if (total_ms) *total_ms = prof_ms_;
+  if (launches) *launches = prof_launches_;
+}
+
+double* Operator::ref_scratch(i64 count) {
+  if (ref_scratch_.size() < static_cast<std::size_t>(count)) ref_scratch_.reset(static_cast<std::size_t>(count));
+  return ref_scratch_.get();
 }
 
 void Operator::apply(const Function& src, Function& dst, int level, Update upd) {

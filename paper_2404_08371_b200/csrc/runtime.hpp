@@ -148,6 +148,12 @@ public:
   const FormInfo& info() const { return form_info(form_); }
   void apply(const Function& src, Function& dst, int level, Update upd);
 
+  // bench instrumentation: CUDA events around the element kernel (K1-K3)
+  // on the context stream; stats() synchronizes and sums the durations.
+  void set_profiling(bool on);
+  void kernel_stats(double* total_ms, i64* launches);
+  double* ref_scratch(i64 count);  // device buffer for reference-numbered I/O
+
 private:
   struct LevelTables {
     DeviceBuffer<P1DeviceTable> p1;
@@ -162,7 +168,19 @@ private:
   std::vector<const Function*> coeffs_;
   std::map<int, std::unique_ptr<LevelTables>> tables_;
   std::map<int, DeviceBuffer<double>> scratch_;
+  DeviceBuffer<double> ref_scratch_;
+  bool profiling_ = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events_;
+  std::size_t events_used_ = 0;
+  double prof_ms_ = 0.0;
+  i64 prof_launches_ = 0;
+
+public:
+  ~Operator();
 };
+
+// number of kernels this library has launched (process-wide)
+i64 launch_count();
 
 // default contiguous partition of macro ids over ranks
 std::vector<int> partition_macros(int num_macros, int rank, int nranks);

@@ -12,7 +12,11 @@ namespace tetmf {
 inline void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
 }
-inline void check_launch(const char* kernel) { cuda_check(cudaGetLastError(), kernel); }
+void count_launch(int k);  // runtime.cpp: process-wide kernel launch counter
+inline void check_launch(const char* kernel) {
+  cuda_check(cudaGetLastError(), kernel);
+  count_launch(1);
+}
 
 } // namespace tetmf
 
