@@ -114,6 +114,8 @@ int tetmf_apply_ref_host(tetmf_op* op, tetmf_fn* src, tetmf_fn* dst, int level, 
 /* instrumentation: CUDA events around the element kernel of every apply on
  * the context stream (enable resets the totals); stats synchronize. */
 int tetmf_op_profile(tetmf_op* op, int enable);
+/* 0 = optimized kernels (default); 1 = first-version kernels (A/B tests) */
+int tetmf_op_set_variant(tetmf_op* op, int variant);
 int tetmf_op_kernel_stats(tetmf_op* op, double* total_ms, int64_t* launches);
 /* kernels launched by this library so far (process-wide) */
 int tetmf_launch_count(int64_t* count);

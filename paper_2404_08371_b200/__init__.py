@@ -93,6 +93,7 @@ _SIGS = {
                                                _c_dp, _c_dp, _c_dp]),
     "tetmf_plan_stencil": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, _c_dp]),
     "tetmf_op_profile": (ctypes.c_int, [_c_vp, ctypes.c_int]),
+    "tetmf_op_set_variant": (ctypes.c_int, [_c_vp, ctypes.c_int]),
     "tetmf_op_kernel_stats": (ctypes.c_int, [_c_vp, _c_dp, _c_i64p]),
     "tetmf_launch_count": (ctypes.c_int, [_c_i64p]),
 }
@@ -347,6 +348,10 @@ class Operator:
         pv = _dptr(v) if isinstance(v, np.ndarray) else ctypes.cast(_c_vp(v), _c_dp)
         pw = _dptr(w) if isinstance(w, np.ndarray) else ctypes.cast(_c_vp(w), _c_dp)
         _check(lib().tetmf_apply_ref_host(self._h, src.handle, dst.handle, level, pv, pw))
+
+    def set_variant(self, variant: int):
+        """0 = optimized kernels (default), 1 = first-version kernels."""
+        _check(lib().tetmf_op_set_variant(self._h, variant))
 
     def profile(self, enable: bool = True):
         _check(lib().tetmf_op_profile(self._h, int(enable)))

@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -43,6 +44,15 @@ void launch_axpy(double* y, const double* x, double a, i64 count, cudaStream_t s
 
 void launch_p1_stencil(const double* x, double* y, const MacroDesc* d_macros, int nmacros, i64 macro_stride,
                        int n, const P1DeviceTable* d_tables, cudaStream_t s);
+// K1 v2: warp-per-(macro, z, x-segment) row walk (k_p1_stencil.cu)
+void build_stencil_tasks(int nmacros, int n, std::vector<int>& out);
+void launch_p1_stencil_v2(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                          const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
+// K3 v2: cube walk, two layer-parity passes, one launch per geometry group
+void build_n1_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out);
+void launch_n1_cubes_v2(const N1DeviceTable* table, int pass, const double* x, const double* alpha,
+                        const double* beta, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
+                        i64 class_stride, i64 coeff_stride, int n, cudaStream_t s);
 void launch_p1k_cubes(const double* x, const double* k, double* y, const MacroDesc* d_macros, int nmacros,
                       i64 macro_stride, int n, const P1DeviceTable* d_tables, cudaStream_t s);
 void launch_n1_cubes(const double* x, const double* alpha, const double* beta, double* y,

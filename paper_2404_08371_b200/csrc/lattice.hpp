@@ -55,7 +55,7 @@ TM_HD i64 lattice_index(i64 n, i64 x, i64 y, i64 z) {
 
 // vertex offsets of the six orientations (mesh.cpp:22-29)
 
-TM_HD Off3 orient_offset(int o, int i) {
+TM_HD constexpr Off3 orient_offset(int o, int i) {
   // packed: per orientation 4 vertices, bits x|y<<1|z<<2
   // WU {0,e1,e2,e3}; WD {e12,e23,e13,e123}; BU {e1,e2,e3,e12};
   // BD {e2,e3,e12,e23}; GU {e1,e3,e12,e13}; GD {e3,e12,e23,e13}
@@ -70,7 +70,7 @@ constexpr int kEdgeDir[7][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}, {1, -1, 0},
                                 {1, 0, -1}, {0, 1, -1}, {1, 1, -1}};
 
 // device-usable accessors of the two tables above
-TM_HD int local_edge_vertex(int le, int k) {
+TM_HD constexpr int local_edge_vertex(int le, int k) {
   // a = {0,0,0,1,1,2}, b = {1,2,3,2,3,3}
   return k == 0 ? (le < 3 ? 0 : (le < 5 ? 1 : 2)) : (le == 0 ? 1 : (le == 1 || le == 3 ? 2 : 3));
 }
@@ -88,7 +88,7 @@ TM_HD Off3 edge_dir(int c) {
 
 // class of a lattice direction; *flipped = direction is -canonical.
 // returns -1 if not an edge direction (fespace.cpp:60-70)
-TM_HD int edge_class_of(int dx, int dy, int dz, bool* flipped) {
+TM_HD constexpr int edge_class_of(int dx, int dy, int dz, bool* flipped) {
   bool f = false;
   if (dx < 0 || (dx == 0 && dy < 0) || (dx == 0 && dy == 0 && dz < 0)) {
     dx = -dx; dy = -dy; dz = -dz; f = true;
@@ -120,12 +120,12 @@ struct LocalEdgeRef {
   bool flipped;
 };
 
-TM_HD LocalEdgeRef local_edge_ref(int o, int le) {
+TM_HD constexpr LocalEdgeRef local_edge_ref(int o, int le) {
   const Off3 pa = orient_offset(o, local_edge_vertex(le, 0));
   const Off3 pb = orient_offset(o, local_edge_vertex(le, 1));
   bool f = false;
   const int c = edge_class_of(pb.x - pa.x, pb.y - pa.y, pb.z - pa.z, &f);
-  LocalEdgeRef r;
+  LocalEdgeRef r{0, 0, 0, 0, false};
   r.ax = pa.x < pb.x ? pa.x : pb.x;
   r.ay = pa.y < pb.y ? pa.y : pb.y;
   r.az = pa.z < pb.z ? pa.z : pb.z;

@@ -130,6 +130,28 @@ Context::LevelData& Context::level(Space s, int level) {
     for (int m : macros_)
       if (rank_of[m] != rank_) fail_arg("context: multi-rank contexts use the default partition");
   }
+  if (s == Space::P1) {
+    std::vector<int> tasks;
+    build_stencil_tasks(static_cast<int>(macros_.size()), n, tasks);
+    ld->ntasks = static_cast<int>(tasks.size() / 4);
+    ld->tasks.upload(tasks.data(), tasks.size(), stream_);
+  } else {
+    std::vector<int> all, part;
+    ld->group_tasks.assign(ngroups_, {0, 0, 0, 0});
+    for (int g = 0; g < ngroups_; ++g) {
+      std::vector<int> members;
+      for (std::size_t li = 0; li < macros_.size(); ++li)
+        if (group_[li] == g) members.push_back(static_cast<int>(li));
+      for (int pass = 0; pass < 2; ++pass) {
+        build_n1_tasks(members, n, pass, part);
+        ld->group_tasks[g][2 * pass] = static_cast<int>(all.size() / 4);
+        ld->group_tasks[g][2 * pass + 1] = static_cast<int>(part.size() / 4);
+        all.insert(all.end(), part.begin(), part.end());
+      }
+    }
+    ld->ntasks = static_cast<int>(all.size() / 4);
+    ld->tasks.upload(all.data(), all.size(), stream_);
+  }
   ld->groups = local_groups_only(mesh_, topo_, ld->lay, rank_of, rank_);
   ld->group_offsets.upload(ld->groups.offsets.data(), ld->groups.offsets.size(), stream_);
   ld->group_copies.upload(ld->groups.copies.data(), ld->groups.copies.size(), stream_);
@@ -151,13 +173,21 @@ Context::LevelData& Context::ref_level(Space s, int level) {
 }
 
 // ---------------------------------------------------------------- function
+// Every level buffer carries zeroed guard regions of storage_guard(n)
+// doubles before and after the macro blocks: the stencil / cube kernels load
+// their register windows without bounds predicates (out-of-lattice values
+// only ever meet zero weights), so the windows may touch up to one row plus
+// one warp width outside the storage.
+i64 storage_guard(int n) { return round_up(static_cast<i64>(n) + 96, 32); }
+
 double* Function::data(int level) {
   auto it = data_.find(level);
-  if (it != data_.end()) return it->second.get();
+  if (it != data_.end()) return it->second.get() + storage_guard(1 << level);
   auto& ld = ctx_->level(space_, level);
-  DeviceBuffer<double> buf(static_cast<std::size_t>(ld.lay.total()));
-  if (buf.get()) TETMF_CUDA(cudaMemsetAsync(buf.get(), 0, buf.size() * sizeof(double), ctx_->stream()));
-  double* p = buf.get();
+  const i64 g = storage_guard(ld.lay.n);
+  DeviceBuffer<double> buf(static_cast<std::size_t>(ld.lay.total() + 2 * g));
+  TETMF_CUDA(cudaMemsetAsync(buf.get(), 0, buf.size() * sizeof(double), ctx_->stream()));
+  double* p = buf.get() + g;
   data_.emplace(level, std::move(buf));
   return p;
 }
@@ -165,7 +195,7 @@ double* Function::data(int level) {
 const double* Function::data(int level) const {
   auto it = data_.find(level);
   if (it == data_.end()) fail_arg("function has no data at level " + std::to_string(level));
-  return it->second.get();
+  return it->second.get() + storage_guard(1 << level);
 }
 
 i64 Function::size(int level) const { return ctx_->level(space_, level).lay.total(); }
@@ -249,6 +279,7 @@ Operator::LevelTables& Operator::tables(int level) {
         done[grp[li]] = true;
       }
     lt->n1.upload(t.data(), t.size(), ctx_->stream());
+    lt->n1_host = t;
   } else {
     std::vector<P1DeviceTable> t(ng);
     std::vector<bool> done(ng, false);
@@ -295,7 +326,11 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
   }
   switch (form_) {
     case Form::P1Diffusion:
-      launch_p1_stencil(x, y, ld.macros.get(), nm, ld.lay.macro_stride, ld.lay.n, t.p1.get(), s);
+      if (kernel_variant_ == 1)
+        launch_p1_stencil(x, y, ld.macros.get(), nm, ld.lay.macro_stride, ld.lay.n, t.p1.get(), s);
+      else
+        launch_p1_stencil_v2(x, y, ld.tasks.get(), ld.ntasks, ld.lay.macro_stride, ld.lay.n, t.p1.get(),
+                             ld.macros.get(), s);
       break;
     case Form::P1KDiffusion:
       launch_p1k_cubes(x, coeffs_[0]->data(level), y, ld.macros.get(), nm, ld.lay.macro_stride, ld.lay.n,
@@ -303,8 +338,18 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
       break;
     case Form::N1CurlCurlMass: {
       auto& cl = ctx_->level(Space::P1, level);
-      launch_n1_cubes(x, coeffs_[0]->data(level), coeffs_[1]->data(level), y, ld.macros.get(), nm,
-                      ld.lay.macro_stride, ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, t.n1.get(), s);
+      if (kernel_variant_ == 1) {
+        launch_n1_cubes(x, coeffs_[0]->data(level), coeffs_[1]->data(level), y, ld.macros.get(), nm,
+                        ld.lay.macro_stride, ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, t.n1.get(), s);
+      } else {
+        for (int pass = 0; pass < 2; ++pass)
+          for (std::size_t g = 0; g < ld.group_tasks.size(); ++g) {
+            const auto& gt = ld.group_tasks[g];
+            launch_n1_cubes_v2(t.n1.get() + g, pass, x, coeffs_[0]->data(level), coeffs_[1]->data(level), y,
+                               ld.tasks.get() + 4 * gt[2 * pass], gt[2 * pass + 1], ld.lay.macro_stride,
+                               ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, s);
+          }
+      }
       break;
     }
     default:
@@ -356,11 +401,14 @@ void Operator::apply(const Function& src, Function& dst, int level, Update upd) 
     kernel_apply(x, dst.data(level), level);
     return;
   }
+  const i64 g = storage_guard(1 << level);
   auto it = scratch_.find(level);
-  if (it == scratch_.end())
-    it = scratch_.emplace(level, DeviceBuffer<double>(static_cast<std::size_t>(dst.size(level)))).first;
-  kernel_apply(x, it->second.get(), level);
-  launch_axpy(dst.data(level), it->second.get(), 1.0, dst.size(level), ctx_->stream());
+  if (it == scratch_.end()) {
+    it = scratch_.emplace(level, DeviceBuffer<double>(static_cast<std::size_t>(dst.size(level) + 2 * g))).first;
+    TETMF_CUDA(cudaMemsetAsync(it->second.get(), 0, it->second.size() * sizeof(double), ctx_->stream()));
+  }
+  kernel_apply(x, it->second.get() + g, level);
+  launch_axpy(dst.data(level), it->second.get() + g, 1.0, dst.size(level), ctx_->stream());
 }
 
 } // namespace tetmf

@@ -97,6 +97,10 @@ public:
     std::unique_ptr<RefNumbering> ref;  // lazily, import/export only
     DeviceBuffer<i64> ref_map;
     std::unique_ptr<Exchange> exchange; // nranks > 1
+    DeviceBuffer<int> tasks;            // kernel task list (per space / level)
+    int ntasks = 0;
+    // ND1: task ranges (offset, count) per (geometry group, parity pass)
+    std::vector<std::array<int, 4>> group_tasks;  // {offset0, count0, offset1, count1}
   };
   LevelData& level(Space s, int level);
   LevelData& ref_level(Space s, int level);  // level() + reference numbering
@@ -153,11 +157,15 @@ public:
   void set_profiling(bool on);
   void kernel_stats(double* total_ms, i64* launches);
   double* ref_scratch(i64 count);  // device buffer for reference-numbered I/O
+  // 0 = optimized kernels (default), 1 = first-version kernels (k_apply_v1.cu),
+  // kept selectable for A/B parity tests and the bench's history
+  void set_kernel_variant(int v) { kernel_variant_ = v; }
 
 private:
   struct LevelTables {
     DeviceBuffer<P1DeviceTable> p1;
     DeviceBuffer<N1DeviceTable> n1;
+    std::vector<N1DeviceTable> n1_host;  // kernel-parameter copies (K3 v2)
   };
   LevelTables& tables(int level);
   void check(const Function& src, const Function& dst, int level) const;
@@ -170,6 +178,7 @@ private:
   std::map<int, DeviceBuffer<double>> scratch_;
   DeviceBuffer<double> ref_scratch_;
   bool profiling_ = false;
+  int kernel_variant_ = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events_;
   std::size_t events_used_ = 0;
   double prof_ms_ = 0.0;
@@ -181,6 +190,9 @@ public:
 
 // number of kernels this library has launched (process-wide)
 i64 launch_count();
+
+// zeroed guard entries before / after every level buffer (runtime.cpp)
+i64 storage_guard(int n);
 
 // default contiguous partition of macro ids over ranks
 std::vector<int> partition_macros(int num_macros, int rank, int nranks);

@@ -96,3 +96,32 @@ def test_config1_dirichlet(tm):
     w_gpu, x_gpu = gpu_apply(tm, "single-tet", "P1", 6, seed=42, dirichlet=True)
     assert np.array_equal(x_gpu, x_ref)
     assert relerr(w_gpu, w_ref) <= RTOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mesh,form,level", [("cube6", "P1", 7), ("single-tet", "P1", 8), ("cubes1x1x2", "P1", 5),
+                                             ("cube6", "N1", 6), ("single-tet", "N1", 7), ("cubes2", "N1", 4),
+                                             ("cube6", "P1K", 6), ("single-tet", "P1K", 8)])
+def test_optimized_vs_first_version(tm, mesh, form, level):
+    """A/B: optimized kernels (variant 0) vs the first-version kernels
+    (variant 1) on identical inputs at sizes beyond the oracle's reach."""
+    fid, sid = FORMS[form]
+    ctx = tm.Context(mesh, device=0)
+    x, y0, y1 = tm.Function(ctx, sid), tm.Function(ctx, sid), tm.Function(ctx, sid)
+    cf = []
+    if form == "N1":
+        a, b = tm.Function(ctx, tm.SPACE_P1), tm.Function(ctx, tm.SPACE_P1)
+        a.fill_coefficient(level, tm.COEFF_ALPHA)
+        b.fill_coefficient(level, tm.COEFF_BETA)
+        cf = [a, b]
+    elif form == "P1K":
+        k = tm.Function(ctx, tm.SPACE_P1)
+        k.fill_coefficient(level, tm.COEFF_K)
+        cf = [k]
+    op = tm.Operator(ctx, fid, cf)
+    x.fill_seeded(level, 3)
+    op.apply(x, y0, level)
+    op.set_variant(1)
+    op.apply(x, y1, level)
+    a, b = y0.download(level), y1.download(level)
+    assert np.abs(a - b).max() <= 1e-13 * np.abs(b).max()
