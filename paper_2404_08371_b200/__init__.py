@@ -21,7 +21,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libtetmf_b200.so")
+LIB_PATH = os.environ.get("TETMF_LIB") or os.path.join(_HERE, "_lib", "libtetmf_b200.so")
 
 SPACE_P1, SPACE_P2, SPACE_ND1 = 0, 1, 2
 FORM_P1, FORM_P2V, FORM_N1, FORM_P1K = 0, 1, 2, 3

@@ -50,7 +50,7 @@ void launch_p1_stencil_v2(const double* x, double* y, const int* d_tasks, int nt
                           const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
 // K3 v2: cube walk, two layer-parity passes, one launch per geometry group
 void build_n1_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out);
-void launch_n1_cubes_v2(const N1DeviceTable* table, int pass, const double* x, const double* alpha,
+void launch_n1_cubes_v2(const N1DeviceTable* table, const N1GramTable* gram, int pass, const double* x, const double* alpha,
                         const double* beta, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
                         i64 class_stride, i64 coeff_stride, int n, cudaStream_t s);
 void launch_p1k_cubes(const double* x, const double* k, double* y, const MacroDesc* d_macros, int nmacros,

@@ -30,6 +30,8 @@
 // table was tried first: ptxas hoisted the constants and spilled them.)
 // Window loads are unpredicated: level buffers carry zeroed guard regions and
 // values of non-existent edges only reach elements that are skipped.
+#include <cstdlib>
+
 #include "device.hpp"
 #include "runtime_check.hpp"
 
@@ -42,9 +44,18 @@ constexpr int kWarps = 4;
 #define TETMF_N1_MIN_BLOCKS 3  // 3 x 4 warps per SM -> <= 170 registers
 #endif
 constexpr int kMinBlocks = TETMF_N1_MIN_BLOCKS;
+constexpr int kChunk = 32;  // rows per task
+#ifndef TETMF_N1_PREFETCH
+#define TETMF_N1_PREFETCH 1
+#endif
+constexpr bool kPrefetch = TETMF_N1_PREFETCH != 0;
+
+__device__ __forceinline__ void prefetch_l1(const double* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 
 struct N1Task {
-  int macro, z, x0, pad;
+  int macro, z, x0, y0;
 };
 
 // per-orientation tables in shared memory: [o][term][22] (16-byte aligned
@@ -78,8 +89,8 @@ __host__ __device__ constexpr int cube_vertex(int o, int i) {
 }
 
 // one element: Y[cube edges] += A_e x_e
-template <int O>
-__device__ __forceinline__ void element(const SmemTable& tb, const double (&X)[19], const double (&al)[8],
+template <int O, typename TB>
+__device__ __forceinline__ void element(const TB& tb, const double (&X)[19], const double (&al)[8],
                                         const double (&be)[8], double (&Y)[19]) {
   constexpr int v0 = cube_vertex(O, 0), v1 = cube_vertex(O, 1), v2 = cube_vertex(O, 2), v3 = cube_vertex(O, 3);
   const double sa = (al[v0] + al[v1]) + (al[v2] + al[v3]);
@@ -112,14 +123,56 @@ __device__ __forceinline__ void element(const SmemTable& tb, const double (&X)[1
   for (int i = 0; i < 6; ++i) Y[cube_edge(O, i)] += ye[i];
 }
 
-template <int PASS>
+// Gram-form element (tables.hpp N1GramTable): 31 table values instead of 105
+template <int O>
+__device__ __forceinline__ void element_gram(const double* __restrict__ tb, const double (&X)[19],
+                                             const double (&al)[8], const double (&be)[8], double (&Y)[19]) {
+  constexpr int v0 = cube_vertex(O, 0), v1 = cube_vertex(O, 1), v2 = cube_vertex(O, 2), v3 = cube_vertex(O, 3);
+  const double sa = (al[v0] + al[v1]) + (al[v2] + al[v3]);
+  const double bv[4] = {be[v0], be[v1], be[v2], be[v3]};
+  const double S = (bv[0] + bv[1]) + (bv[2] + bv[3]);
+  const double S2 = S + S;
+  double Bt[4][4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const double u = S + bv[p];
+#pragma unroll
+    for (int q = p + 1; q < 4; ++q) Bt[p][q] = Bt[q][p] = u + bv[q];
+    Bt[p][p] = fma(4.0, bv[p], S2);
+  }
+  // A_e x_e accumulated straight into the cube accumulators Y
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+#pragma unroll
+    for (int j = i; j < 6; ++j) {
+      const int a = local_edge_vertex(i, 0), b = local_edge_vertex(i, 1);
+      const int c = local_edge_vertex(j, 0), d = local_edge_vertex(j, 1);
+      const bool neg = local_edge_ref(O, i).flipped != local_edge_ref(O, j).flipped;
+      double m = Bt[a][c] * tb[22 + sym4(b, d)];
+      m = fma(-Bt[a][d], tb[22 + sym4(b, c)], m);
+      m = fma(-Bt[b][c], tb[22 + sym4(a, d)], m);
+      m = fma(Bt[b][d], tb[22 + sym4(a, c)], m);
+      const double aij = fma(sa, tb[sym6(i, j)], neg ? -m : m);
+      Y[cube_edge(O, i)] = fma(aij, X[cube_edge(O, j)], Y[cube_edge(O, i)]);
+      if (j != i) Y[cube_edge(O, j)] = fma(aij, X[cube_edge(O, i)], Y[cube_edge(O, j)]);
+    }
+  }
+}
+
+template <int PASS, int MODE>
 __global__ void __launch_bounds__(32 * kWarps, kMinBlocks)
-n1_cubes_kernel(const N1DeviceTable* __restrict__ table, const double* __restrict__ xin,
+n1_cubes_kernel(const N1GramTable* __restrict__ gram, const N1DeviceTable* __restrict__ table,
+                const double* __restrict__ xin,
                 const double* __restrict__ alpha, const double* __restrict__ beta, double* __restrict__ yout,
                 const N1Task* __restrict__ tasks, int ntasks, i64 stride, i64 cstride, i64 cf_stride, int n) {
   __shared__ __align__(16) SmemTable st;
-  for (int i = threadIdx.x; i < 6 * 5 * 21; i += blockDim.x)
-    st.e[i / 105][(i / 21) % 5][i % 21] = __ldg(&table->e[0][0][0] + i);
+  __shared__ __align__(16) N1GramTable sg;
+  if (MODE == 0) {
+    for (int i = threadIdx.x; i < 6 * 5 * 21; i += blockDim.x)
+      st.e[i / 105][(i / 21) % 5][i % 21] = __ldg(&table->e[0][0][0] + i);
+  } else {
+    for (int i = threadIdx.x; i < 6 * 32; i += blockDim.x) sg.o[i / 32][i % 32] = __ldg(&gram->o[0][0] + i);
+  }
   __syncthreads();
   const int warp = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (warp >= ntasks) return;
@@ -135,27 +188,62 @@ n1_cubes_kernel(const N1DeviceTable* __restrict__ table, const double* __restric
   const double* __restrict__ B = beta + static_cast<i64>(t.macro) * cf_stride + cx;
   const int cs = static_cast<int>(cstride);
 
-  // row starts (offset of x = 0) of row y in the edge lattice (planes z, z+1)
-  // and in the vertex lattice (coefficients, planes z, z+1)
-  int ez = static_cast<int>(plane_offset(m, z));
-  int eu = static_cast<int>(plane_offset(m, z + 1));
-  int vz = static_cast<int>(plane_offset(n, z));
-  int vu = static_cast<int>(plane_offset(n, z + 1));
-  int elen = m - z + 1;      // edge-lattice row y length in plane z
-  int vlen = n - z + 1;      // vertex-lattice row y length in plane z
+  // The task covers rows [y0, y0 + kChunk) of the layer; a task with y0 > 0
+  // first recomputes cube row y0 - 1 (halo step, no stores) to obtain the
+  // partial sums its row-y0 owners receive from that row.
+  const int y0 = t.y0;
+  const int ys = y0 > 0 ? y0 - 1 : 0;
+  const int ymax = min(n - 1 - z - t.x0, y0 + kChunk - 1);  // lane 1 (x = x0) has a cube
+  // row starts (offset of x = 0) of row ys in the edge lattice (planes z,
+  // z+1) and in the vertex lattice (coefficients, planes z, z+1)
+  int ez = static_cast<int>(plane_offset(m, z) + row_offset(m, z, ys));
+  int eu = static_cast<int>(plane_offset(m, z + 1) + row_offset(m, z + 1, ys));
+  int vz = static_cast<int>(plane_offset(n, z) + row_offset(n, z, ys));
+  int vu = static_cast<int>(plane_offset(n, z + 1) + row_offset(n, z + 1, ys));
+  int elen = m - z + 1 - ys;  // edge-lattice row length in plane z
+  int vlen = n - z + 1 - ys;  // vertex-lattice row length in plane z
 
   // carried state: layer-z partial sums for row-y owners from cube row y-1
   // (the edge / coefficient windows are re-read each step; the values of
   // row y+1 are L1 hits by then and the kernel is FP64-bound)
   double c0 = 0.0, c2 = 0.0, c4 = 0.0, cT0 = 0.0;
 
-  const int ymax = n - 1 - z - t.x0;  // lane 1 (x = x0) has a cube while y <= ymax
-  for (int yy = 0; yy <= ymax; ++yy) {
+  for (int yy = ys; yy <= ymax; ++yy) {
     // keep the table reads inside the loop (no hoisting of 630 invariants
     // into registers): they are warp-uniform shared-memory broadcasts
     asm volatile("" ::: "memory");
     const int ez1 = ez + elen, eu1 = eu + elen - 1;   // edge rows y+1 (plane z), y+1 (plane z+1)
     const int vz1 = vz + vlen, vu1 = vu + vlen - 1;   // vertex rows y+1
+    if (kPrefetch && yy < ymax) {
+      // warm L1 with the rows the next step loads first (y+2 rows of planes
+      // z, z+1): no registers, no scoreboard, the lines land during this
+      // step's arithmetic
+      const int ez2 = ez1 + elen - 1, eu2 = eu1 + elen - 2;
+      const int vz2 = vz1 + vlen - 1, vu2 = vu1 + vlen - 2;
+      prefetch_l1(X + ez1);
+      prefetch_l1(X + cs + ez1);
+      prefetch_l1(X + 3 * cs + ez1);
+      prefetch_l1(X + 5 * cs + ez1);
+      prefetch_l1(X + 6 * cs + ez1);
+      prefetch_l1(X + ez2);
+      prefetch_l1(X + 2 * cs + ez2);
+      prefetch_l1(X + 4 * cs + ez2);
+      prefetch_l1(X + cs + eu1);
+      prefetch_l1(X + 3 * cs + eu1);
+      prefetch_l1(X + eu2);
+      prefetch_l1(A + vz2);
+      prefetch_l1(A + vu2);
+      prefetch_l1(B + vz2);
+      prefetch_l1(B + vu2);
+      if (PASS == 1) {  // the in-plane partial sums the next step updates
+        prefetch_l1(Yo + ez1);
+        prefetch_l1(Yo + cs + ez1);
+        prefetch_l1(Yo + 3 * cs + ez1);
+        prefetch_l1(Yo + eu1);
+        prefetch_l1(Yo + cs + eu1);
+        prefetch_l1(Yo + 3 * cs + eu1);
+      }
+    }
     double Xc[19];
     Xc[0] = __ldg(X + ez);
     Xc[1] = __ldg(X + cs + ez);
@@ -186,15 +274,40 @@ n1_cubes_kernel(const N1DeviceTable* __restrict__ table, const double* __restric
 #pragma unroll
     for (int k = 0; k < 19; ++k) Y[k] = 0.0;
     const int s = cx + yy + z;
-    if (cx >= 0) {
-      if (s <= n - 1) element<WU>(st, Xc, al, be, Y);
-      if (s <= n - 2) {
-        element<BU>(st, Xc, al, be, Y);
-        element<BD>(st, Xc, al, be, Y);
-        element<GU>(st, Xc, al, be, Y);
-        element<GD>(st, Xc, al, be, Y);
+    if (MODE == 1 && __all_sync(0xffffffffu, s <= n - 3)) {
+      // warp-uniform fast path: every lane holds a complete cube (lane 0 of
+      // an x0 = 0 task is the non-existent cube x = -1: computed on finite
+      // guard / neighbour values, its contributions are dropped below)
+      element_gram<WU>(sg.o[WU], Xc, al, be, Y);
+      element_gram<BU>(sg.o[BU], Xc, al, be, Y);
+      element_gram<BD>(sg.o[BD], Xc, al, be, Y);
+      element_gram<GU>(sg.o[GU], Xc, al, be, Y);
+      element_gram<GD>(sg.o[GD], Xc, al, be, Y);
+      element_gram<WD>(sg.o[WD], Xc, al, be, Y);
+      if (cx < 0) {
+#pragma unroll
+        for (int k = 0; k < 19; ++k) Y[k] = 0.0;
       }
-      if (s <= n - 3) element<WD>(st, Xc, al, be, Y);
+    } else if (cx >= 0) {
+      if (MODE == 0) {
+        if (s <= n - 1) element<WU>(st, Xc, al, be, Y);
+        if (s <= n - 2) {
+          element<BU>(st, Xc, al, be, Y);
+          element<BD>(st, Xc, al, be, Y);
+          element<GU>(st, Xc, al, be, Y);
+          element<GD>(st, Xc, al, be, Y);
+        }
+        if (s <= n - 3) element<WD>(st, Xc, al, be, Y);
+      } else {
+        if (s <= n - 1) element_gram<WU>(sg.o[WU], Xc, al, be, Y);
+        if (s <= n - 2) {
+          element_gram<BU>(sg.o[BU], Xc, al, be, Y);
+          element_gram<BD>(sg.o[BD], Xc, al, be, Y);
+          element_gram<GU>(sg.o[GU], Xc, al, be, Y);
+          element_gram<GD>(sg.o[GD], Xc, al, be, Y);
+        }
+        if (s <= n - 3) element_gram<WD>(sg.o[WD], Xc, al, be, Y);
+      }
     }
     // x+1 owners: from lane l to lane l+1
     double r7 = __shfl_up_sync(0xffffffffu, Y[7], 1);
@@ -205,7 +318,7 @@ n1_cubes_kernel(const N1DeviceTable* __restrict__ table, const double* __restric
     if (!owner) r7 = r8 = r9 = r13 = r17 = 0.0;
 
     // owners of row y: plane z (all classes) and plane z+1 (in-plane classes)
-    if (owner && s <= n - 1) {
+    if (owner && s <= n - 1 && yy >= y0) {
       double* __restrict__ yz = Yo + ez;
       yz[2 * cs] = Y[2] + c2 + r8;
       yz[4 * cs] = Y[4] + c4;
@@ -251,32 +364,44 @@ n1_cubes_kernel(const N1DeviceTable* __restrict__ table, const double* __restric
 
 } // namespace
 
-// Task lists of one level, per parity pass: (macro, z, x0) with x0 stepping
-// by 31 (lane 0 of every warp is a halo cube). Longest rows first.
+// Task lists of one level, per parity pass: (macro, z, x0, y0) with x0
+// stepping by 31 (lane 0 of every warp is a halo cube) and row chunks of
+// kChunk rows (bounded critical path: the longest task is kChunk + 1 steps).
 void build_n1_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out) {
   out.clear();
   for (int z = parity; z <= n - 1; z += 2)
     for (int x0 = 0; x0 <= n - 1 - z; x0 += 31)
-      for (int li : local_macros) {
-        out.push_back(li);
-        out.push_back(z);
-        out.push_back(x0);
-        out.push_back(0);
-      }
+      for (int y0 = 0; y0 <= n - 1 - z - x0; y0 += kChunk)
+        for (int li : local_macros) {
+          out.push_back(li);
+          out.push_back(z);
+          out.push_back(x0);
+          out.push_back(y0);
+        }
 }
 
-void launch_n1_cubes_v2(const N1DeviceTable* table, int pass, const double* x, const double* alpha,
-                        const double* beta, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
-                        i64 class_stride, i64 coeff_stride, int n, cudaStream_t s) {
+void launch_n1_cubes_v2(const N1DeviceTable* table, const N1GramTable* gram, int pass, const double* x,
+                        const double* alpha, const double* beta, double* y, const int* d_tasks, int ntasks,
+                        i64 macro_stride, i64 class_stride, i64 coeff_stride, int n, cudaStream_t s) {
   if (ntasks == 0) return;
   const unsigned grid = static_cast<unsigned>((ntasks + kWarps - 1) / kWarps);
   const auto* tk = reinterpret_cast<const N1Task*>(d_tasks);
-  if (pass == 0)
-    n1_cubes_kernel<0><<<grid, 32 * kWarps, 0, s>>>(table, x, alpha, beta, y, tk, ntasks, macro_stride, class_stride,
-                                                    coeff_stride, n);
+  // table form: 1 = Gram (default, 31 shared-memory values per element);
+  // 0 = assembled T tables (105 values per element; saturates L1 at 87%).
+  // A kernel-parameter constant-bank variant measured 3.3x slower (ptxas
+  // either hoists and spills the constants or emits an indexed LDC each).
+  static const int mode = [] {
+    const char* e = std::getenv("TETMF_N1_TABLE");
+    return e ? std::atoi(e) : 1;
+  }();
+  auto go = [&](auto kern) {
+    kern<<<grid, 32 * kWarps, 0, s>>>(gram, table, x, alpha, beta, y, tk, ntasks, macro_stride, class_stride,
+                                      coeff_stride, n);
+  };
+  if (mode == 1)
+    pass == 0 ? go(n1_cubes_kernel<0, 1>) : go(n1_cubes_kernel<1, 1>);
   else
-    n1_cubes_kernel<1><<<grid, 32 * kWarps, 0, s>>>(table, x, alpha, beta, y, tk, ntasks, macro_stride, class_stride,
-                                                    coeff_stride, n);
+    pass == 0 ? go(n1_cubes_kernel<0, 0>) : go(n1_cubes_kernel<1, 0>);
   check_launch("n1_cubes");
 }
 

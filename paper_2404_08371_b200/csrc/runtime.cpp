@@ -44,6 +44,7 @@ template class DeviceBuffer<i64>;
 template class DeviceBuffer<MacroDesc>;
 template class DeviceBuffer<P1DeviceTable>;
 template class DeviceBuffer<N1DeviceTable>;
+template class DeviceBuffer<N1GramTable>;
 
 // ---------------------------------------------------------------- forms
 const FormInfo& form_info(Form f) {
@@ -279,7 +280,14 @@ Operator::LevelTables& Operator::tables(int level) {
         done[grp[li]] = true;
       }
     lt->n1.upload(t.data(), t.size(), ctx_->stream());
-    lt->n1_host = t;
+    std::vector<N1GramTable> gt(ng);
+    std::fill(done.begin(), done.end(), false);
+    for (std::size_t li = 0; li < macros.size(); ++li)
+      if (!done[grp[li]]) {
+        gt[grp[li]] = n1_gram_table(ctx_->mesh(), macros[li], level);
+        done[grp[li]] = true;
+      }
+    lt->n1g.upload(gt.data(), gt.size(), ctx_->stream());
   } else {
     std::vector<P1DeviceTable> t(ng);
     std::vector<bool> done(ng, false);
@@ -345,7 +353,7 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
         for (int pass = 0; pass < 2; ++pass)
           for (std::size_t g = 0; g < ld.group_tasks.size(); ++g) {
             const auto& gt = ld.group_tasks[g];
-            launch_n1_cubes_v2(t.n1.get() + g, pass, x, coeffs_[0]->data(level), coeffs_[1]->data(level), y,
+            launch_n1_cubes_v2(t.n1.get() + g, t.n1g.get() + g, pass, x, coeffs_[0]->data(level), coeffs_[1]->data(level), y,
                                ld.tasks.get() + 4 * gt[2 * pass], gt[2 * pass + 1], ld.lay.macro_stride,
                                ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, s);
           }

@@ -165,7 +165,7 @@ private:
   struct LevelTables {
     DeviceBuffer<P1DeviceTable> p1;
     DeviceBuffer<N1DeviceTable> n1;
-    std::vector<N1DeviceTable> n1_host;  // kernel-parameter copies (K3 v2)
+    DeviceBuffer<N1GramTable> n1g;       // Gram form per geometry group (K3 v2)
   };
   LevelTables& tables(int level);
   void check(const Function& src, const Function& dst, int level) const;

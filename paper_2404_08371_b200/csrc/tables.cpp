@@ -177,6 +177,22 @@ N1DeviceTable pack_n1(const N1Tables& t) {
   return d;
 }
 
+N1GramTable n1_gram_table(const MacroMesh& mesh, int macro, int level) {
+  N1GramTable out;
+  std::memset(&out, 0, sizeof(out));
+  const N1Tables t = n1_tables(mesh, macro, level);
+  for (int o = 0; o < 6; ++o) {
+    for (int i = 0; i < 6; ++i)
+      for (int j = i; j < 6; ++j) out.o[o][sym6(i, j)] = t.Kc[o][i][j];
+    const OrientGeom g = orient_geometry(mesh, macro, level, o);
+    V3 G[4];
+    for (int i = 0; i < 4; ++i) G[i] = mat_vec(g.JinvT, kGradRef[i]);
+    for (int x = 0; x < 4; ++x)
+      for (int y = x; y < 4; ++y) out.o[o][22 + sym4(x, y)] = g.vol / 120.0 * dot(G[x], G[y]);
+  }
+  return out;
+}
+
 std::vector<int> geometry_groups(const MacroMesh& mesh, const std::vector<int>& macros, int* num_groups) {
   std::map<std::array<double, 9>, int> seen;
   std::vector<int> out;

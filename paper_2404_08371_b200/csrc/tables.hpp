@@ -68,6 +68,19 @@ struct N1DeviceTable {
 P1DeviceTable pack_p1(const P1Tables& t);
 N1DeviceTable pack_n1(const N1Tables& t);
 
+// Gram form of the N1 element matrix (K3): per orientation
+//   Kc[q]  = s_i s_j vol/4 curl_i . curl_j        (21 packed, + 1 pad)
+//   g[xy]  = vol/120 G_x . G_y, G = J^-T grad lambda (10 packed, sym4)
+// and for edges i = (a,b), j = (c,d), beta in P1, S = sum_m beta_m:
+//   int beta phi_i.phi_j = Bt_ac g_bd - Bt_ad g_bc - Bt_bc g_ad + Bt_bd g_ac
+//   Bt_pq = S + beta_p + beta_q (p != q),  Bt_pp = 2 S + 4 beta_p
+// (exact: int lambda_m lambda_p lambda_q = 6 vol a!b!c!d!/6!). The local
+// signs s_i s_j of the mass term are compile-time constants in the kernel.
+struct N1GramTable {
+  double o[6][32];  // [orientation][Kc 0..20, pad 21, g 22..31]
+};
+N1GramTable n1_gram_table(const MacroMesh& mesh, int macro, int level);
+
 // packed index of (i, j), i <= j < 6 (row-major upper triangle)
 TM_HD int sym6(int i, int j) {
   if (i > j) { const int t = i; i = j; j = t; }
