@@ -225,6 +225,8 @@ def run_gpu(a):
         k.fill_coefficient(level, tm.COEFF_K)
         coeffs = [k]
     op = tm.Operator(ctx, fid, coeffs)
+    if a.variant:
+        op.set_variant(a.variant)  # kernel A/B (0 = default optimized kernels)
     x.fill_seeded(level, 42, cfg.get("dirichlet", False))
     y.size(level)
     torch.cuda.synchronize()
@@ -425,6 +427,7 @@ def main():
     p.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-fp64-peak", dest="fp64_peak", action="store_false")
+    p.add_argument("--variant", type=int, default=0, help="kernel variant for A/B runs (0 = default)")
     a = p.parse_args()
     a.warmup = max(a.warmup, 3)
     if a.impl == "reference":

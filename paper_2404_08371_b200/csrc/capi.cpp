@@ -304,7 +304,7 @@ int tetmf_op_profile(tetmf_op* op, int enable) {
 int tetmf_op_set_variant(tetmf_op* op, int variant) {
   return guard([&] {
     need(op, "op");
-    if (variant < 0 || variant > 1) fail_arg("unknown kernel variant");
+    if (variant < 0 || variant > 4) fail_arg("unknown kernel variant");
     op->impl->set_kernel_variant(variant);
   });
 }

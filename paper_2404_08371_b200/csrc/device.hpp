@@ -48,6 +48,18 @@ void launch_p1_stencil(const double* x, double* y, const MacroDesc* d_macros, in
 void build_stencil_tasks(int nmacros, int n, std::vector<int>& out);
 void launch_p1_stencil_v2(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
                           const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
+// K1 default: two-plane row walk (k_p1_stencil2.cu)
+void build_stencil2_tasks(int nmacros, int n, std::vector<int>& out);
+void launch_p1_stencil2(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                        const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
+// K1 variant 4: 32 x 4 register tiles (k_p1_stencil_tile.cu)
+void build_stencil_tile_tasks(int nmacros, int n, std::vector<int>& out);
+void launch_p1_stencil_tile(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                            const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
+// K1 v3: TMA plane streaming (k_p1_stencil_tma.cu)
+void build_stencil_tma_tasks(int nmacros, int n, std::vector<int>& out);
+void launch_p1_stencil_tma(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                           const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
 // K3 v2: cube walk, two layer-parity passes, one launch per geometry group
 void build_n1_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out);
 void launch_n1_cubes_v2(const N1DeviceTable* table, const N1GramTable* gram, int pass, const double* x, const double* alpha,

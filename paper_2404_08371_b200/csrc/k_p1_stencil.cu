@@ -1,16 +1,19 @@
-// k_p1_stencil.cu -- K1: P1 -Laplace apply via the assembled 15-point stencil.
+// k_p1_stencil.cu -- K1: P1 -Laplace apply via the assembled 15-point stencil,
+// register-window row walk.
 //
-// Work decomposition: one warp per task (macro, plane z, 32-wide x segment
-// x0, row chunk [y0, y0+32)); lane = x. The warp walks the rows of its chunk.
-// All neighbours of the 15-point stencil lie in planes z-1, z, z+1 and rows
-// y-1..y+1, so a rolling register window keeps every value loaded once per
-// warp: per point 7 coalesced 8-byte loads (plane z: row y at x+1, row y+1
-// at x-1, x; plane z-1: row y+1 at x, x+1; plane z+1: row y at x-1, x),
-// 15 DFMA, 1 store. The loads of row y+1 are issued before the arithmetic of
-// row y (software pipelining), so every warp keeps a step of loads in flight.
-// HBM traffic per point is the compulsory 16 bytes (x read once, y written
-// once) while the three planes of a task stay L2-resident for the
-// neighbouring plane tasks, which are scheduled adjacently.
+// Work decomposition: one warp per task (macro, row chunk [y0, y0+kChunk),
+// 32-wide x segment x0, plane z); lane = x. The warp walks the rows of its
+// chunk. All neighbours of the 15-point stencil lie in planes z-1, z, z+1 and
+// rows y-1..y+1, so a rolling register window keeps every value loaded once
+// per warp: per point 7 coalesced 8-byte loads (plane z: row y at x+1, row
+// y+1 at x-1, x; plane z-1: row y+1 at x, x+1; plane z+1: row y at x-1, x),
+// 15 DFMA, 1 store. The chunk loop is fully unrolled (static register
+// renaming, no rotation copies) and branch-free.
+//
+// Task order puts z innermost: the four warps of a CTA compute the same
+// (x0, y0) tile of four consecutive planes, so the planes they share (each
+// plane is read by the tasks of planes z-1, z and z+1) are served from L1
+// instead of three separate L2 reads.
 //
 // No bounds predicates on the window loads: the level buffers carry zeroed
 // guard regions (runtime.cpp storage_guard) and every out-of-lattice value a
@@ -27,7 +30,7 @@ namespace tetmf {
 namespace {
 
 constexpr int kWarps = 4;
-constexpr int kChunk = 32;  // rows per task
+constexpr int kChunk = 8;  // rows per task
 
 struct StencilTask {
   int macro, z, x0, y0;
@@ -51,7 +54,6 @@ p1_stencil_kernel(const double* __restrict__ xin, double* __restrict__ yout, con
 #pragma unroll
   for (int k = 0; k < 15; ++k) w[k] = __ldg(tab + k);
 
-  const int y1 = min(n - z - x0, y0 + kChunk - 1);  // last row with a point in lane 0
   // row starts (offset of x = 0) of row y0 in planes z, z-1, z+1; a missing
   // plane aliases plane z (its weights are zero)
   int rz = static_cast<int>(plane_offset(n, z) + row_offset(n, z, y0));
@@ -59,51 +61,29 @@ p1_stencil_kernel(const double* __restrict__ xin, double* __restrict__ yout, con
   int ru = z < n ? static_cast<int>(plane_offset(n, z + 1) + row_offset(n, z + 1, y0)) : rz;
   const int dl = z > 0 ? 1 : 0;   // row-length delta of plane z-1 vs z
   const int du = z < n ? -1 : 0;  // and of plane z+1
+  int lenz = n - z - y0 + 1;      // length of row y in plane z
 
   // window at row y0: rows y0-1 may lie in the front guard (zero weights)
-  const int rzm = rz - (n - z - y0 + 2);
-  const int rum = ru - (n - z - y0 + 1 + du + 1);
+  const int rzm = rz - (lenz + 1);
+  const int rum = ru - (lenz + du + 1);
   double Zm0 = __ldg(X + rzm), Zm1 = __ldg(X + rzm + 1);
   double Umm = __ldg(X + rum - 1), Um0 = __ldg(X + rum);
   double Z0m = __ldg(X + rz - 1), Z00 = __ldg(X + rz);
   double L00 = __ldg(X + rl), L01 = __ldg(X + rl + 1);
+  const bool face_free = z > 0 && x0 > 0;  // rows y >= 1 of this warp avoid x=0, z=0
 
-  // step loads (row y: Z01, U0m, U00; row y+1: Zpm, Zp0, Lp0, Lp1), kept
-  // two row steps ahead of the arithmetic
-  int lenz = n - z - y0 + 1;  // length of row y in plane z
-  double nZ01 = __ldg(X + rz + 1);
-  double nZpm = __ldg(X + rz + lenz - 1), nZp0 = __ldg(X + rz + lenz);
-  double nLp0 = __ldg(X + rl + lenz + dl), nLp1 = __ldg(X + rl + lenz + dl + 1);
-  double nU0m = __ldg(X + ru - 1), nU00 = __ldg(X + ru);
-  int pz = rz + lenz, pl = rl + lenz + dl, pu = ru + lenz + du, plen = lenz - 1;  // row y0+1
-  double mZ01 = __ldg(X + pz + 1);
-  double mZpm = __ldg(X + pz + plen - 1), mZp0 = __ldg(X + pz + plen);
-  double mLp0 = __ldg(X + pl + plen + dl), mLp1 = __ldg(X + pl + plen + dl + 1);
-  double mU0m = __ldg(X + pu - 1), mU00 = __ldg(X + pu);
-
-#pragma unroll 2
-  for (int yy = y0; yy <= y1; ++yy) {
-    const double Z01 = nZ01, Zpm = nZpm, Zp0 = nZp0, Lp0 = nLp0, Lp1 = nLp1, U0m = nU0m, U00 = nU00;
-    nZ01 = mZ01; nZpm = mZpm; nZp0 = mZp0; nLp0 = mLp0; nLp1 = mLp1; nU0m = mU0m; nU00 = mU00;
-    // prefetch row step yy+2 (rows past the plane land in valid storage)
-    pz += plen;
-    pl += plen + dl;
-    pu += plen + du;
-    --plen;
-    mZ01 = __ldg(X + pz + 1);
-    mZpm = __ldg(X + pz + plen - 1);
-    mZp0 = __ldg(X + pz + plen);
-    mLp0 = __ldg(X + pl + plen + dl);
-    mLp1 = __ldg(X + pl + plen + dl + 1);
-    mU0m = __ldg(X + pu - 1);
-    mU00 = __ldg(X + pu);
-    const int rz1 = rz + lenz, rl1 = rl + lenz + dl, ru1 = ru + lenz + du;
-    const int lenz1 = lenz - 1;
+#pragma unroll
+  for (int r = 0; r < kChunk; ++r) {
+    const int yy = y0 + r;
+    const int rz1 = rz + lenz, rl1 = rl + lenz + dl;
+    const double Z01 = __ldg(X + rz + 1);
+    const double Zpm = __ldg(X + rz1 - 1), Zp0 = __ldg(X + rz1);
+    const double Lp0 = __ldg(X + rl1), Lp1 = __ldg(X + rl1 + 1);
+    const double U0m = __ldg(X + ru - 1), U00 = __ldg(X + ru);
     double acc;
-    // warp-uniform: no lane of this step on a macro face (x=0, y=0, z=0 or
+    // warp-uniform: no lane of this row on a macro face (x=0, y=0, z=0 or
     // x+y+z=n) -> every lane is an interior point
-    if (z > 0 && yy > 0 && x0 > 0 && x0 + 31 + yy + z < n) {
-      // four independent partial sums (no 15-deep DFMA dependency chain)
+    if (face_free && yy > 0 && x0 + 31 + yy + z < n) {
       double a0 = w[0] * Z00, a1 = w[1] * Z01, a2 = w[2] * Z0m, a3 = w[3] * Zp0;
       a0 = fma(w[4], Zm0, a0);
       a1 = fma(w[5], U00, a1);
@@ -117,29 +97,28 @@ p1_stencil_kernel(const double* __restrict__ xin, double* __restrict__ yout, con
       a1 = fma(w[13], Lp1, a1);
       a2 = fma(w[14], Umm, a2);
       acc = (a0 + a1) + (a2 + a3);
-      Y[rz] = acc;
+      if (yy <= n - z) Y[rz] = acc;
     } else {
       const int s = px + yy + z;
       const int type = (px == 0 ? 1 : 0) | (yy == 0 ? 2 : 0) | (z == 0 ? 4 : 0) | (s == n ? 8 : 0);
       const double* __restrict__ wt = tab + 16 * type;
-      acc = __ldg(wt + 0) * Z00;
-      acc = fma(__ldg(wt + 1), Z01, acc);
-      acc = fma(__ldg(wt + 2), Z0m, acc);
-      acc = fma(__ldg(wt + 3), Zp0, acc);
-      acc = fma(__ldg(wt + 4), Zm0, acc);
-      acc = fma(__ldg(wt + 5), U00, acc);
-      acc = fma(__ldg(wt + 6), L00, acc);
-      acc = fma(__ldg(wt + 7), Zm1, acc);
-      acc = fma(__ldg(wt + 8), Zpm, acc);
-      acc = fma(__ldg(wt + 9), L01, acc);
-      acc = fma(__ldg(wt + 10), U0m, acc);
-      acc = fma(__ldg(wt + 11), Lp0, acc);
-      acc = fma(__ldg(wt + 12), Um0, acc);
-      acc = fma(__ldg(wt + 13), Lp1, acc);
-      acc = fma(__ldg(wt + 14), Umm, acc);
+      double a0 = __ldg(wt + 0) * Z00, a1 = __ldg(wt + 1) * Z01, a2 = __ldg(wt + 2) * Z0m,
+             a3 = __ldg(wt + 3) * Zp0;
+      a0 = fma(__ldg(wt + 4), Zm0, a0);
+      a1 = fma(__ldg(wt + 5), U00, a1);
+      a2 = fma(__ldg(wt + 6), L00, a2);
+      a3 = fma(__ldg(wt + 7), Zm1, a3);
+      a0 = fma(__ldg(wt + 8), Zpm, a0);
+      a1 = fma(__ldg(wt + 9), L01, a1);
+      a2 = fma(__ldg(wt + 10), U0m, a2);
+      a3 = fma(__ldg(wt + 11), Lp0, a3);
+      a0 = fma(__ldg(wt + 12), Um0, a0);
+      a1 = fma(__ldg(wt + 13), Lp1, a1);
+      a2 = fma(__ldg(wt + 14), Umm, a2);
+      acc = (a0 + a1) + (a2 + a3);
       if (s <= n) Y[rz] = acc;
     }
-    // rotate the window to row y+1
+    // slide the window to row y+1 (static renaming after unrolling)
     Zm0 = Z00;
     Zm1 = Z01;
     Z0m = Zpm;
@@ -148,23 +127,23 @@ p1_stencil_kernel(const double* __restrict__ xin, double* __restrict__ yout, con
     L01 = Lp1;
     Umm = U0m;
     Um0 = U00;
+    ru += lenz + du;
     rz = rz1;
     rl = rl1;
-    ru = ru1;
-    lenz = lenz1;
+    --lenz;
   }
 }
 
 } // namespace
 
-// Task list of one level: (macro, z, x0, y0) for every plane, 32-wide x
-// segment and chunk of <= kChunk rows.
+// Task list of one level: (macro, z, x0, y0) for every row chunk, 32-wide x
+// segment and plane, z innermost (L1 sharing of adjacent planes in a CTA).
 void build_stencil_tasks(int nmacros, int n, std::vector<int>& out) {
   out.clear();
   for (int li = 0; li < nmacros; ++li)
-    for (int z = 0; z <= n; ++z)
-      for (int x0 = 0; x0 <= n - z; x0 += 32)
-        for (int y0 = 0; y0 <= n - z - x0; y0 += kChunk) {
+    for (int y0 = 0; y0 <= n; y0 += kChunk)
+      for (int x0 = 0; x0 <= n - y0; x0 += 32)
+        for (int z = 0; z <= n - y0 - x0; ++z) {
           out.push_back(li);
           out.push_back(z);
           out.push_back(x0);

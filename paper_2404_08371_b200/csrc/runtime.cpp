@@ -133,9 +133,18 @@ Context::LevelData& Context::level(Space s, int level) {
   }
   if (s == Space::P1) {
     std::vector<int> tasks;
-    build_stencil_tasks(static_cast<int>(macros_.size()), n, tasks);
+    build_stencil2_tasks(static_cast<int>(macros_.size()), n, tasks);
     ld->ntasks = static_cast<int>(tasks.size() / 4);
     ld->tasks.upload(tasks.data(), tasks.size(), stream_);
+    build_stencil_tile_tasks(static_cast<int>(macros_.size()), n, tasks);
+    ld->ntasks4 = static_cast<int>(tasks.size() / 4);
+    ld->tasks4.upload(tasks.data(), tasks.size(), stream_);
+    build_stencil_tma_tasks(static_cast<int>(macros_.size()), n, tasks);
+    ld->ntasks3 = static_cast<int>(tasks.size() / 4);
+    ld->tasks3.upload(tasks.data(), tasks.size(), stream_);
+    build_stencil_tasks(static_cast<int>(macros_.size()), n, tasks);
+    ld->ntasks2 = static_cast<int>(tasks.size() / 4);
+    ld->tasks2.upload(tasks.data(), tasks.size(), stream_);
   } else {
     std::vector<int> all, part;
     ld->group_tasks.assign(ngroups_, {0, 0, 0, 0});
@@ -336,9 +345,18 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
     case Form::P1Diffusion:
       if (kernel_variant_ == 1)
         launch_p1_stencil(x, y, ld.macros.get(), nm, ld.lay.macro_stride, ld.lay.n, t.p1.get(), s);
-      else
-        launch_p1_stencil_v2(x, y, ld.tasks.get(), ld.ntasks, ld.lay.macro_stride, ld.lay.n, t.p1.get(),
+      else if (kernel_variant_ == 2)
+        launch_p1_stencil_v2(x, y, ld.tasks2.get(), ld.ntasks2, ld.lay.macro_stride, ld.lay.n, t.p1.get(),
                              ld.macros.get(), s);
+      else if (kernel_variant_ == 3)
+        launch_p1_stencil_tma(x, y, ld.tasks3.get(), ld.ntasks3, ld.lay.macro_stride, ld.lay.n, t.p1.get(),
+                              ld.macros.get(), s);
+      else if (kernel_variant_ == 4)
+        launch_p1_stencil_tile(x, y, ld.tasks4.get(), ld.ntasks4, ld.lay.macro_stride, ld.lay.n, t.p1.get(),
+                               ld.macros.get(), s);
+      else
+        launch_p1_stencil2(x, y, ld.tasks.get(), ld.ntasks, ld.lay.macro_stride, ld.lay.n, t.p1.get(),
+                           ld.macros.get(), s);
       break;
     case Form::P1KDiffusion:
       launch_p1k_cubes(x, coeffs_[0]->data(level), y, ld.macros.get(), nm, ld.lay.macro_stride, ld.lay.n,

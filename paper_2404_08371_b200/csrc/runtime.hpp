@@ -99,6 +99,12 @@ public:
     std::unique_ptr<Exchange> exchange; // nranks > 1
     DeviceBuffer<int> tasks;            // kernel task list (per space / level)
     int ntasks = 0;
+    DeviceBuffer<int> tasks2;           // P1: row-walk stencil tasks (variant 2)
+    int ntasks2 = 0;
+    DeviceBuffer<int> tasks3;           // P1: TMA plane-streaming tasks (variant 3)
+    int ntasks3 = 0;
+    DeviceBuffer<int> tasks4;           // P1: register-tile tasks (variant 4)
+    int ntasks4 = 0;
     // ND1: task ranges (offset, count) per (geometry group, parity pass)
     std::vector<std::array<int, 4>> group_tasks;  // {offset0, count0, offset1, count1}
   };
