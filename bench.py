@@ -121,10 +121,18 @@ def cpu_reference_sample(cfg_key: str, seconds: float = 12.0, verbatim: bool = T
     """Times the reference's own FormSystem::apply (oracle/_ref, compiled from
     the reference sources) single-threaded on a bounded sample of the
     workload. Returns (GDoF/s, sample description, dofs, seconds/apply)."""
-    from oracle.refapi import RefSystem
+    import tempfile
+
+    from oracle.refapi import RefSystem, write_kuhn_mesh
     cfg = CONFIGS[cfg_key]
     mesh, level = CPU_SAMPLE[cfg_key]
-    r = RefSystem(mesh, cfg["form"], level, fixed=not verbatim)
+    mesh_arg = mesh
+    if mesh.startswith("cubes"):  # the reference loads K^3 Kuhn meshes from its text format
+        k = [int(v) for v in mesh[5:].split("x")]
+        k = k * 3 if len(k) == 1 else k
+        mesh_arg = os.path.join(tempfile.gettempdir(), f"tetmf_{mesh}.mesh")
+        write_kuhn_mesh(mesh_arg, *k)
+    r = RefSystem(mesh_arg, cfg["form"], level, fixed=not verbatim)
     x = r.seeded_input(42)
     c0, c1 = r.coefficients()
     # same rule class as the GPU: exact, cheapest (P1: 2, N1: 3)

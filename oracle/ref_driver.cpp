@@ -57,6 +57,7 @@ double k_fn(const tetmf::Vec3& p) {
 
 } // namespace
 
+#pragma GCC visibility push(default)
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
@@ -284,3 +285,4 @@ int ref_quadrature(int degree, double* pts, double* wts, int cap) {
 }
 
 } // extern "C"
+#pragma GCC visibility pop
