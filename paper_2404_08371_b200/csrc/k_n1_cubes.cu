@@ -44,7 +44,10 @@ constexpr int kWarps = 4;
 #define TETMF_N1_MIN_BLOCKS 3  // 3 x 4 warps per SM -> <= 170 registers
 #endif
 constexpr int kMinBlocks = TETMF_N1_MIN_BLOCKS;
-constexpr int kChunk = 32;  // rows per task
+#ifndef TETMF_N1_CHUNK
+#define TETMF_N1_CHUNK 32
+#endif
+constexpr int kChunk = TETMF_N1_CHUNK;  // rows per task
 #ifndef TETMF_N1_PREFETCH
 #define TETMF_N1_PREFETCH 1
 #endif
@@ -126,10 +129,12 @@ __device__ __forceinline__ void element(const TB& tb, const double (&X)[19], con
 // Gram-form element (tables.hpp N1GramTable): 31 table values instead of 105
 template <int O>
 __device__ __forceinline__ void element_gram(const double* __restrict__ tb, const double (&X)[19],
-                                             const double (&al)[8], const double (&be)[8], double (&Y)[19]) {
+                                             const double (&al)[8], const double (&be)[8], double (&Y)[19],
+                                             bool valid) {
   constexpr int v0 = cube_vertex(O, 0), v1 = cube_vertex(O, 1), v2 = cube_vertex(O, 2), v3 = cube_vertex(O, 3);
-  const double sa = (al[v0] + al[v1]) + (al[v2] + al[v3]);
-  const double bv[4] = {be[v0], be[v1], be[v2], be[v3]};
+  // invalid element: all coefficients 0 -> A_e = 0 (inputs are finite)
+  const double sa = valid ? (al[v0] + al[v1]) + (al[v2] + al[v3]) : 0.0;
+  const double bv[4] = {valid ? be[v0] : 0.0, valid ? be[v1] : 0.0, valid ? be[v2] : 0.0, valid ? be[v3] : 0.0};
   const double S = (bv[0] + bv[1]) + (bv[2] + bv[3]);
   const double S2 = S + S;
   double Bt[4][4];
@@ -274,20 +279,18 @@ n1_cubes_kernel(const N1GramTable* __restrict__ gram, const N1DeviceTable* __res
 #pragma unroll
     for (int k = 0; k < 19; ++k) Y[k] = 0.0;
     const int s = cx + yy + z;
-    if (MODE == 1 && __all_sync(0xffffffffu, s <= n - 3)) {
-      // warp-uniform fast path: every lane holds a complete cube (lane 0 of
-      // an x0 = 0 task is the non-existent cube x = -1: computed on finite
-      // guard / neighbour values, its contributions are dropped below)
-      element_gram<WU>(sg.o[WU], Xc, al, be, Y);
-      element_gram<BU>(sg.o[BU], Xc, al, be, Y);
-      element_gram<BD>(sg.o[BD], Xc, al, be, Y);
-      element_gram<GU>(sg.o[GU], Xc, al, be, Y);
-      element_gram<GD>(sg.o[GD], Xc, al, be, Y);
-      element_gram<WD>(sg.o[WD], Xc, al, be, Y);
-      if (cx < 0) {
-#pragma unroll
-        for (int k = 0; k < 19; ++k) Y[k] = 0.0;
-      }
+    if (MODE == 1) {
+      // one branch-free path: an element outside the macro (partial cubes at
+      // the row end, the halo cube x = -1 of an x0 = 0 task) gets zero
+      // coefficients, so its (finite, guard-region) inputs contribute 0
+      const bool in = cx >= 0;
+      const bool vWU = in && s <= n - 1, vMid = in && s <= n - 2, vWD = in && s <= n - 3;
+      element_gram<WU>(sg.o[WU], Xc, al, be, Y, vWU);
+      element_gram<BU>(sg.o[BU], Xc, al, be, Y, vMid);
+      element_gram<BD>(sg.o[BD], Xc, al, be, Y, vMid);
+      element_gram<GU>(sg.o[GU], Xc, al, be, Y, vMid);
+      element_gram<GD>(sg.o[GD], Xc, al, be, Y, vMid);
+      element_gram<WD>(sg.o[WD], Xc, al, be, Y, vWD);
     } else if (cx >= 0) {
       if (MODE == 0) {
         if (s <= n - 1) element<WU>(st, Xc, al, be, Y);
@@ -298,15 +301,6 @@ n1_cubes_kernel(const N1GramTable* __restrict__ gram, const N1DeviceTable* __res
           element<GD>(st, Xc, al, be, Y);
         }
         if (s <= n - 3) element<WD>(st, Xc, al, be, Y);
-      } else {
-        if (s <= n - 1) element_gram<WU>(sg.o[WU], Xc, al, be, Y);
-        if (s <= n - 2) {
-          element_gram<BU>(sg.o[BU], Xc, al, be, Y);
-          element_gram<BD>(sg.o[BD], Xc, al, be, Y);
-          element_gram<GU>(sg.o[GU], Xc, al, be, Y);
-          element_gram<GD>(sg.o[GD], Xc, al, be, Y);
-        }
-        if (s <= n - 3) element_gram<WD>(sg.o[WD], Xc, al, be, Y);
       }
     }
     // x+1 owners: from lane l to lane l+1
