@@ -33,11 +33,14 @@
 #include <cstdlib>
 
 #include "device.hpp"
+#include "n1_common.cuh"
 #include "runtime_check.hpp"
 
 namespace tetmf {
 
 namespace {
+
+using namespace n1;
 
 constexpr int kWarps = 4;
 #ifndef TETMF_N1_MIN_BLOCKS
@@ -53,10 +56,6 @@ constexpr int kChunk = TETMF_N1_CHUNK;  // rows per task
 #endif
 constexpr bool kPrefetch = TETMF_N1_PREFETCH != 0;
 
-__device__ __forceinline__ void prefetch_l1(const double* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
-
 struct N1Task {
   int macro, z, x0, y0;
 };
@@ -66,30 +65,6 @@ struct N1Task {
 struct SmemTable {
   double e[6][5][22];
 };
-
-// cube edge numbering: (owner offset, class)
-//  0..6: (000, c)   7: (100,1)  8: (100,2)  9: (100,5)
-// 10: (010,0) 11: (010,2) 12: (010,4) 13: (110,2)
-// 14: (001,0) 15: (001,1) 16: (001,3) 17: (101,1) 18: (011,0)
-__host__ __device__ constexpr int cube_edge_id(int ox, int oy, int oz, int c) {
-  return (ox == 0 && oy == 0 && oz == 0) ? c
-         : (ox == 1 && oy == 0 && oz == 0) ? (c == 1 ? 7 : c == 2 ? 8 : 9)
-         : (ox == 0 && oy == 1 && oz == 0) ? (c == 0 ? 10 : c == 2 ? 11 : 12)
-         : (ox == 1 && oy == 1 && oz == 0) ? 13
-         : (ox == 0 && oy == 0 && oz == 1) ? (c == 0 ? 14 : c == 1 ? 15 : 16)
-         : (ox == 1 && oy == 0 && oz == 1) ? 17
-                                           : 18;
-}
-
-__host__ __device__ constexpr int cube_edge(int o, int le) {
-  // local edge (a,b) of orientation o -> cube edge id (lattice.hpp conventions)
-  return cube_edge_id(local_edge_ref(o, le).ax, local_edge_ref(o, le).ay, local_edge_ref(o, le).az,
-                      local_edge_ref(o, le).cls);
-}
-
-__host__ __device__ constexpr int cube_vertex(int o, int i) {
-  return orient_offset(o, i).x + 2 * orient_offset(o, i).y + 4 * orient_offset(o, i).z;
-}
 
 // one element: Y[cube edges] += A_e x_e
 template <int O, typename TB>
@@ -126,43 +101,16 @@ __device__ __forceinline__ void element(const TB& tb, const double (&X)[19], con
   for (int i = 0; i < 6; ++i) Y[cube_edge(O, i)] += ye[i];
 }
 
-// Gram-form element (tables.hpp N1GramTable): 31 table values instead of 105
-template <int O>
-__device__ __forceinline__ void element_gram(const double* __restrict__ tb, const double (&X)[19],
-                                             const double (&al)[8], const double (&be)[8], double (&Y)[19],
-                                             bool valid) {
-  constexpr int v0 = cube_vertex(O, 0), v1 = cube_vertex(O, 1), v2 = cube_vertex(O, 2), v3 = cube_vertex(O, 3);
-  // invalid element: all coefficients 0 -> A_e = 0 (inputs are finite)
-  const double sa = valid ? (al[v0] + al[v1]) + (al[v2] + al[v3]) : 0.0;
-  const double bv[4] = {valid ? be[v0] : 0.0, valid ? be[v1] : 0.0, valid ? be[v2] : 0.0, valid ? be[v3] : 0.0};
-  const double S = (bv[0] + bv[1]) + (bv[2] + bv[3]);
-  const double S2 = S + S;
-  double Bt[4][4];
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const double u = S + bv[p];
-#pragma unroll
-    for (int q = p + 1; q < 4; ++q) Bt[p][q] = Bt[q][p] = u + bv[q];
-    Bt[p][p] = fma(4.0, bv[p], S2);
-  }
-  // A_e x_e accumulated straight into the cube accumulators Y
-#pragma unroll
-  for (int i = 0; i < 6; ++i) {
-#pragma unroll
-    for (int j = i; j < 6; ++j) {
-      const int a = local_edge_vertex(i, 0), b = local_edge_vertex(i, 1);
-      const int c = local_edge_vertex(j, 0), d = local_edge_vertex(j, 1);
-      const bool neg = local_edge_ref(O, i).flipped != local_edge_ref(O, j).flipped;
-      double m = Bt[a][c] * tb[22 + sym4(b, d)];
-      m = fma(-Bt[a][d], tb[22 + sym4(b, c)], m);
-      m = fma(-Bt[b][c], tb[22 + sym4(a, d)], m);
-      m = fma(Bt[b][d], tb[22 + sym4(a, c)], m);
-      const double aij = fma(sa, tb[sym6(i, j)], neg ? -m : m);
-      Y[cube_edge(O, i)] = fma(aij, X[cube_edge(O, j)], Y[cube_edge(O, i)]);
-      if (j != i) Y[cube_edge(O, j)] = fma(aij, X[cube_edge(O, i)], Y[cube_edge(O, j)]);
-    }
-  }
-}
+// MODE 1 input accessor: the cube's inputs loaded into registers
+struct RegIn {
+  const double (&X)[19];
+  const double (&al)[8];
+  const double (&be)[8];
+  template <int K>
+  __device__ __forceinline__ double x() const { return X[K]; }
+  template <int V, int W>
+  __device__ __forceinline__ double c() const { return W ? be[V] : al[V]; }
+};
 
 template <int PASS, int MODE>
 __global__ void __launch_bounds__(32 * kWarps, kMinBlocks)
@@ -285,12 +233,7 @@ n1_cubes_kernel(const N1GramTable* __restrict__ gram, const N1DeviceTable* __res
       // coefficients, so its (finite, guard-region) inputs contribute 0
       const bool in = cx >= 0;
       const bool vWU = in && s <= n - 1, vMid = in && s <= n - 2, vWD = in && s <= n - 3;
-      element_gram<WU>(sg.o[WU], Xc, al, be, Y, vWU);
-      element_gram<BU>(sg.o[BU], Xc, al, be, Y, vMid);
-      element_gram<BD>(sg.o[BD], Xc, al, be, Y, vMid);
-      element_gram<GU>(sg.o[GU], Xc, al, be, Y, vMid);
-      element_gram<GD>(sg.o[GD], Xc, al, be, Y, vMid);
-      element_gram<WD>(sg.o[WD], Xc, al, be, Y, vWD);
+      cube_elements(SmemTabs{sg}, RegIn{Xc, al, be}, Y, vWU, vMid, vWD);
     } else if (cx >= 0) {
       if (MODE == 0) {
         if (s <= n - 1) element<WU>(st, Xc, al, be, Y);
@@ -356,12 +299,215 @@ n1_cubes_kernel(const N1GramTable* __restrict__ gram, const N1DeviceTable* __res
   }
 }
 
+// ---------------------------------------------------------------------------
+// MODE 2: shared-memory row ring. Same tasks, traversal, element formula and
+// write-back as n1_cubes_kernel<PASS, 1>; only the input path differs. Each
+// warp keeps the rows y, y+1, y+2 of the 14 input arrays it reads
+//   0..6  X plane z, classes 0..6        7..9  X plane z+1, classes 0, 1, 3
+//   10/11 alpha planes z / z+1           12/13 beta planes z / z+1
+// in a 3-slot ring (33 values per row: the warp's 32 columns + 1). At step y
+// the warp issues cp.async copies of row y+2 and waits for row y+1: no global
+// load latency on the arithmetic path, and the element code reads its inputs
+// from shared memory where it uses them (lower register pressure -> 4 CTAs
+// per SM). Only rows <= ymax + 1 are copied -- the rows MODE 1 reads -- so
+// every address is one MODE 1 reads and the results are bit-identical.
+constexpr int kRingArrays = 14;
+constexpr int kRingRow = 34;                            // doubles per ring row
+constexpr int kRingSlot = kRingArrays * kRingRow;       // one row of all arrays
+constexpr int kRingWarp = 3 * kRingSlot;                // doubles per warp
+#ifndef TETMF_N1R_MIN_BLOCKS
+#define TETMF_N1R_MIN_BLOCKS 3  // 168 registers, no spills (4 -> 128 + spills: slower)
+#endif
+
+// ring position (array, row +0/+1, column +0/+1) of cube edge k
+__host__ __device__ constexpr int ring_edge_array(int k) {
+  return k <= 6 ? k : k == 7 ? 1 : k == 8 ? 2 : k == 9 ? 5 : k == 10 ? 0 : k == 11 ? 2 : k == 12 ? 4
+       : k == 13 ? 2 : k == 14 ? 7 : k == 15 ? 8 : k == 16 ? 9 : k == 17 ? 8 : 7;
+}
+__host__ __device__ constexpr int ring_edge_row(int k) { return (k >= 10 && k <= 13) || k == 18 ? 1 : 0; }
+__host__ __device__ constexpr int ring_edge_col(int k) {
+  return k == 7 || k == 8 || k == 9 || k == 13 || k == 17 ? 1 : 0;
+}
+
+// MODE 2 input accessor: rows y (r0) and y+1 (r1) of the warp's ring
+struct RingIn {
+  const double* r0;
+  const double* r1;
+  template <int K>
+  __device__ __forceinline__ double x() const {
+    return lds((ring_edge_row(K) ? r1 : r0) + ring_edge_array(K) * kRingRow + ring_edge_col(K));
+  }
+  // coefficient at cube vertex v (bit 0 x, bit 1 y, bit 2 z); W 0 alpha, 1 beta
+  template <int V, int W>
+  __device__ __forceinline__ double c() const {
+    return lds((((V >> 1) & 1) ? r1 : r0) + (10 + 2 * W + (V >> 2)) * kRingRow + (V & 1));
+  }
+};
+
+template <int PASS>
+__global__ void __launch_bounds__(32 * kWarps, TETMF_N1R_MIN_BLOCKS)
+n1_ring_kernel(const N1GramTable* __restrict__ gram, const double* __restrict__ xin,
+               const double* __restrict__ alpha, const double* __restrict__ beta, double* __restrict__ yout,
+               const N1Task* __restrict__ tasks, int ntasks, i64 stride, i64 cstride, i64 cf_stride, int n) {
+  extern __shared__ __align__(16) double dsm[];
+  N1GramTable& sg = *reinterpret_cast<N1GramTable*>(dsm);
+  for (int i = threadIdx.x; i < 6 * 32; i += blockDim.x) sg.o[i / 32][i % 32] = __ldg(&gram->o[0][0] + i);
+  __syncthreads();
+  const int warp = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (warp >= ntasks) return;
+  const int lane = threadIdx.x & 31;
+  double* ring = dsm + sizeof(N1GramTable) / sizeof(double) + (threadIdx.x >> 5) * kRingWarp;
+  const N1Task t = tasks[warp];
+  const int z = t.z;
+  const int cx = t.x0 - 1 + lane;
+  const bool owner = lane > 0;
+  const int m = n - 1;
+  const double* __restrict__ X = xin + static_cast<i64>(t.macro) * stride + cx;
+  double* __restrict__ Yo = yout + static_cast<i64>(t.macro) * stride + cx;
+  const double* __restrict__ A = alpha + static_cast<i64>(t.macro) * cf_stride + cx;
+  const double* __restrict__ B = beta + static_cast<i64>(t.macro) * cf_stride + cx;
+  const int cs = static_cast<int>(cstride);
+
+  const int y0 = t.y0;
+  const int ys = y0 > 0 ? y0 - 1 : 0;
+  const int ymax = min(n - 1 - z - t.x0, y0 + kChunk - 1);
+  int ez = static_cast<int>(plane_offset(m, z) + row_offset(m, z, ys));
+  int eu = static_cast<int>(plane_offset(m, z + 1) + row_offset(m, z + 1, ys));
+  int elen = m - z + 1 - ys;
+
+  // copy cursor: row rc of every array into ring slot rc % 3
+  int rc = ys, cslot = 0;
+  int cez = ez, ceu = eu, celen = elen;
+  int cvz = static_cast<int>(plane_offset(n, z) + row_offset(n, z, ys));
+  int cvu = static_cast<int>(plane_offset(n, z + 1) + row_offset(n, z + 1, ys));
+  int cvlen = n - z + 1 - ys;
+  auto copy_row = [&]() {
+    double* d = ring + cslot * kRingSlot + lane;
+#pragma unroll
+    for (int c = 0; c < 7; ++c) cp_async8(d + c * kRingRow, X + c * cs + cez);
+    cp_async8(d + 7 * kRingRow, X + ceu);
+    cp_async8(d + 8 * kRingRow, X + cs + ceu);
+    cp_async8(d + 9 * kRingRow, X + 3 * cs + ceu);
+    cp_async8(d + 10 * kRingRow, A + cvz);
+    cp_async8(d + 11 * kRingRow, A + cvu);
+    cp_async8(d + 12 * kRingRow, B + cvz);
+    cp_async8(d + 13 * kRingRow, B + cvu);
+    if (lane == 31) {  // column +1 of the arrays read at x+1
+      cp_async8(d + 1 * kRingRow + 1, X + cs + cez + 1);
+      cp_async8(d + 2 * kRingRow + 1, X + 2 * cs + cez + 1);
+      cp_async8(d + 5 * kRingRow + 1, X + 5 * cs + cez + 1);
+      cp_async8(d + 8 * kRingRow + 1, X + cs + ceu + 1);
+      cp_async8(d + 10 * kRingRow + 1, A + cvz + 1);
+      cp_async8(d + 11 * kRingRow + 1, A + cvu + 1);
+      cp_async8(d + 12 * kRingRow + 1, B + cvz + 1);
+      cp_async8(d + 13 * kRingRow + 1, B + cvu + 1);
+    }
+    ++rc;
+    cslot = cslot == 2 ? 0 : cslot + 1;
+    cez += celen;
+    ceu += celen - 1;
+    cvz += cvlen;
+    cvu += cvlen - 1;
+    --celen;
+    --cvlen;
+  };
+  copy_row();  // row ys
+  cp_async_commit();
+  copy_row();  // row ys + 1 (<= ymax + 1)
+  cp_async_commit();
+
+  double c0 = 0.0, c2 = 0.0, c4 = 0.0, cT0 = 0.0;
+  int sy = 0;  // ring slot of row yy
+  for (int yy = ys; yy <= ymax; ++yy) {
+    asm volatile("" ::: "memory");
+    if (rc <= ymax + 1) copy_row();  // row yy + 2
+    cp_async_commit();
+    if (PASS == 1 && yy < ymax) {  // the in-plane partial sums the next step updates
+      const int ez1 = ez + elen, eu1 = eu + elen - 1;
+      prefetch_l1(Yo + ez1);
+      prefetch_l1(Yo + cs + ez1);
+      prefetch_l1(Yo + 3 * cs + ez1);
+      prefetch_l1(Yo + eu1);
+      prefetch_l1(Yo + cs + eu1);
+      prefetch_l1(Yo + 3 * cs + eu1);
+    }
+    cp_async_wait1();  // rows yy, yy + 1 have landed (this lane's copies)
+    __syncwarp();      // ... and every lane's
+    const double* r0 = ring + sy * kRingSlot + lane;
+    const double* r1 = ring + (sy == 2 ? 0 : sy + 1) * kRingSlot + lane;
+
+    double Y[19];
+#pragma unroll
+    for (int k = 0; k < 19; ++k) Y[k] = 0.0;
+    const int s = cx + yy + z;
+    const bool in = cx >= 0;
+    const bool vWU = in && s <= n - 1, vMid = in && s <= n - 2, vWD = in && s <= n - 3;
+    cube_elements(SmemTabs{sg}, RingIn{r0, r1}, Y, vWU, vMid, vWD);
+    __syncwarp();  // ring slot sy is refilled by the next step's copies
+
+    double r7 = __shfl_up_sync(0xffffffffu, Y[7], 1);
+    double r8 = __shfl_up_sync(0xffffffffu, Y[8], 1);
+    double r9 = __shfl_up_sync(0xffffffffu, Y[9], 1);
+    double r13 = __shfl_up_sync(0xffffffffu, Y[13], 1);
+    double r17 = __shfl_up_sync(0xffffffffu, Y[17], 1);
+    if (!owner) r7 = r8 = r9 = r13 = r17 = 0.0;
+
+    if (owner && s <= n - 1 && yy >= y0) {
+      double* __restrict__ yz = Yo + ez;
+      yz[2 * cs] = Y[2] + c2 + r8;
+      yz[4 * cs] = Y[4] + c4;
+      yz[5 * cs] = Y[5] + r9;
+      if (s <= n - 2) yz[6 * cs] = Y[6];
+      const double f0 = Y[0] + c0, f1 = Y[1] + r7, f3 = Y[3];
+      if (PASS == 0) {
+        yz[0] = f0;
+        yz[cs] = f1;
+        yz[3 * cs] = f3;
+      } else {
+        yz[0] += f0;
+        yz[cs] += f1;
+        yz[3 * cs] += f3;
+      }
+      if (s <= n - 2) {
+        double* __restrict__ yu = Yo + eu;
+        const double g0 = Y[14] + cT0, g1 = Y[15] + r17, g3 = Y[16];
+        if (PASS == 0) {
+          yu[0] = g0;
+          yu[cs] = g1;
+          yu[3 * cs] = g3;
+        } else {
+          yu[0] += g0;
+          yu[cs] += g1;
+          yu[3 * cs] += g3;
+        }
+      }
+    }
+    c0 = Y[10];
+    c2 = Y[11] + r13;
+    c4 = Y[12];
+    cT0 = Y[18];
+    ez += elen;
+    eu += elen - 1;
+    --elen;
+    sy = sy == 2 ? 0 : sy + 1;
+  }
+}
+
 } // namespace
 
 // Task lists of one level, per parity pass: (macro, z, x0, y0) with x0
 // stepping by 31 (lane 0 of every warp is a halo cube) and row chunks of
 // kChunk rows (bounded critical path: the longest task is kChunk + 1 steps).
+int n1_kernel_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("TETMF_N1_TABLE");
+    return e ? std::atoi(e) : 3;
+  }();
+  return mode;
+}
+
 void build_n1_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out) {
+  if (n1_kernel_mode() == 3) return build_n1_fold_tasks(local_macros, n, parity, out);
   out.clear();
   for (int z = parity; z <= n - 1; z += 2)
     for (int x0 = 0; x0 <= n - 1 - z; x0 += 31)
@@ -384,15 +530,26 @@ void launch_n1_cubes_v2(const N1DeviceTable* table, const N1GramTable* gram, int
   // 0 = assembled T tables (105 values per element; saturates L1 at 87%).
   // A kernel-parameter constant-bank variant measured 3.3x slower (ptxas
   // either hoists and spills the constants or emits an indexed LDC each).
-  static const int mode = [] {
-    const char* e = std::getenv("TETMF_N1_TABLE");
-    return e ? std::atoi(e) : 1;
-  }();
+  const int mode = n1_kernel_mode();
+  if (mode == 3)
+    return launch_n1_fold(gram, pass, x, alpha, beta, y, d_tasks, ntasks, macro_stride, class_stride, coeff_stride,
+                          n, s);
   auto go = [&](auto kern) {
     kern<<<grid, 32 * kWarps, 0, s>>>(gram, table, x, alpha, beta, y, tk, ntasks, macro_stride, class_stride,
                                       coeff_stride, n);
   };
-  if (mode == 1)
+  if (mode == 2) {
+    constexpr int smem = static_cast<int>(sizeof(N1GramTable) + sizeof(double) * kRingWarp * kWarps);
+    static const bool attr = [] {
+      cudaFuncSetAttribute(n1_ring_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(n1_ring_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      return true;
+    }();
+    (void)attr;
+    auto kern = pass == 0 ? n1_ring_kernel<0> : n1_ring_kernel<1>;
+    kern<<<grid, 32 * kWarps, smem, s>>>(gram, x, alpha, beta, y, tk, ntasks, macro_stride, class_stride,
+                                         coeff_stride, n);
+  } else if (mode == 1)
     pass == 0 ? go(n1_cubes_kernel<0, 1>) : go(n1_cubes_kernel<1, 1>);
   else
     pass == 0 ? go(n1_cubes_kernel<0, 0>) : go(n1_cubes_kernel<1, 0>);

@@ -1,0 +1,147 @@
+// n1_common.cuh -- pieces shared by the N1 cube kernels (k_n1_cubes.cu,
+// k_n1_fold.cu): cube edge / vertex numbering, the Gram-form element, and the
+// cp.async / shared-memory helpers of the staged input paths.
+#pragma once
+
+#include "device.hpp"
+
+namespace tetmf {
+namespace n1 {
+
+// cube edge numbering: (owner offset, class)
+//  0..6: (000, c)   7: (100,1)  8: (100,2)  9: (100,5)
+// 10: (010,0) 11: (010,2) 12: (010,4) 13: (110,2)
+// 14: (001,0) 15: (001,1) 16: (001,3) 17: (101,1) 18: (011,0)
+__host__ __device__ constexpr int cube_edge_id(int ox, int oy, int oz, int c) {
+  return (ox == 0 && oy == 0 && oz == 0) ? c
+         : (ox == 1 && oy == 0 && oz == 0) ? (c == 1 ? 7 : c == 2 ? 8 : 9)
+         : (ox == 0 && oy == 1 && oz == 0) ? (c == 0 ? 10 : c == 2 ? 11 : 12)
+         : (ox == 1 && oy == 1 && oz == 0) ? 13
+         : (ox == 0 && oy == 0 && oz == 1) ? (c == 0 ? 14 : c == 1 ? 15 : 16)
+         : (ox == 1 && oy == 0 && oz == 1) ? 17
+                                           : 18;
+}
+
+__host__ __device__ constexpr int cube_edge(int o, int le) {
+  // local edge (a,b) of orientation o -> cube edge id (lattice.hpp conventions)
+  return cube_edge_id(local_edge_ref(o, le).ax, local_edge_ref(o, le).ay, local_edge_ref(o, le).az,
+                      local_edge_ref(o, le).cls);
+}
+
+__host__ __device__ constexpr int cube_vertex(int o, int i) {
+  return orient_offset(o, i).x + 2 * orient_offset(o, i).y + 4 * orient_offset(o, i).z;
+}
+
+__device__ __forceinline__ void prefetch_l1(const double* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// volatile shared load: not CSE'd across elements, so values are re-read
+// where used instead of being held in registers for the whole step
+__device__ __forceinline__ double lds(const double* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))));
+  return v;
+}
+
+// (i, j) of the P-th packed upper-triangle entry of a symmetric 6x6
+__host__ __device__ constexpr int pair_i(int p) { return p < 6 ? 0 : p < 11 ? 1 : p < 15 ? 2 : p < 18 ? 3 : p < 20 ? 4 : 5; }
+__host__ __device__ constexpr int pair_j(int p) {
+  return p < 6 ? p : p < 11 ? p - 5 : p < 15 ? p - 9 : p < 18 ? p - 12 : p < 20 ? p - 14 : 5;
+}
+
+// Gram table of one orientation in shared memory (tables.hpp N1GramTable row)
+struct SmemTab {
+  const double* p;
+  template <int I>
+  __device__ __forceinline__ double get() const { return p[I]; }
+};
+
+// entry P of A_e x_e (template recursion: every table index is a compile-
+// time constant, so a constant-bank table becomes a DFMA operand)
+template <int O, int P, typename Tab>
+__device__ __forceinline__ void gram_pairs(const Tab& tb, const double (&Bt)[4][4], double sa, const double (&xe)[6],
+                                           double (&Y)[19]) {
+  constexpr int i = pair_i(P), j = pair_j(P);
+  constexpr int a = local_edge_vertex(i, 0), b = local_edge_vertex(i, 1);
+  constexpr int c = local_edge_vertex(j, 0), d = local_edge_vertex(j, 1);
+  constexpr bool neg = local_edge_ref(O, i).flipped != local_edge_ref(O, j).flipped;
+  double m = Bt[a][c] * tb.template get<22 + sym4(b, d)>();
+  m = fma(-Bt[a][d], tb.template get<22 + sym4(b, c)>(), m);
+  m = fma(-Bt[b][c], tb.template get<22 + sym4(a, d)>(), m);
+  m = fma(Bt[b][d], tb.template get<22 + sym4(a, c)>(), m);
+  const double aij = fma(sa, tb.template get<sym6(i, j)>(), neg ? -m : m);
+  constexpr int ei = cube_edge(O, i), ej = cube_edge(O, j);
+  Y[ei] = fma(aij, xe[j], Y[ei]);
+  if constexpr (i != j) Y[ej] = fma(aij, xe[i], Y[ej]);
+  if constexpr (P + 1 < 21) gram_pairs<O, P + 1>(tb, Bt, sa, xe, Y);
+}
+
+// Gram-form element (tables.hpp N1GramTable): Y[cube edges] += A_e x_e with
+//   A_ij = sa Kc_ij + s_ij (B_ac g_bd - B_ad g_bc - B_bc g_ad + B_bd g_ac)
+// In: accessor with  template <int K> double x()  (cube edge K) and
+//     template <int V, int W> double c()  (cube vertex V; W 0 alpha, 1 beta).
+// Tab: template <int I> double get()  (entry I of the orientation's row).
+// An invalid element gets zero coefficients -> A_e = 0 (inputs are finite).
+template <int O, typename Tab, typename In>
+__device__ __forceinline__ void element_gram(const Tab& tb, const In& in, double (&Y)[19], bool valid) {
+  constexpr int v0 = cube_vertex(O, 0), v1 = cube_vertex(O, 1), v2 = cube_vertex(O, 2), v3 = cube_vertex(O, 3);
+  const double a4 = (in.template c<v0, 0>() + in.template c<v1, 0>()) +
+                    (in.template c<v2, 0>() + in.template c<v3, 0>());
+  const double sa = valid ? a4 : 0.0;
+  const double bv[4] = {valid ? in.template c<v0, 1>() : 0.0, valid ? in.template c<v1, 1>() : 0.0,
+                        valid ? in.template c<v2, 1>() : 0.0, valid ? in.template c<v3, 1>() : 0.0};
+  const double S = (bv[0] + bv[1]) + (bv[2] + bv[3]);
+  const double S2 = S + S;
+  double Bt[4][4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const double u = S + bv[p];
+#pragma unroll
+    for (int q = p + 1; q < 4; ++q) Bt[p][q] = Bt[q][p] = u + bv[q];
+    Bt[p][p] = fma(4.0, bv[p], S2);
+  }
+  double xe[6];
+  xe[0] = in.template x<cube_edge(O, 0)>();
+  xe[1] = in.template x<cube_edge(O, 1)>();
+  xe[2] = in.template x<cube_edge(O, 2)>();
+  xe[3] = in.template x<cube_edge(O, 3)>();
+  xe[4] = in.template x<cube_edge(O, 4)>();
+  xe[5] = in.template x<cube_edge(O, 5)>();
+  gram_pairs<O, 0>(tb, Bt, sa, xe, Y);
+}
+
+// the six elements of the cube (validity by anchor sum class); Tabs:
+// template <int O> tab() -> the orientation's table accessor
+template <typename Tabs, typename In>
+__device__ __forceinline__ void cube_elements(const Tabs& ts, const In& in, double (&Y)[19], bool vWU, bool vMid,
+                                              bool vWD) {
+  element_gram<WU>(ts.template tab<WU>(), in, Y, vWU);
+  element_gram<BU>(ts.template tab<BU>(), in, Y, vMid);
+  element_gram<BD>(ts.template tab<BD>(), in, Y, vMid);
+  element_gram<GU>(ts.template tab<GU>(), in, Y, vMid);
+  element_gram<GD>(ts.template tab<GD>(), in, Y, vMid);
+  element_gram<WD>(ts.template tab<WD>(), in, Y, vWD);
+}
+
+// the six orientation rows of an N1GramTable in shared memory
+struct SmemTabs {
+  const N1GramTable& sg;
+  template <int O>
+  __device__ __forceinline__ SmemTab tab() const { return SmemTab{sg.o[O]}; }
+};
+
+} // namespace n1
+
+// kernel variant of the N1 apply (TETMF_N1_TABLE, read once):
+// 0 assembled tables, 1 Gram + direct loads, 2 Gram + row ring, 3 folded walk
+int n1_kernel_mode();
+
+} // namespace tetmf

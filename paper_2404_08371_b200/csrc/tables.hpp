@@ -82,11 +82,11 @@ struct N1GramTable {
 N1GramTable n1_gram_table(const MacroMesh& mesh, int macro, int level);
 
 // packed index of (i, j), i <= j < 6 (row-major upper triangle)
-TM_HD int sym6(int i, int j) {
+TM_HD constexpr int sym6(int i, int j) {
   if (i > j) { const int t = i; i = j; j = t; }
   return i * 6 - i * (i - 1) / 2 + (j - i);
 }
-TM_HD int sym4(int i, int j) {
+TM_HD constexpr int sym4(int i, int j) {
   if (i > j) { const int t = i; i = j; j = t; }
   return i * 4 - i * (i - 1) / 2 + (j - i);
 }
