@@ -124,7 +124,7 @@ n1_cubes_kernel(const N1GramTable* __restrict__ gram, const N1DeviceTable* __res
     for (int i = threadIdx.x; i < 6 * 5 * 21; i += blockDim.x)
       st.e[i / 105][(i / 21) % 5][i % 21] = __ldg(&table->e[0][0][0] + i);
   } else {
-    for (int i = threadIdx.x; i < 6 * 32; i += blockDim.x) sg.o[i / 32][i % 32] = __ldg(&gram->o[0][0] + i);
+    for (int i = threadIdx.x; i < 6 * kGramRow; i += blockDim.x) (&sg.o[0][0])[i] = __ldg(&gram->o[0][0] + i);
   }
   __syncthreads();
   const int warp = blockIdx.x * kWarps + (threadIdx.x >> 5);
@@ -351,7 +351,7 @@ n1_ring_kernel(const N1GramTable* __restrict__ gram, const double* __restrict__ 
                const N1Task* __restrict__ tasks, int ntasks, i64 stride, i64 cstride, i64 cf_stride, int n) {
   extern __shared__ __align__(16) double dsm[];
   N1GramTable& sg = *reinterpret_cast<N1GramTable*>(dsm);
-  for (int i = threadIdx.x; i < 6 * 32; i += blockDim.x) sg.o[i / 32][i % 32] = __ldg(&gram->o[0][0] + i);
+  for (int i = threadIdx.x; i < 6 * kGramRow; i += blockDim.x) (&sg.o[0][0])[i] = __ldg(&gram->o[0][0] + i);
   __syncthreads();
   const int warp = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (warp >= ntasks) return;

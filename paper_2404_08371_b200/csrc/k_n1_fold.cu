@@ -108,7 +108,7 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram, const double* __restrict__ 
                const FoldTask* __restrict__ tasks, int ntasks, i64 stride, i64 cstride, i64 cf_stride, int n) {
   extern __shared__ __align__(16) double dsm[];
   N1GramTable& sg = *reinterpret_cast<N1GramTable*>(dsm);
-  for (int i = threadIdx.x; i < 6 * 32; i += blockDim.x) sg.o[i / 32][i % 32] = __ldg(&gram->o[0][0] + i);
+  for (int i = threadIdx.x; i < 6 * kGramRow; i += blockDim.x) (&sg.o[0][0])[i] = __ldg(&gram->o[0][0] + i);
   const int lane = threadIdx.x & 31;
   double* ring = dsm + sizeof(N1GramTable) / sizeof(double) + (threadIdx.x >> 5) * kWarpSmem;
   for (int i = lane; i < kRing; i += 32) ring[i] = 0.0;  // unfilled positions must read finite

@@ -73,10 +73,17 @@ __device__ __forceinline__ void gram_pairs(const Tab& tb, const double (&Bt)[4][
   constexpr int a = local_edge_vertex(i, 0), b = local_edge_vertex(i, 1);
   constexpr int c = local_edge_vertex(j, 0), d = local_edge_vertex(j, 1);
   constexpr bool neg = local_edge_ref(O, i).flipped != local_edge_ref(O, j).flipped;
-  double m = Bt[a][c] * tb.template get<22 + sym4(b, d)>();
-  m = fma(-Bt[a][d], tb.template get<22 + sym4(b, c)>(), m);
-  m = fma(-Bt[b][c], tb.template get<22 + sym4(a, d)>(), m);
-  m = fma(Bt[b][d], tb.template get<22 + sym4(a, c)>(), m);
+  double m;
+  if constexpr (i == j) {  // Bt_aa g_bb + Bt_bb g_aa - 2 Bt_ab g_ab
+    m = Bt[a][a] * tb.template get<22 + sym4(b, b)>();
+    m = fma(Bt[b][b], tb.template get<22 + sym4(a, a)>(), m);
+    m = fma(Bt[a][b], tb.template get<32 + i>(), m);
+  } else {
+    m = Bt[a][c] * tb.template get<22 + sym4(b, d)>();
+    m = fma(-Bt[a][d], tb.template get<22 + sym4(b, c)>(), m);
+    m = fma(-Bt[b][c], tb.template get<22 + sym4(a, d)>(), m);
+    m = fma(Bt[b][d], tb.template get<22 + sym4(a, c)>(), m);
+  }
   const double aij = fma(sa, tb.template get<sym6(i, j)>(), neg ? -m : m);
   constexpr int ei = cube_edge(O, i), ej = cube_edge(O, j);
   Y[ei] = fma(aij, xe[j], Y[ei]);

@@ -189,6 +189,8 @@ N1GramTable n1_gram_table(const MacroMesh& mesh, int macro, int level) {
     for (int i = 0; i < 4; ++i) G[i] = mat_vec(g.JinvT, kGradRef[i]);
     for (int x = 0; x < 4; ++x)
       for (int y = x; y < 4; ++y) out.o[o][22 + sym4(x, y)] = g.vol / 120.0 * dot(G[x], G[y]);
+    for (int e = 0; e < 6; ++e)
+      out.o[o][32 + e] = -2.0 * out.o[o][22 + sym4(local_edge_vertex(e, 0), local_edge_vertex(e, 1))];
   }
   return out;
 }

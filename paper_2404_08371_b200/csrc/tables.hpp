@@ -76,8 +76,11 @@ N1DeviceTable pack_n1(const N1Tables& t);
 //   Bt_pq = S + beta_p + beta_q (p != q),  Bt_pp = 2 S + 4 beta_p
 // (exact: int lambda_m lambda_p lambda_q = 6 vol a!b!c!d!/6!). The local
 // signs s_i s_j of the mass term are compile-time constants in the kernel.
+// Diagonal entries i = (a,b) use  Bt_aa g_bb + Bt_bb g_aa + Bt_ab (-2 g_ab),
+// with -2 g_ab stored per local edge (one FP64 op fewer per diagonal entry).
+constexpr int kGramRow = 40;
 struct N1GramTable {
-  double o[6][32];  // [orientation][Kc 0..20, pad 21, g 22..31]
+  double o[6][kGramRow];  // [orientation][Kc 0..20, pad 21, g 22..31, -2 g_ab 32..37, pad]
 };
 N1GramTable n1_gram_table(const MacroMesh& mesh, int macro, int level);
 
