@@ -70,6 +70,10 @@ void build_n1_fold_tasks(const std::vector<int>& local_macros, int n, int parity
 void launch_n1_fold(const N1GramTable* gram, int pass, const double* x, const double* alpha, const double* beta,
                     double* y, const int* d_tasks, int ntasks, i64 macro_stride, i64 class_stride, i64 coeff_stride,
                     int n, cudaStream_t s);
+// K2 default: per-point gather over the 24 incident elements (k_p1k_gather.cu)
+void build_p1k_tasks(int nmacros, int n, std::vector<int>& out);
+void launch_p1k_gather(const double* x, const double* k, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
+                       int n, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
 void launch_p1k_cubes(const double* x, const double* k, double* y, const MacroDesc* d_macros, int nmacros,
                       i64 macro_stride, int n, const P1DeviceTable* d_tables, cudaStream_t s);
 void launch_n1_cubes(const double* x, const double* alpha, const double* beta, double* y,

@@ -22,7 +22,18 @@ namespace tetmf {
 namespace {
 
 constexpr int kWarps = 4;
-constexpr int kChunk = 8;  // rows per task
+#ifndef TETMF_P1S_CHUNK
+#define TETMF_P1S_CHUNK 8
+#endif
+#ifndef TETMF_P1S_PREFETCH
+#define TETMF_P1S_PREFETCH 0  // rows ahead warmed into L1 (measured: 2-8 rows ahead are 10-15 % slower)
+#endif
+constexpr int kChunk = TETMF_P1S_CHUNK;  // rows per task
+constexpr int kAhead = TETMF_P1S_PREFETCH;
+
+__device__ __forceinline__ void prefetch_l1(const double* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 
 struct Task2 {
   int macro, z, x0, y0;
@@ -112,6 +123,15 @@ p1_stencil2_kernel(const double* __restrict__ xin, double* __restrict__ yout, co
     const int yy = y0 + r;
     // new rows: L, A, B row y+1; U row y
     const int rl1 = rl + ll, ra1 = ra + la, rb1 = rb + lb;
+    if (kAhead > 0) {
+      // warm L1 with row y + 1 + kAhead of the four planes (no registers held)
+      const int d = kAhead;
+      const int tr = d * (d + 1) / 2;  // rows shrink by one per step
+      prefetch_l1(X + rl1 + d * ll - tr);
+      prefetch_l1(X + ra1 + d * la - tr);
+      prefetch_l1(X + rb1 + d * lb - tr);
+      prefetch_l1(X + ru + (d + 1) * lu - tr);
+    }
     const double Lp0 = __ldg(X + rl1), Lp1 = __ldg(X + rl1 + 1);
     const double Apm = __ldg(X + ra1 - 1), Ap0 = __ldg(X + ra1), Ap1 = __ldg(X + ra1 + 1);
     const double Bpm = __ldg(X + rb1 - 1), Bp0 = __ldg(X + rb1), Bp1 = __ldg(X + rb1 + 1);

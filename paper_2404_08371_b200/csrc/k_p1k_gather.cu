@@ -1,0 +1,155 @@
+// k_p1k_gather.cu -- K2 (default): P1 -div(k grad) with k in P1, gather form.
+//
+//   y_p = sum over the micro elements e containing p of  kbar_e (A_e x_e)_p,
+//   kbar_e = (k_a + k_b + k_c + k_d) / 4,  A_e = K_o (P1 stiffness of the
+//   element's orientation, tables.cpp)
+// i.e. the config-2 harness (forms.cpp:133-193 local_matrix
+// with k in P1 and the degree-2 rule, exact for P1 k).
+//
+// Each lane owns one lattice point; a warp covers 32 consecutive x of one row
+// (task = macro, z, y, x0). The 24 elements around p are the 6 orientations
+// of the 8 cubes anchored at p - d, d in {0,1}^3, restricted to the (o, i)
+// with vertex i of orientation o at cube corner d (6 elements share corners
+// 0 and 7, two share each other corner). Their vertices are p + (offset - d),
+// all within p's 15-point neighbourhood; x and k are read there (L1 / L2
+// resident across the warp). Each lane sums its own contributions in a fixed
+// order: deterministic, no atomics (the first version, k_apply_v1.cu,
+// scatters with FP64 atomics).
+#include "device.hpp"
+#include "runtime_check.hpp"
+
+namespace tetmf {
+
+namespace {
+
+constexpr int kWarps = 4;
+
+struct RowTask {
+  int macro, z, y, x0;
+};
+
+// The 24 (corner d, orientation o, local vertex i) with vertex i of o at
+// cube corner d, and for each the neighbourhood slots q = (rx+1) + 3 (ry+1) +
+// 9 (rz+1) of the element's four vertices relative to the point: a compile-
+// time table, so every index below folds to a constant.
+struct Incident {
+  int d, o, i, q[4];
+};
+struct IncidentTable {
+  Incident e[24];
+  unsigned slots;  // bit q: slot q is a vertex of some incident element
+};
+constexpr IncidentTable make_incident() {
+  IncidentTable t{};
+  int k = 0;
+  for (int d = 0; d < 8; ++d)
+    for (int o = 0; o < 6; ++o)
+      for (int i = 0; i < 4; ++i) {
+        const Off3 c = orient_offset(o, i);
+        if (c.x + 2 * c.y + 4 * c.z != d) continue;
+        Incident& e = t.e[k++];
+        e.d = d;
+        e.o = o;
+        e.i = i;
+        for (int j = 0; j < 4; ++j) {
+          const Off3 v = orient_offset(o, j);
+          e.q[j] = (v.x - (d & 1) + 1) + 3 * (v.y - ((d >> 1) & 1) + 1) + 9 * (v.z - (d >> 2) + 1);
+          t.slots |= 1u << e.q[j];
+        }
+      }
+  return t;
+}
+constexpr IncidentTable kInc = make_incident();
+
+// contribution of incident element K (template recursion: everything about the
+// element is a compile-time constant)
+template <int K>
+__device__ __forceinline__ void incident(const double (&xv)[27], const double (&kv)[27],
+                                         const double* __restrict__ Kt, int px, int py, int pz, int n,
+                                         double& acc) {
+  constexpr int d = kInc.e[K].d, o = kInc.e[K].o, i = kInc.e[K].i;
+  constexpr int dx = d & 1, dy = (d >> 1) & 1, dz = d >> 2;
+  constexpr int q0 = kInc.e[K].q[0], q1 = kInc.e[K].q[1], q2 = kInc.e[K].q[2], q3 = kInc.e[K].q[3];
+  // element (anchor p - d, orientation o) exists
+  if (px >= dx && py >= dy && pz >= dz && px + py + pz - dx - dy - dz <= orient_sum_limit(o, n)) {
+    const double ks = (kv[q0] + kv[q1]) + (kv[q2] + kv[q3]);
+    double row = __ldg(Kt + o * 10 + sym4(i, 0)) * xv[q0];
+    row = fma(__ldg(Kt + o * 10 + sym4(i, 1)), xv[q1], row);
+    row = fma(__ldg(Kt + o * 10 + sym4(i, 2)), xv[q2], row);
+    row = fma(__ldg(Kt + o * 10 + sym4(i, 3)), xv[q3], row);
+    acc = fma(0.25 * ks, row, acc);
+  }
+  if constexpr (K + 1 < 24) incident<K + 1>(xv, kv, Kt, px, py, pz, n, acc);
+}
+
+template <int Q>
+__device__ __forceinline__ void neighbour(double (&xv)[27], double (&kv)[27], const double* __restrict__ xm,
+                                          const double* __restrict__ km, const i64 (&rs)[3][3], int px, int py,
+                                          int pz, int n) {
+  constexpr int rx = Q % 3 - 1, ry = (Q / 3) % 3 - 1, rz = Q / 9 - 1;
+  xv[Q] = kv[Q] = 0.0;
+  if constexpr (((kInc.slots >> Q) & 1u) != 0) {
+    if (px + rx >= 0 && py + ry >= 0 && pz + rz >= 0 && px + py + pz + rx + ry + rz <= n) {
+      const i64 a = rs[rz + 1][ry + 1] + rx;
+      xv[Q] = __ldg(xm + a);
+      kv[Q] = __ldg(km + a);
+    }
+  }
+  if constexpr (Q + 1 < 27) neighbour<Q + 1>(xv, kv, xm, km, rs, px, py, pz, n);
+}
+
+__global__ void __launch_bounds__(32 * kWarps)
+p1k_gather_kernel(const double* __restrict__ x, const double* __restrict__ kc, double* __restrict__ y,
+                  const RowTask* __restrict__ tasks, int ntasks, i64 stride, int n,
+                  const P1DeviceTable* __restrict__ tabs, const MacroDesc* __restrict__ macros) {
+  const int warp = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (warp >= ntasks) return;
+  const RowTask t = tasks[warp];
+  const int pz = t.z, py = t.y, px = t.x0 + (threadIdx.x & 31);
+  if (px > n - pz - py) return;  // past the row end
+  const double* __restrict__ K = &tabs[macros[t.macro].group].K[0][0];
+  const double* __restrict__ xm = x + static_cast<i64>(t.macro) * stride;
+  const double* __restrict__ km = kc + static_cast<i64>(t.macro) * stride;
+  // row starts of rows py-1 .. py+1 in planes pz-1 .. pz+1
+  i64 rs[3][3];
+#pragma unroll
+  for (int dz = -1; dz <= 1; ++dz)
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy)
+      rs[dz + 1][dy + 1] = plane_offset(n, pz + dz) + row_offset(n, pz + dz, py + dy) + px;
+  // x and k on the 15-point neighbourhood (slot (rx+1) + 3 (ry+1) + 9 (rz+1)),
+  // all loads issued up front; out-of-lattice neighbours read as 0 (they
+  // only belong to elements that are skipped)
+  double xv[27], kv[27];
+  neighbour<0>(xv, kv, xm, km, rs, px, py, pz, n);
+  double acc = 0.0;
+  incident<0>(xv, kv, K, px, py, pz, n, acc);
+  y[static_cast<i64>(t.macro) * stride + rs[1][1]] = acc;
+}
+
+} // namespace
+
+// one task per (macro, plane z, row y, 32-wide x segment)
+void build_p1k_tasks(int nmacros, int n, std::vector<int>& out) {
+  out.clear();
+  for (int li = 0; li < nmacros; ++li)
+    for (int z = 0; z <= n; ++z)
+      for (int yy = 0; yy <= n - z; ++yy)
+        for (int x0 = 0; x0 <= n - z - yy; x0 += 32) {
+          out.push_back(li);
+          out.push_back(z);
+          out.push_back(yy);
+          out.push_back(x0);
+        }
+}
+
+void launch_p1k_gather(const double* x, const double* k, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
+                       int n, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
+  if (ntasks == 0) return;
+  const unsigned grid = static_cast<unsigned>((ntasks + kWarps - 1) / kWarps);
+  p1k_gather_kernel<<<grid, 32 * kWarps, 0, s>>>(x, k, y, reinterpret_cast<const RowTask*>(d_tasks), ntasks,
+                                                 macro_stride, n, d_tables, d_macros);
+  check_launch("p1k_gather");
+}
+
+} // namespace tetmf

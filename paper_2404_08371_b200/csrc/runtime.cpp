@@ -145,6 +145,9 @@ Context::LevelData& Context::level(Space s, int level) {
     build_stencil_tasks(static_cast<int>(macros_.size()), n, tasks);
     ld->ntasks2 = static_cast<int>(tasks.size() / 4);
     ld->tasks2.upload(tasks.data(), tasks.size(), stream_);
+    build_p1k_tasks(static_cast<int>(macros_.size()), n, tasks);
+    ld->np1k_tasks = static_cast<int>(tasks.size() / 4);
+    ld->p1k_tasks.upload(tasks.data(), tasks.size(), stream_);
   } else {
     std::vector<int> all, part;
     ld->group_tasks.assign(ngroups_, {0, 0, 0, 0});
@@ -359,8 +362,12 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
                            ld.macros.get(), s);
       break;
     case Form::P1KDiffusion:
-      launch_p1k_cubes(x, coeffs_[0]->data(level), y, ld.macros.get(), nm, ld.lay.macro_stride, ld.lay.n,
-                       t.p1.get(), s);
+      if (kernel_variant_ == 1)
+        launch_p1k_cubes(x, coeffs_[0]->data(level), y, ld.macros.get(), nm, ld.lay.macro_stride, ld.lay.n,
+                         t.p1.get(), s);
+      else
+        launch_p1k_gather(x, coeffs_[0]->data(level), y, ld.p1k_tasks.get(), ld.np1k_tasks, ld.lay.macro_stride,
+                          ld.lay.n, t.p1.get(), ld.macros.get(), s);
       break;
     case Form::N1CurlCurlMass: {
       auto& cl = ctx_->level(Space::P1, level);

@@ -105,6 +105,8 @@ public:
     int ntasks3 = 0;
     DeviceBuffer<int> tasks4;           // P1: register-tile tasks (variant 4)
     int ntasks4 = 0;
+    DeviceBuffer<int> p1k_tasks;        // P1: row tasks of the P1K gather kernel (K2)
+    int np1k_tasks = 0;
     // ND1: task ranges (offset, count) per (geometry group, parity pass)
     std::vector<std::array<int, 4>> group_tasks;  // {offset0, count0, offset1, count1}
   };
