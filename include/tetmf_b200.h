@@ -111,6 +111,21 @@ int tetmf_apply(tetmf_op* op, const tetmf_fn* src, tetmf_fn* dst, int level, int
 int tetmf_apply_ref_host(tetmf_op* op, tetmf_fn* src, tetmf_fn* dst, int level, const double* host_v,
                          double* host_w);
 
+/* Dirichlet-masked matrix-free CG (the reference's
+ * cg_solve, which its sources do not contain). Homogeneous
+ * Dirichlet conditions on the reference's boundary carriers (interior() == 0,
+ * fespace.hpp:95-96). Inner products count every carrier once (owner copy)
+ * and skip Dirichlet carriers; all ranks see identical scalars. */
+/* *out = sum over interior carriers of a * b (collective over ranks) */
+int tetmf_fn_dot(const tetmf_fn* a, const tetmf_fn* b, int level, double* out);
+/* zero the Dirichlet (boundary) carriers of fn */
+int tetmf_fn_mask_dirichlet(tetmf_fn* fn, int level);
+/* solve P A P x = P b for x (initial guess in, solution out, Dirichlet
+ * carriers 0); stops at ||r|| <= rtol ||r0|| or max_iter iterations.
+ * iterations / rel_residual / converged may be NULL. */
+int tetmf_cg_solve(tetmf_op* op, const tetmf_fn* b, tetmf_fn* x, int level, double rtol, int max_iter,
+                   int* iterations, double* rel_residual, int* converged);
+
 /* instrumentation: CUDA events around the element kernel of every apply on
  * the context stream (enable resets the totals); stats synchronize. */
 int tetmf_op_profile(tetmf_op* op, int enable);
@@ -129,6 +144,9 @@ int tetmf_host_free(void* ptr);
 int tetmf_plan_ref_map(tetmf_ctx* ctx, int space, int level, int64_t* out, int64_t entries,
                        int64_t* num_ref_dofs);
 int tetmf_plan_layout(tetmf_ctx* ctx, int space, int level, int64_t* macro_stride, int64_t* class_stride);
+/* interior (non-Dirichlet) mask in reference numbering, as the solver and the
+ * seeded Dirichlet fill use it (FieldVector interior(), fespace.hpp:95-96) */
+int tetmf_plan_interior(tetmf_ctx* ctx, int space, int level, unsigned char* out, int64_t num_ref_dofs);
 /* rank-local interface groups: sizes, then CSR arrays */
 int tetmf_plan_local_groups(tetmf_ctx* ctx, int space, int level, int64_t* ngroups, int64_t* ncopies,
                             int64_t* offsets, int64_t* copies);

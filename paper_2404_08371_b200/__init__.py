@@ -81,6 +81,8 @@ _SIGS = {
     "tetmf_host_free": (ctypes.c_int, [_c_vp]),
     "tetmf_plan_ref_map": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, _c_i64p, ctypes.c_int64, _c_i64p]),
     "tetmf_plan_layout": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, _c_i64p, _c_i64p]),
+    "tetmf_plan_interior": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_ubyte),
+                                           ctypes.c_int64]),
     "tetmf_plan_local_groups": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, _c_i64p, _c_i64p, _c_i64p,
                                                _c_i64p]),
     "tetmf_plan_exchange": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, _c_ip, _c_i64p, _c_i64p, _c_i64p,
@@ -92,6 +94,10 @@ _SIGS = {
     "tetmf_plan_local_matrix": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                _c_dp, _c_dp, _c_dp]),
     "tetmf_plan_stencil": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, _c_dp]),
+    "tetmf_fn_dot": (ctypes.c_int, [_c_vp, _c_vp, ctypes.c_int, _c_dp]),
+    "tetmf_fn_mask_dirichlet": (ctypes.c_int, [_c_vp, ctypes.c_int]),
+    "tetmf_cg_solve": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, ctypes.c_int, ctypes.c_double, ctypes.c_int, _c_ip, _c_dp,
+                                      _c_ip]),
     "tetmf_op_profile": (ctypes.c_int, [_c_vp, ctypes.c_int]),
     "tetmf_op_set_variant": (ctypes.c_int, [_c_vp, ctypes.c_int]),
     "tetmf_op_kernel_stats": (ctypes.c_int, [_c_vp, _c_dp, _c_i64p]),
@@ -203,6 +209,13 @@ class Context:
         nd = ctypes.c_int64()
         _check(lib().tetmf_plan_ref_map(self._h, space, level, _iptr(out), total, ctypes.byref(nd)))
         return out, nd.value
+
+    def interior(self, space: int, level: int) -> np.ndarray:
+        """Interior (non-Dirichlet) mask in reference numbering (uint8)."""
+        _, nd = self.ref_map(space, level)
+        out = np.empty(nd, dtype=np.uint8)
+        _check(lib().tetmf_plan_interior(self._h, space, level, out.ctypes.data_as(ctypes.POINTER(ctypes.c_ubyte)), nd))
+        return out
 
     def local_groups(self, space: int, level: int):
         ng, nc = ctypes.c_int64(), ctypes.c_int64()
@@ -316,6 +329,16 @@ class Function:
         _check(lib().tetmf_fn_export_ref(self._h, level, _dptr(out)))
         return out
 
+    def dot(self, other: "Function", level: int) -> float:
+        """Inner product over the interior (non-Dirichlet) carriers, each once."""
+        out = ctypes.c_double()
+        _check(lib().tetmf_fn_dot(self._h, other.handle, level, ctypes.byref(out)))
+        return out.value
+
+    def mask_dirichlet(self, level: int):
+        """Zero the Dirichlet (domain-boundary) carriers."""
+        _check(lib().tetmf_fn_mask_dirichlet(self._h, level))
+
 
 class Operator:
     """Form + coefficient functions (FormSystem + coefficient binding)."""
@@ -348,6 +371,16 @@ class Operator:
         pv = _dptr(v) if isinstance(v, np.ndarray) else ctypes.cast(_c_vp(v), _c_dp)
         pw = _dptr(w) if isinstance(w, np.ndarray) else ctypes.cast(_c_vp(w), _c_dp)
         _check(lib().tetmf_apply_ref_host(self._h, src.handle, dst.handle, level, pv, pw))
+
+    def cg_solve(self, b: Function, x: Function, level: int, rtol: float = 1e-10, max_iter: int = 1000):
+        """Dirichlet-masked CG for A x = b (x: initial guess in, solution out).
+        Returns (iterations, relative residual, converged)."""
+        it = ctypes.c_int()
+        rr = ctypes.c_double()
+        cv = ctypes.c_int()
+        _check(lib().tetmf_cg_solve(self._h, b.handle, x.handle, level, rtol, max_iter, ctypes.byref(it),
+                                    ctypes.byref(rr), ctypes.byref(cv)))
+        return it.value, rr.value, bool(cv.value)
 
     def set_variant(self, variant: int):
         """0 = optimized kernels (default), 1 = first-version kernels."""

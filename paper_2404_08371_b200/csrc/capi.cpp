@@ -14,6 +14,7 @@
 #include "exchange.hpp"
 #include "runtime.hpp"
 #include "runtime_check.hpp"
+#include "solver.hpp"
 
 namespace tetmf {
 void nccl_get_unique_id(void* out);
@@ -294,6 +295,35 @@ int tetmf_apply_ref_host(tetmf_op* op, tetmf_fn* src, tetmf_fn* dst, int level, 
   });
 }
 
+int tetmf_fn_dot(const tetmf_fn* a, const tetmf_fn* b, int level, double* out) {
+  return guard([&] {
+    need(a, "a");
+    need(b, "b");
+    need(out, "out");
+    *out = masked_dot(*a->impl, *b->impl, level);
+  });
+}
+
+int tetmf_fn_mask_dirichlet(tetmf_fn* fn, int level) {
+  return guard([&] {
+    need(fn, "fn");
+    mask_dirichlet(*fn->impl, level);
+  });
+}
+
+int tetmf_cg_solve(tetmf_op* op, const tetmf_fn* b, tetmf_fn* x, int level, double rtol, int max_iter,
+                   int* iterations, double* rel_residual, int* converged) {
+  return guard([&] {
+    need(op, "op");
+    need(b, "b");
+    need(x, "x");
+    const CgResult r = cg_solve(*op->impl, *b->impl, *x->impl, level, rtol, max_iter);
+    if (iterations) *iterations = r.iterations;
+    if (rel_residual) *rel_residual = r.rel_residual;
+    if (converged) *converged = r.converged ? 1 : 0;
+  });
+}
+
 int tetmf_op_profile(tetmf_op* op, int enable) {
   return guard([&] {
     need(op, "op");
@@ -337,6 +367,27 @@ int tetmf_host_free(void* ptr) {
 }
 
 // ------------------------------------------------------------ planning hooks
+int tetmf_plan_interior(tetmf_ctx* ctx, int space, int level, unsigned char* out, int64_t num_ref_dofs) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    const Context& c = *ctx->impl;
+    const Space sp = space_of(space);
+    const auto lay = LevelLayout::make(sp, level, c.mesh().num_tets(), c.macros());
+    const auto rn = build_ref_numbering(c.mesh(), c.topo(), lay);
+    if (num_ref_dofs != rn.num_dofs) fail_arg("plan_interior: output length does not match num_ref_dofs");
+    std::memset(out, 1, static_cast<std::size_t>(num_ref_dofs));
+    for (std::size_t li = 0; li < lay.macros.size(); ++li) {
+      const int m = lay.macros[li];
+      const i64 base = static_cast<i64>(li) * lay.macro_stride;
+      for_each_carrier(sp, lay.n, [&](const Carrier& car) {
+        const i64 e = rn.map[base + car.slot];
+        if (e >= 0 && !carrier_interior(c.topo(), m, lay.n, car)) out[e >> 2] = 0;
+      });
+    }
+  });
+}
+
 int tetmf_plan_layout(tetmf_ctx* ctx, int space, int level, int64_t* macro_stride, int64_t* class_stride) {
   return guard([&] {
     need(ctx, "ctx");

@@ -1,0 +1,111 @@
+// cg.cpp -- host driver of the Dirichlet-masked matrix-free CG (solver.hpp).
+//
+// Plain CG (Hestenes-Stiefel) on P A P with P the Dirichlet mask:
+//   r = P(b - A x), p = r
+//   repeat: q = P A p;  alpha = <r,r> / <p,q>;  x += alpha p;  r -= alpha q
+//           beta = <r_new,r_new> / <r,r>;  p = r + beta p
+// Every vector op is a kernel on the context stream; the two inner products
+// per iteration are read back to the host (the iteration count decision).
+#include <cmath>
+
+#include "runtime.hpp"
+#include "runtime_check.hpp"
+#include "solver.hpp"
+
+namespace tetmf {
+
+void nccl_allgather_doubles(void* comm, const double* d_in, double* d_out, int count, cudaStream_t stream);
+
+namespace {
+
+SlotSpace slot_space(const Context::LevelData& ld) {
+  return SlotSpace{ld.lay.n, ld.lay.space == Space::ND1 ? 1 : 0, ld.lay.macro_stride, ld.lay.class_stride};
+}
+
+} // namespace
+
+double masked_dot(const Function& a, const Function& b, int level) {
+  if (a.space() != b.space() || &a.ctx() != &b.ctx()) fail_arg("dot: functions of different spaces / contexts");
+  Context& ctx = a.ctx();
+  auto& ld = ctx.level(a.space(), level);
+  const cudaStream_t s = ctx.stream();
+  double* scratch = ld.dot_scratch.get();
+  const int np = masked_dot_partials();
+  double* local = scratch + np;          // this rank's sum
+  double* gathered = local + 1;          // nranks sums
+  double* total = gathered + ctx.nranks();
+  if (ld.lay.macros.empty()) {
+    TETMF_CUDA(cudaMemsetAsync(local, 0, sizeof(double), s));
+  } else {
+    launch_masked_dot(a.data(level), b.data(level), slot_space(ld), ld.slot_table.get(), ld.lay.total(), scratch,
+                      local, s);
+  }
+  double out = 0.0;
+  if (ctx.nranks() > 1) {
+    nccl_allgather_doubles(ctx.comm_backend().get(), local, gathered, 1, s);
+    launch_sum_ordered(gathered, ctx.nranks(), total, s);
+    TETMF_CUDA(cudaMemcpyAsync(&out, total, sizeof(double), cudaMemcpyDeviceToHost, s));
+  } else {
+    TETMF_CUDA(cudaMemcpyAsync(&out, local, sizeof(double), cudaMemcpyDeviceToHost, s));
+  }
+  TETMF_CUDA(cudaStreamSynchronize(s));
+  return out;
+}
+
+void mask_dirichlet(Function& f, int level) {
+  auto& ld = f.ctx().level(f.space(), level);
+  if (ld.lay.macros.empty()) return;
+  launch_mask_dirichlet(f.data(level), slot_space(ld), ld.slot_table.get(), ld.lay.total(), f.ctx().stream());
+}
+
+CgResult cg_solve(Operator& op, const Function& b, Function& x, int level, double rtol, int max_iter) {
+  const Space sp = op.info().trial;
+  if (b.space() != sp || x.space() != sp) fail_arg("cg: b and x must be in the operator's trial space");
+  if (!(rtol > 0.0) || max_iter < 0) fail_arg("cg: rtol must be > 0 and max_iter >= 0");
+  Context& ctx = x.ctx();
+  const cudaStream_t s = ctx.stream();
+  const i64 count = x.size(level);
+  Function r(ctx, sp), p(ctx, sp), q(ctx, sp);
+  double* X = x.data(level);
+  double* R = r.data(level);
+  double* P = p.data(level);
+  double* Q = q.data(level);
+  const double* B = b.data(level);
+
+  mask_dirichlet(x, level);
+  op.apply(x, q, level, Update::Replace);  // q = A x
+  TETMF_CUDA(cudaMemcpyAsync(R, B, sizeof(double) * count, cudaMemcpyDeviceToDevice, s));
+  launch_axpy(R, Q, -1.0, count, s);       // r = b - A x
+  mask_dirichlet(r, level);
+  TETMF_CUDA(cudaMemcpyAsync(P, R, sizeof(double) * count, cudaMemcpyDeviceToDevice, s));
+  double rr = masked_dot(r, r, level);
+  const double rr0 = rr;
+  CgResult res;
+  res.rel_residual = rr0 > 0.0 ? 1.0 : 0.0;
+  if (rr0 == 0.0) {
+    res.converged = true;
+    return res;
+  }
+  const double stop = rtol * rtol * rr0;
+  for (int it = 0; it < max_iter; ++it) {
+    op.apply(p, q, level, Update::Replace);
+    mask_dirichlet(q, level);
+    const double pq = masked_dot(p, q, level);
+    if (!(pq > 0.0)) fail_internal("cg: operator is not positive definite on the interior carriers");
+    const double alpha = rr / pq;
+    launch_axpy(X, P, alpha, count, s);
+    launch_axpy(R, Q, -alpha, count, s);
+    const double rr_new = masked_dot(r, r, level);
+    res.iterations = it + 1;
+    res.rel_residual = std::sqrt(rr_new / rr0);
+    if (rr_new <= stop) {
+      res.converged = true;
+      break;
+    }
+    launch_xpby(P, R, rr_new / rr, count, s);  // p = r + beta p
+    rr = rr_new;
+  }
+  return res;
+}
+
+} // namespace tetmf

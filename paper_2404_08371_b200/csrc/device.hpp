@@ -21,7 +21,7 @@ namespace tetmf {
 // One stored macro as the kernels see it.
 struct MacroDesc {
   int group;         // geometry group (index into the table array)
-  int bface;         // bit v: face opposite local vertex v is domain boundary
+  int dmask;         // bit k: carriers with support mask k are Dirichlet (Topology::dirichlet_mask)
   i64 V0[3];         // integer world coords (scaled by n * D) of local vertex 0
   i64 E[3][3];       // integer edge vectors v_{c+1} - v_0 (scaled by D), E[c][r]
   double X0[3];      // world coords of local vertex 0

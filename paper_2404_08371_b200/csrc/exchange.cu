@@ -99,4 +99,10 @@ void nccl_comm_destroy(void* comm) {
   if (comm) ncclCommDestroy(static_cast<ncclComm_t>(comm));
 }
 
+// out[r * count + k] = in_r[k] for every rank r (solver scalars, solver.hpp)
+void nccl_allgather_doubles(void* comm, const double* d_in, double* d_out, int count, cudaStream_t stream) {
+  if (!comm) throw CommError("allgather: no NCCL communicator attached to the context");
+  nccl_check(ncclAllGather(d_in, d_out, count, ncclDouble, static_cast<ncclComm_t>(comm), stream), "ncclAllGather");
+}
+
 } // namespace tetmf

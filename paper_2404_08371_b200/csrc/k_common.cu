@@ -52,11 +52,9 @@ __device__ void world_pos(const MacroDesc& m, int n, int x, int y, int z, double
                           static_cast<double>(z) * m.dX[2][r]);
 }
 
-__device__ bool on_boundary_face(const MacroDesc& m, unsigned mask) {
-  for (int v = 0; v < 4; ++v)
-    if (((m.bface >> v) & 1) && !(mask & (1u << v))) return true;
-  return false;
-}
+// Dirichlet carrier: its support simplex lies in a domain boundary face of
+// some macro (Topology::dirichlet_mask; fespace.cpp:207-214, 226)
+__device__ bool on_boundary_face(const MacroDesc& m, unsigned mask) { return (m.dmask >> (mask & 15u)) & 1; }
 
 __device__ unsigned support_mask_dev(int n, int x, int y, int z) {
   return (n - x - y - z > 0 ? 1u : 0u) | (x > 0 ? 2u : 0u) | (y > 0 ? 4u : 0u) | (z > 0 ? 8u : 0u);

@@ -206,13 +206,10 @@ inline std::array<int, 3> record_base(int cls, const std::array<int, 3>& a) {
 } // namespace
 
 bool carrier_interior(const Topology& topo, int m, int n, const Carrier& c) {
-  // boundary iff the carrier lies in a boundary face plane of macro m
-  // (fespace.cpp:207-214): a boundary face opposite local vertex v whose
-  // weight is zero on every endpoint, i.e. bit v absent from the mask.
-  for (int v = 0; v < 4; ++v)
-    if (topo.boundary_face[m][v] && !(c.mask & (1u << v))) return false;
+  // boundary iff the carrier lies in a boundary face plane of any macro that
+  // holds it (fespace.cpp:207-214; flags OR-merged over copies, :226)
   (void)n;
-  return true;
+  return !((topo.dirichlet_mask[m] >> (c.mask & 15u)) & 1u);
 }
 
 RefNumbering build_ref_numbering(const MacroMesh& mesh, const Topology& topo, const LevelLayout& lay) {

@@ -183,6 +183,26 @@ Topology::Topology(const MacroMesh& mesh) {
   boundary_face.assign(nt, {false, false, false, false});
   for (int m = 0; m < nt; ++m)
     for (int f = 0; f < 4; ++f) boundary_face[m][f] = bset.count(face_of(mesh.tets[m], f)) > 0;
+  dirichlet_mask.assign(nt, 0u);
+  for (int m = 0; m < nt; ++m)
+    for (unsigned mask = 1; mask < 16; ++mask) {
+      bool on = false;
+      for (int m2 : sharers[m][mask])
+        for (int f = 0; f < 4 && !on; ++f) {
+          if (!boundary_face[m2][f]) continue;
+          const int skip = mesh.tets[m2][f];  // the face is tet m2 without this vertex
+          bool inside = true;
+          for (int v = 0; v < 4; ++v)
+            if ((mask >> v) & 1u) {
+              const int g = mesh.tets[m][v];
+              bool in_tet = false;
+              for (int w = 0; w < 4; ++w) in_tet = in_tet || mesh.tets[m2][w] == g;
+              if (!in_tet || g == skip) inside = false;
+            }
+          on = inside;
+        }
+      if (on) dirichlet_mask[m] |= 1u << mask;
+    }
 
   // integer coordinate scale (world keys of the seeded input generator)
   coord_scale = 0;

@@ -46,6 +46,11 @@ struct Topology {
   std::vector<std::array<std::vector<int>, 16>> sharers;
   // [macro][local face f (opposite local vertex f)] -> true if domain boundary
   std::vector<std::array<bool, 4>> boundary_face;
+  // [macro] bit `mask`: the sub-simplex of that support mask lies in a domain
+  // boundary face (of ANY macro), i.e. its carriers are Dirichlet carriers.
+  // The reference OR-merges the per-copy boundary flag over all macros that
+  // hold a carrier (fespace.cpp:207-214, 226).
+  std::vector<unsigned> dirichlet_mask;
   // integer scale D such that D * vertex coordinates are integers (0 if none)
   std::int64_t coord_scale = 0;
   std::vector<std::array<std::int64_t, 3>> int_vertices;  // D * vertices

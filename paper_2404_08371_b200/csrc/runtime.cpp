@@ -1,5 +1,6 @@
 // runtime.cpp -- Context / Function / Operator (host C++).
 #include "runtime.hpp"
+#include "solver.hpp"
 
 #include <algorithm>
 #include <atomic>
@@ -109,9 +110,7 @@ Context::LevelData& Context::level(Space s, int level) {
     MacroDesc& d = descs[li];
     std::memset(&d, 0, sizeof(d));
     d.group = group_[li];
-    d.bface = 0;
-    for (int v = 0; v < 4; ++v)
-      if (topo_.boundary_face[m][v]) d.bface |= 1 << v;
+    d.dmask = static_cast<int>(topo_.dirichlet_mask[m]);
     for (int r = 0; r < 3; ++r) {
       d.V0[r] = static_cast<i64>(n) * topo_.int_vertices[t[0]][r];
       d.X0[r] = mesh_.vertices[t[0]][r];
@@ -164,6 +163,23 @@ Context::LevelData& Context::level(Space s, int level) {
     }
     ld->ntasks = static_cast<int>(all.size() / 4);
     ld->tasks.upload(all.data(), all.size(), stream_);
+  }
+  {
+    // solver slot classes (solver.cu): interior = not in a boundary face plane
+    // of any macro holding the carrier (fespace.cpp:207-214, 226), owner =
+    // lowest sharing macro id
+    std::vector<unsigned char> table(16 * macros_.size(), 0);
+    for (std::size_t li = 0; li < macros_.size(); ++li) {
+      const int m = macros_[li];
+      for (unsigned mask = 1; mask < 16; ++mask) {
+        const bool interior = !((topo_.dirichlet_mask[m] >> mask) & 1u);
+        const auto& sh = topo_.sharers[m][mask];
+        const bool owner = sh.empty() || sh.front() == m;
+        table[16 * li + mask] = static_cast<unsigned char>((interior ? 1 : 0) | (owner ? 2 : 0));
+      }
+    }
+    ld->slot_table.upload(table.data(), table.size(), stream_);
+    ld->dot_scratch.reset(static_cast<std::size_t>(masked_dot_partials() + 2 * (nranks_ + 1)));
   }
   ld->groups = local_groups_only(mesh_, topo_, ld->lay, rank_of, rank_);
   ld->group_offsets.upload(ld->groups.offsets.data(), ld->groups.offsets.size(), stream_);

@@ -107,6 +107,10 @@ public:
     int ntasks4 = 0;
     DeviceBuffer<int> p1k_tasks;        // P1: row tasks of the P1K gather kernel (K2)
     int np1k_tasks = 0;
+    // solver (solver.hpp): per local macro, [support mask] -> {bit 0 interior,
+    // bit 1 owner copy}; reduction scratch
+    DeviceBuffer<unsigned char> slot_table;
+    DeviceBuffer<double> dot_scratch;
     // ND1: task ranges (offset, count) per (geometry group, parity pass)
     std::vector<std::array<int, 4>> group_tasks;  // {offset0, count0, offset1, count1}
   };

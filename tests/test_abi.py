@@ -101,6 +101,27 @@ def test_ref_numbering_matches_reference_geometry(tm, mesh, form, level):
     assert (owners == 1).all()
 
 
+@pytest.mark.parametrize("mesh", ["single-tet", "cube6", "cubes2", "cubes2x1x3"])
+@pytest.mark.parametrize("form", ["P1", "N1"])
+def test_dirichlet_mask_matches_reference_interior(tm, tmp_path, mesh, form):
+    """Dirichlet carriers = boundary flag OR-merged over every macro holding the
+    carrier (fespace.cpp:207-214, 226). Kuhn-cube meshes have macros that
+    touch the domain boundary only along an edge or a vertex."""
+    from oracle.refapi import PortSystem, write_kuhn_mesh
+    space = tm.SPACE_ND1 if form == "N1" else tm.SPACE_P1
+    level = 2
+    ctx = tm.Context(mesh, device=-1)
+    port_mesh = mesh
+    if mesh.startswith("cubes"):
+        dims = [int(v) for v in mesh[5:].split("x")]
+        port_mesh = str(tmp_path / "kuhn.mesh")
+        write_kuhn_mesh(port_mesh, *dims)
+    want = PortSystem(port_mesh, form, level).interior()
+    got = ctx.interior(space, level)
+    assert got.shape == want.shape
+    assert np.array_equal(got, want), (int((got != want).sum()), got.size)
+
+
 @pytest.mark.parametrize("space", [0, 2])
 def test_interface_groups_are_geometric_copies(tm, space):
     ctx = tm.Context("cube6", device=-1)
