@@ -155,3 +155,53 @@ def test_p1_manufactured_solution_converges_second_order(tm):
     print("max errors", errs, "rates", rates, "rms rates", rms_rates)
     # O(h^2): the rates approach 2 from below (pre-asymptotic at coarse levels)
     assert rates[-1] > 1.75 and rms_rates[-1] > 1.8, (errs, rates, rms, rms_rates)
+
+
+# ---- N1 manufactured solution: curl curl E + E = f on the unit cube, n x E = 0
+
+def _edge_interpolant(F, a, b):
+    """DoF = line integral of F . t along a -> b, 2-point Gauss (fespace.cpp:494-521)."""
+    g = 0.5 / math.sqrt(3.0)
+    t = b - a
+    out = np.zeros(len(a))
+    for s in (0.5 - g, 0.5 + g):
+        p = a + s * t
+        out += 0.5 * np.einsum("ij,ij->i", F(p), t)
+    return out
+
+
+def _E(p):
+    sx, sy, sz = np.sin(math.pi * p[:, 0]), np.sin(math.pi * p[:, 1]), np.sin(math.pi * p[:, 2])
+    return np.stack([sy * sz, sz * sx, sx * sy], axis=1)
+
+
+def test_n1_manufactured_solution_converges(tm):
+    """curl curl E = 2 pi^2 E for the field above; load vector b = M I_h f with
+    M the ND1 mass matrix (the N1 operator with alpha = 0, beta = 1)."""
+    errs = []
+    for level in (2, 3, 4, 5):
+        ctx = tm.Context("cube6", device=0)
+        one = tm.Function(ctx, tm.SPACE_P1)
+        zero = tm.Function(ctx, tm.SPACE_P1)
+        one.fill_coefficient(level, tm.COEFF_CONST, 1.0)
+        zero.fill_coefficient(level, tm.COEFF_CONST, 0.0)
+        A = tm.Operator(ctx, tm.FORM_N1, [one, one])   # curl curl + mass
+        M = tm.Operator(ctx, tm.FORM_N1, [zero, one])  # mass
+        port = PortSystem("cube6", "N1", level)
+        _, a, b = port.dof_geometry()
+        interior = port.interior().astype(bool)
+        IE = _edge_interpolant(_E, a, b)
+        If = (2 * math.pi ** 2 + 1.0) * IE
+        fI = tm.Function(ctx, tm.SPACE_ND1)
+        fI.import_ref(level, If)
+        rhs = tm.Function(ctx, tm.SPACE_ND1)
+        M.apply(fI, rhs, level)
+        x = tm.Function(ctx, tm.SPACE_ND1)
+        it, rel, ok = A.cg_solve(rhs, x, level, rtol=1e-12, max_iter=5000)
+        assert ok
+        e = (x.export_ref(level) - IE)[interior]
+        errs.append(np.abs(e).max() / np.abs(IE).max())
+    rates = [math.log2(errs[i] / errs[i + 1]) for i in range(len(errs) - 1)]
+    print("N1 relative DoF errors", errs, "rates", rates)
+    # at least first order (SURVEY.md 8(f): O(h) for ND1)
+    assert min(rates[-2:]) > 0.9, (errs, rates)
