@@ -289,6 +289,13 @@ def run_gpu(a):
 
     # ---------------- roofline of the dominant (element) kernel
     kern_avg_ms = kern_ms / max(kern_n, 1)
+    # DRAM traffic of the dominant kernel per apply, from the committed ncu
+    # --set full capture of this configuration (None if not captured)
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json"))).get(a.config)
+    except Exception:
+        pass
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -303,7 +310,9 @@ def run_gpu(a):
         fp64_peak = ctx.fp64_peak(1.0) if a.fp64_peak else None
         bytes_alg = 8.0 * (2 * nd1_local + 2 * p1_local)
         roof = {"bound": "fp64", "achieved": flops / (kern_avg_ms * 1e-3) / 1e12,
-                "peak": fp64_peak, "unit": "TFLOP/s", "traffic": None,
+                "peak": fp64_peak, "unit": "TFLOP/s",
+                "traffic": traffic["bytes_per_launch"] if traffic else None,
+                "traffic_source": traffic["source"] if traffic else None,
                 "frac": (flops / (kern_avg_ms * 1e-3) / 1e12) / fp64_peak if fp64_peak else None,
                 "flop_per_launch": flops, "flop_per_element": FLOP_PER_ELEM["N1"],
                 "peak_source": "measured FP64 DFMA-chain probe (tetmf_measure_fp64_peak) on this GPU",
@@ -313,7 +322,9 @@ def run_gpu(a):
         p1_local = local_counts["p1_points"]
         nbytes = 8.0 * p1_local * (3 if form == "P1K" else 2)
         roof = {"bound": "hbm", "achieved": nbytes / (kern_avg_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                "frac": nbytes / (kern_avg_ms * 1e-3) / 1e9 / hbm_peak, "traffic": None,
+                "frac": nbytes / (kern_avg_ms * 1e-3) / 1e9 / hbm_peak,
+                "traffic": traffic["bytes_per_launch"] if traffic else None,
+                "traffic_source": traffic["source"] if traffic else None,
                 "bytes_per_launch": nbytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
     roof["kernel_ms"] = kern_avg_ms
     roof["kernel_share_of_step"] = kern_avg_ms / ms_per_step
