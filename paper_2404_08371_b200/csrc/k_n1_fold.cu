@@ -54,7 +54,10 @@ namespace {
 
 using namespace n1;
 
-constexpr int kWarps = 4;
+#ifndef TETMF_N1F_WARPS
+#define TETMF_N1F_WARPS 4  // warps per CTA
+#endif
+constexpr int kWarps = TETMF_N1F_WARPS;
 #ifndef TETMF_N1F_MIN_BLOCKS
 #define TETMF_N1F_MIN_BLOCKS 3
 #endif
