@@ -61,6 +61,9 @@ constexpr int kWarps = TETMF_N1F_WARPS;
 #ifndef TETMF_N1F_MIN_BLOCKS
 #define TETMF_N1F_MIN_BLOCKS 3
 #endif
+#ifndef TETMF_N1F_STAGE_RMW
+#define TETMF_N1F_STAGE_RMW 1  // pass 1: stage the partial sums by cp.async (0: read-modify-write)
+#endif
 #ifndef TETMF_N1F_CHUNK
 #define TETMF_N1F_CHUNK 32
 #endif
@@ -198,7 +201,10 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram, const double* __restrict__ 
         cp_async8(e + 13 * kRow, Bm + vu + 1);
       }
     }
-    if (PASS == 1) {
+    // only for steps that write (>= t0): the halo step writes nothing, and a
+    // prologue staging into the 2-slot ring would still be in flight when the
+    // first loop step stages into the same slot
+    if (PASS == 1 && TETMF_N1F_STAGE_RMW && tc + 1 >= t0) {
       // in-plane partial sums of step tc + 1's writes: [0..2] plane z classes
       // 0, 1, 3; [3..5] plane z+1 classes 0, 1, 3 (class 0 at the delayed row
       // in phase 2)
@@ -274,43 +280,51 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram, const double* __restrict__ 
     if (tt >= t0) {
       // pass 1: the staged partial sums (copied at step tt - 1)
       const double* st = rmw + ((tt + 1) & 1) * kRmw;
-      auto acc = [&](int k) { return PASS == 1 ? st[32 * k] : 0.0; };
+      // in-plane partial sums: pass 0 stores, pass 1 adds (staged operand k)
+      auto wr = [&](double* p, int k, double v) {
+        if (PASS == 0)
+          *p = v;
+        else if (TETMF_N1F_STAGE_RMW)
+          *p = st[32 * k] + v;
+        else
+          *p += v;
+      };
       if (p1) {
         if (lane > 0 && cube && s <= n - 1) {  // all owned edges of row y
           double* __restrict__ yz = Ym + ez_of(y) + X;
           yz[2 * cs] = Y[2] + c2 + r8;
           yz[4 * cs] = Y[4] + c4;
           yz[5 * cs] = Y[5] + r9;
-          yz[0] = acc(0) + (Y[0] + c0);
-          yz[cs] = acc(1) + (Y[1] + r7);
-          yz[3 * cs] = acc(2) + Y[3];
+          wr(yz, 0, (Y[0] + c0));
+          wr(yz + cs, 1, (Y[1] + r7));
+          wr(yz + 3 * cs, 2, Y[3]);
           if (s <= n - 2) {
             yz[6 * cs] = Y[6];
             double* __restrict__ yu = Ym + eu_of(y) + X;
-            yu[0] = acc(3) + (Y[14] + cT0);
-            yu[cs] = acc(4) + (Y[15] + r17);
-            yu[3 * cs] = acc(5) + Y[16];
+            wr(yu, 3, (Y[14] + cT0));
+            wr(yu + cs, 4, (Y[15] + r17));
+            wr(yu + 3 * cs, 5, Y[16]);
           }
         }
       } else if (lane < 31 && far_ok) {
         if (cube) {  // owned edges of row y with no share from row y-1
           double* __restrict__ yz = Ym + ez_of(y) + X;
           yz[5 * cs] = Y[5] + r9;
-          yz[cs] = acc(1) + (Y[1] + r7);
-          yz[3 * cs] = acc(2) + Y[3];
+          wr(yz + cs, 1, (Y[1] + r7));
+          wr(yz + 3 * cs, 2, Y[3]);
           if (s <= n - 2) {
             yz[6 * cs] = Y[6];
             double* __restrict__ yu = Ym + eu_of(y) + X;
-            yu[cs] = acc(4) + (Y[15] + r17);
-            yu[3 * cs] = acc(5) + Y[16];
+            wr(yu + cs, 4, (Y[15] + r17));
+            wr(yu + 3 * cs, 5, Y[16]);
           }
         }
         if (y + 1 >= 0 && y + 1 <= ytop) {  // delayed edges of row y+1
           double* __restrict__ yz = Ym + ez_of(y + 1) + X;
           yz[2 * cs] = Y[11] + c2 + r13;
           yz[4 * cs] = Y[12] + c4;
-          yz[0] = acc(0) + (Y[10] + c0);
-          if (s + 1 <= n - 2) Ym[eu_of(y + 1) + X] = acc(3) + (Y[18] + cT0);
+          wr(yz, 0, (Y[10] + c0));
+          if (s + 1 <= n - 2) wr(Ym + eu_of(y + 1) + X, 3, Y[18] + cT0);
         }
       }
     }

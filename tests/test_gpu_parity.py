@@ -101,6 +101,7 @@ def test_config1_dirichlet(tm):
 @pytest.mark.gpu
 @pytest.mark.parametrize("mesh,form,level", [("cube6", "P1", 7), ("single-tet", "P1", 8), ("cubes1x1x2", "P1", 5),
                                              ("cube6", "N1", 6), ("single-tet", "N1", 7), ("cubes2", "N1", 4),
+                                             ("cubes2", "N1", 6), ("cubes1x1x2", "N1", 7),
                                              ("cube6", "P1K", 6), ("single-tet", "P1K", 8)])
 def test_optimized_vs_first_version(tm, mesh, form, level):
     """A/B: optimized kernels (variant 0) vs the first-version kernels
