@@ -31,8 +31,14 @@ constexpr int kWarps = 4;
 constexpr int kChunk = TETMF_P1S_CHUNK;  // rows per task
 constexpr int kAhead = TETMF_P1S_PREFETCH;
 
+#ifndef TETMF_P1S_PREFETCH_L2
+#define TETMF_P1S_PREFETCH_L2 0  // 1: prefetch into L2 only (no L1 allocation)
+#endif
 __device__ __forceinline__ void prefetch_l1(const double* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+  if (TETMF_P1S_PREFETCH_L2)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  else
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
 struct Task2 {
@@ -77,7 +83,13 @@ __device__ __forceinline__ double stencil_var(const double* __restrict__ wt, dou
   return (a0 + a1) + (a2 + a3);
 }
 
+// no minimum-blocks bound by default: ptxas then settles at 128 registers
+// (an explicit minimum of 1 lets it take 190 and costs 55 % in occupancy)
+#ifdef TETMF_P1S_MIN_BLOCKS
+__global__ void __launch_bounds__(32 * kWarps, TETMF_P1S_MIN_BLOCKS)
+#else
 __global__ void __launch_bounds__(32 * kWarps)
+#endif
 p1_stencil2_kernel(const double* __restrict__ xin, double* __restrict__ yout, const Task2* __restrict__ tasks,
                    int ntasks, i64 stride, int n, const P1DeviceTable* __restrict__ tabs,
                    const MacroDesc* __restrict__ macros) {
