@@ -42,8 +42,9 @@
 // Copied addresses are the ones k_n1_cubes.cu reads.
 //
 // Pass 1 (odd layers) adds to in-plane partial sums written by pass 0; those
-// six values per cube are staged by cp.async one step ahead as well (2-slot
-// ring), so the read-modify-write costs no load latency.
+// six values per cube are staged by cp.async one step ahead as well (one slot
+// per lane, filled at the end of the previous step), so the read-modify-write
+// costs no load latency.
 #include "device.hpp"
 #include "n1_common.cuh"
 #include "runtime_check.hpp"
@@ -74,7 +75,7 @@ constexpr int kRow = 34;                 // positions per array row
 constexpr int kSlot = kArrays * kRow;    // doubles per ring slot
 constexpr int kRing = 3 * kSlot;         // input ring, doubles per warp
 constexpr int kRmw = 6 * 32;             // pass-1 staging slot, doubles per warp
-constexpr int kWarpSmem = kRing + 2 * kRmw;
+constexpr int kWarpSmem = kRing + kRmw;
 
 struct FoldTask {
   int macro, z, k, t0;  // layer, near segment, first step of the chunk
@@ -118,7 +119,7 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram, const double* __restrict__ 
   const int lane = threadIdx.x & 31;
   double* ring = dsm + sizeof(N1GramTable) / sizeof(double) + (threadIdx.x >> 5) * kWarpSmem;
   for (int i = lane; i < kRing; i += 32) ring[i] = 0.0;  // unfilled positions must read finite
-  double* rmw = ring + kRing + lane;                     // [2][6][32]
+  double* rmw = ring + kRing + lane;                     // [6][32]
   __syncthreads();
   const int warp = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (warp >= ntasks) return;
@@ -157,9 +158,8 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram, const double* __restrict__ 
   auto eu_of = [&](int r) { return peu + r * (lez - 1) - tri(r); };
 
   // the copies made at step tc, for step tc + 1: input row (phase-1 row
-  // tc + 2, or the far row step tc + 1 reads first) into ring slot `slot`;
-  // in pass 1 also the partial sums step tc + 1 adds to (staging slot rs)
-  auto copy_for = [&](int tc, int slot, int rs) {
+  // tc + 2, or the far row step tc + 1 reads first) into ring slot `slot`
+  auto copy_for = [&](int tc, int slot) {
     int row = -1, col = 0;
     bool far = false;
     if (tc + 1 < P1) {
@@ -201,53 +201,55 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram, const double* __restrict__ 
         cp_async8(e + 13 * kRow, Bm + vu + 1);
       }
     }
-    // only for steps that write (>= t0): the halo step writes nothing, and a
-    // prologue staging into the 2-slot ring would still be in flight when the
-    // first loop step stages into the same slot
-    if (PASS == 1 && TETMF_N1F_STAGE_RMW && tc + 1 >= t0) {
-      // in-plane partial sums of step tc + 1's writes: [0..2] plane z classes
-      // 0, 1, 3; [3..5] plane z+1 classes 0, 1, 3 (class 0 at the delayed row
-      // in phase 2)
-      double* r = rmw + rs * kRmw;
-      const int tn = tc + 1;
-      if (tn < P1) {
-        if (tn >= 0 && lane > 0) {
-          const double* a = Ym + ez_of(tn) + Xn;
-          const double* b = Ym + eu_of(tn) + Xn;
-          cp_async8(r, a);
-          cp_async8(r + 32, a + cs);
-          cp_async8(r + 64, a + 3 * cs);
-          cp_async8(r + 96, b);
-          cp_async8(r + 128, b + cs);
-          cp_async8(r + 160, b + 3 * cs);
-        }
-      } else if (far_ok && lane < 31) {
-        const int yn = D - tn;
-        if (yn >= 0 && yn <= ytop) {
-          const double* a = Ym + ez_of(yn) + Xf;
-          const double* b = Ym + eu_of(yn) + Xf;
-          cp_async8(r + 32, a + cs);
-          cp_async8(r + 64, a + 3 * cs);
-          cp_async8(r + 128, b + cs);
-          cp_async8(r + 160, b + 3 * cs);
-        }
-        if (yn + 1 >= 0 && yn + 1 <= ytop) {
-          cp_async8(r, Ym + ez_of(yn + 1) + Xf);
-          cp_async8(r + 96, Ym + eu_of(yn + 1) + Xf);
-        }
+    cp_async_commit();
+  };
+  // pass 1: the in-plane partial sums step tn adds to -- [0..2] plane z
+  // classes 0, 1, 3; [3..5] plane z+1 classes 0, 1, 3 (class 0 at the delayed
+  // row in phase 2) -- staged into the warp's single staging slot at the end
+  // of step tn - 1 (after that step's writes consumed the slot); the next
+  // step's cp.async.wait_group 1 covers it
+  auto stage_rmw = [&](int tn) {
+    double* r = rmw;
+    if (tn < P1) {
+      if (tn >= 0 && lane > 0) {
+        const double* a = Ym + ez_of(tn) + Xn;
+        const double* b = Ym + eu_of(tn) + Xn;
+        cp_async8(r, a);
+        cp_async8(r + 32, a + cs);
+        cp_async8(r + 64, a + 3 * cs);
+        cp_async8(r + 96, b);
+        cp_async8(r + 128, b + cs);
+        cp_async8(r + 160, b + 3 * cs);
+      }
+    } else if (far_ok && lane < 31) {
+      const int yn = D - tn;
+      if (yn >= 0 && yn <= ytop) {
+        const double* a = Ym + ez_of(yn) + Xf;
+        const double* b = Ym + eu_of(yn) + Xf;
+        cp_async8(r + 32, a + cs);
+        cp_async8(r + 64, a + 3 * cs);
+        cp_async8(r + 128, b + cs);
+        cp_async8(r + 160, b + 3 * cs);
+      }
+      if (yn + 1 >= 0 && yn + 1 <= ytop) {
+        cp_async8(r, Ym + ez_of(yn + 1) + Xf);
+        cp_async8(r + 96, Ym + eu_of(yn + 1) + Xf);
       }
     }
     cp_async_commit();
   };
+  constexpr bool kStage = PASS == 1 && TETMF_N1F_STAGE_RMW != 0;
+
   int slot = ts % 3;  // ring slot of the copy made at step tt
-  copy_for(ts - 2, slot == 0 ? 1 : slot == 1 ? 2 : 0, ts & 1);
-  copy_for(ts - 1, slot == 0 ? 2 : slot - 1, (ts + 1) & 1);
+  copy_for(ts - 2, slot == 0 ? 1 : slot == 1 ? 2 : 0);
+  copy_for(ts - 1, slot == 0 ? 2 : slot - 1);
+  if (kStage && t0 == 0) stage_rmw(0);  // the first step writes (no halo step)
 
   double c0 = 0.0, c2 = 0.0, c4 = 0.0, cT0 = 0.0;
   for (int tt = ts; tt < te; ++tt) {
     asm volatile("" ::: "memory");  // table reads stay in the loop (no hoisting)
-    copy_for(tt, slot, tt & 1);
-    cp_async_wait1();  // copies of steps tt-2, tt-1 landed (this lane's)
+    copy_for(tt, slot);
+    cp_async_wait1();  // all but this step's input copy landed (this lane's)
     __syncwarp();      // ... and every lane's
     const int sA = slot == 2 ? 0 : slot + 1;  // (tt + 1) mod 3
     const int sB = sA == 2 ? 0 : sA + 1;      // (tt + 2) mod 3
@@ -278,8 +280,8 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram, const double* __restrict__ 
     const double r17 = __shfl_sync(0xffffffffu, Y[17], src);
 
     if (tt >= t0) {
-      // pass 1: the staged partial sums (copied at step tt - 1)
-      const double* st = rmw + ((tt + 1) & 1) * kRmw;
+      // pass 1: the staged partial sums (copied at the end of step tt - 1)
+      const double* st = rmw;
       // in-plane partial sums: pass 0 stores, pass 1 adds (staged operand k)
       auto wr = [&](double* p, int k, double v) {
         if (PASS == 0)
@@ -328,6 +330,7 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram, const double* __restrict__ 
         }
       }
     }
+    if (kStage && tt + 1 < te) stage_rmw(tt + 1);  // tt + 1 >= t0 always (tt >= t0 - 1)
     // carried partial sums: phase 1 -> owners of row y+1, phase 2 -> this
     // row's delayed edges
     if (p1) {
