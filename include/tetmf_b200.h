@@ -126,6 +126,15 @@ int tetmf_fn_mask_dirichlet(tetmf_fn* fn, int level);
 int tetmf_cg_solve(tetmf_op* op, const tetmf_fn* b, tetmf_fn* x, int level, double rtol, int max_iter,
                    int* iterations, double* rel_residual, int* converged);
 
+/* operator diagonal d_i = A_ii of the level (every interface copy holds the
+ * full sum, the inverse-diagonal of Jacobi / Chebyshev
+ * smoothing): the diagonal of the reference's assembled FormSystem operator */
+int tetmf_op_diagonal(tetmf_op* op, tetmf_fn* diag, int level);
+/* tetmf_cg_solve with Jacobi preconditioning by diag (from tetmf_op_diagonal;
+ * NULL = unpreconditioned) */
+int tetmf_pcg_solve(tetmf_op* op, const tetmf_fn* b, tetmf_fn* x, const tetmf_fn* diag, int level, double rtol,
+                    int max_iter, int* iterations, double* rel_residual, int* converged);
+
 /* instrumentation: CUDA events around the element kernel of every apply on
  * the context stream (enable resets the totals); stats synchronize. */
 int tetmf_op_profile(tetmf_op* op, int enable);

@@ -98,6 +98,9 @@ _SIGS = {
     "tetmf_fn_mask_dirichlet": (ctypes.c_int, [_c_vp, ctypes.c_int]),
     "tetmf_cg_solve": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, ctypes.c_int, ctypes.c_double, ctypes.c_int, _c_ip, _c_dp,
                                       _c_ip]),
+    "tetmf_op_diagonal": (ctypes.c_int, [_c_vp, _c_vp, ctypes.c_int]),
+    "tetmf_pcg_solve": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp, ctypes.c_int, ctypes.c_double, ctypes.c_int, _c_ip,
+                                       _c_dp, _c_ip]),
     "tetmf_op_profile": (ctypes.c_int, [_c_vp, ctypes.c_int]),
     "tetmf_op_set_variant": (ctypes.c_int, [_c_vp, ctypes.c_int]),
     "tetmf_op_kernel_stats": (ctypes.c_int, [_c_vp, _c_dp, _c_i64p]),
@@ -372,15 +375,25 @@ class Operator:
         pw = _dptr(w) if isinstance(w, np.ndarray) else ctypes.cast(_c_vp(w), _c_dp)
         _check(lib().tetmf_apply_ref_host(self._h, src.handle, dst.handle, level, pv, pw))
 
-    def cg_solve(self, b: Function, x: Function, level: int, rtol: float = 1e-10, max_iter: int = 1000):
-        """Dirichlet-masked CG for A x = b (x: initial guess in, solution out).
+    def cg_solve(self, b: Function, x: Function, level: int, rtol: float = 1e-10, max_iter: int = 1000,
+                 diag: Function | None = None):
+        """Dirichlet-masked CG for A x = b (x: initial guess in, solution out);
+        diag (from diagonal()) -> Jacobi-preconditioned CG.
         Returns (iterations, relative residual, converged)."""
         it = ctypes.c_int()
         rr = ctypes.c_double()
         cv = ctypes.c_int()
-        _check(lib().tetmf_cg_solve(self._h, b.handle, x.handle, level, rtol, max_iter, ctypes.byref(it),
-                                    ctypes.byref(rr), ctypes.byref(cv)))
+        if diag is None:
+            _check(lib().tetmf_cg_solve(self._h, b.handle, x.handle, level, rtol, max_iter, ctypes.byref(it),
+                                        ctypes.byref(rr), ctypes.byref(cv)))
+        else:
+            _check(lib().tetmf_pcg_solve(self._h, b.handle, x.handle, diag.handle, level, rtol, max_iter,
+                                         ctypes.byref(it), ctypes.byref(rr), ctypes.byref(cv)))
         return it.value, rr.value, bool(cv.value)
+
+    def diagonal(self, d: Function, level: int):
+        """d = diag(A) (the assembled operator's diagonal; all copies hold the sum)."""
+        _check(lib().tetmf_op_diagonal(self._h, d.handle, level))
 
     def set_variant(self, variant: int):
         """0 = optimized kernels (default), 1 = first-version kernels."""

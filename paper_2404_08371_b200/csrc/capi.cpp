@@ -324,6 +324,28 @@ int tetmf_cg_solve(tetmf_op* op, const tetmf_fn* b, tetmf_fn* x, int level, doub
   });
 }
 
+int tetmf_op_diagonal(tetmf_op* op, tetmf_fn* diag, int level) {
+  return guard([&] {
+    need(op, "op");
+    need(diag, "diag");
+    op->impl->diagonal(*diag->impl, level);
+  });
+}
+
+int tetmf_pcg_solve(tetmf_op* op, const tetmf_fn* b, tetmf_fn* x, const tetmf_fn* diag, int level, double rtol,
+                    int max_iter, int* iterations, double* rel_residual, int* converged) {
+  return guard([&] {
+    need(op, "op");
+    need(b, "b");
+    need(x, "x");
+    const CgResult r =
+        cg_solve(*op->impl, *b->impl, *x->impl, level, rtol, max_iter, diag ? diag->impl.get() : nullptr);
+    if (iterations) *iterations = r.iterations;
+    if (rel_residual) *rel_residual = r.rel_residual;
+    if (converged) *converged = r.converged ? 1 : 0;
+  });
+}
+
 int tetmf_op_profile(tetmf_op* op, int enable) {
   return guard([&] {
     need(op, "op");

@@ -7,6 +7,7 @@
 // Every vector op is a kernel on the context stream; the two inner products
 // per iteration are read back to the host (the iteration count decision).
 #include <cmath>
+#include <memory>
 
 #include "runtime.hpp"
 #include "runtime_check.hpp"
@@ -58,27 +59,39 @@ void mask_dirichlet(Function& f, int level) {
   launch_mask_dirichlet(f.data(level), slot_space(ld), ld.slot_table.get(), ld.lay.total(), f.ctx().stream());
 }
 
-CgResult cg_solve(Operator& op, const Function& b, Function& x, int level, double rtol, int max_iter) {
+CgResult cg_solve(Operator& op, const Function& b, Function& x, int level, double rtol, int max_iter,
+                  const Function* diag) {
   const Space sp = op.info().trial;
   if (b.space() != sp || x.space() != sp) fail_arg("cg: b and x must be in the operator's trial space");
+  if (diag && (diag->space() != sp || !diag->has_level(level))) fail_arg("cg: diagonal not in the trial space");
   if (!(rtol > 0.0) || max_iter < 0) fail_arg("cg: rtol must be > 0 and max_iter >= 0");
   Context& ctx = x.ctx();
   const cudaStream_t s = ctx.stream();
   const i64 count = x.size(level);
   Function r(ctx, sp), p(ctx, sp), q(ctx, sp);
+  std::unique_ptr<Function> zf;
   double* X = x.data(level);
   double* R = r.data(level);
   double* P = p.data(level);
   double* Q = q.data(level);
   const double* B = b.data(level);
+  const double* Dg = diag ? diag->data(level) : nullptr;
+  double* Z = R;  // unpreconditioned: z = r
+  if (Dg) {
+    zf = std::make_unique<Function>(ctx, sp);
+    Z = zf->data(level);
+  }
+  const Function& z = Dg ? *zf : r;
 
   mask_dirichlet(x, level);
   op.apply(x, q, level, Update::Replace);  // q = A x
   TETMF_CUDA(cudaMemcpyAsync(R, B, sizeof(double) * count, cudaMemcpyDeviceToDevice, s));
   launch_axpy(R, Q, -1.0, count, s);       // r = b - A x
   mask_dirichlet(r, level);
-  TETMF_CUDA(cudaMemcpyAsync(P, R, sizeof(double) * count, cudaMemcpyDeviceToDevice, s));
+  if (Dg) launch_jacobi(Z, R, Dg, count, s);  // z = D^-1 r
+  TETMF_CUDA(cudaMemcpyAsync(P, Z, sizeof(double) * count, cudaMemcpyDeviceToDevice, s));
   double rr = masked_dot(r, r, level);
+  double rz = Dg ? masked_dot(r, z, level) : rr;
   const double rr0 = rr;
   CgResult res;
   res.rel_residual = rr0 > 0.0 ? 1.0 : 0.0;
@@ -92,18 +105,23 @@ CgResult cg_solve(Operator& op, const Function& b, Function& x, int level, doubl
     mask_dirichlet(q, level);
     const double pq = masked_dot(p, q, level);
     if (!(pq > 0.0)) fail_internal("cg: operator is not positive definite on the interior carriers");
-    const double alpha = rr / pq;
+    const double alpha = rz / pq;
     launch_axpy(X, P, alpha, count, s);
     launch_axpy(R, Q, -alpha, count, s);
-    const double rr_new = masked_dot(r, r, level);
+    rr = masked_dot(r, r, level);
     res.iterations = it + 1;
-    res.rel_residual = std::sqrt(rr_new / rr0);
-    if (rr_new <= stop) {
+    res.rel_residual = std::sqrt(rr / rr0);
+    if (rr <= stop) {
       res.converged = true;
       break;
     }
-    launch_xpby(P, R, rr_new / rr, count, s);  // p = r + beta p
-    rr = rr_new;
+    double rz_new = rr;
+    if (Dg) {
+      launch_jacobi(Z, R, Dg, count, s);
+      rz_new = masked_dot(r, z, level);
+    }
+    launch_xpby(P, Z, rz_new / rz, count, s);  // p = z + beta p
+    rz = rz_new;
   }
   return res;
 }

@@ -39,7 +39,8 @@ void launch_fill_coeff(double* out, const MacroDesc* d_macros, int nmacros, i64 
                        CoeffSpec spec, cudaStream_t s);
 void launch_import_ref(double* lat, const i64* map, i64 total, const double* ref, cudaStream_t s);
 void launch_export_ref(const double* lat, const i64* map, i64 total, double* ref, cudaStream_t s);
-void launch_interface_sum(double* y, const i64* offsets, const i64* copies, i64 ngroups, cudaStream_t s);
+void launch_interface_sum(double* y, const i64* offsets, const i64* copies, i64 ngroups, cudaStream_t s,
+                          bool signed_values = true);
 void launch_axpy(double* y, const double* x, double a, i64 count, cudaStream_t s);
 
 void launch_p1_stencil(const double* x, double* y, const MacroDesc* d_macros, int nmacros, i64 macro_stride,
@@ -79,6 +80,15 @@ void launch_p1k_cubes(const double* x, const double* k, double* y, const MacroDe
 void launch_n1_cubes(const double* x, const double* alpha, const double* beta, double* y,
                      const MacroDesc* d_macros, int nmacros, i64 macro_stride, i64 class_stride,
                      i64 coeff_stride, int n, const N1DeviceTable* d_tables, cudaStream_t s);
+
+// operator diagonals per stored macro copy (k_diagonal.cu, k_p1k_gather.cu)
+void launch_p1_diagonal(double* d, const MacroDesc* d_macros, int nmacros, i64 macro_stride, int n,
+                        const P1DeviceTable* d_tables, cudaStream_t s);
+void launch_p1k_diagonal(const double* k, double* d, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                         const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
+void launch_n1_diagonal(double* d, const double* alpha, const double* beta, const MacroDesc* d_macros, int nmacros,
+                        i64 macro_stride, i64 class_stride, i64 coeff_stride, int n, const N1GramTable* d_gram,
+                        cudaStream_t s);
 
 // FP64 DFMA-chain peak probe (used by bench.py to measure the FP64 roof).
 void launch_fp64_peak(double* out, int blocks, int threads, int iters, cudaStream_t s);

@@ -11,14 +11,15 @@ namespace tetmf {
 
 namespace {
 
-__global__ void pack_kernel(const double* y, const i64* send_index, double* send, i64 count) {
+__global__ void pack_kernel(const double* y, const i64* send_index, double* send, i64 count, bool sgn) {
   const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
-  if (i < count) exchange_pack_one(y, send_index, send, i);
+  if (i < count) exchange_pack_one(y, send_index, send, i, sgn);
 }
 
-__global__ void combine_kernel(double* y, const double* recv, const i64* offsets, const i64* entries, i64 ngroups) {
+__global__ void combine_kernel(double* y, const double* recv, const i64* offsets, const i64* entries, i64 ngroups,
+                               bool sgn) {
   const i64 g = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
-  if (g < ngroups) exchange_combine_one(y, recv, offsets, entries, g);
+  if (g < ngroups) exchange_combine_one(y, recv, offsets, entries, g, sgn);
 }
 
 template <typename T>
@@ -52,12 +53,13 @@ Exchange::~Exchange() {
   cudaFree(d_recv_);
 }
 
-void Exchange::run(double* y, cudaStream_t stream) {
+void Exchange::run(double* y, cudaStream_t stream, bool signed_values) {
   if (plan_.peers.empty()) return;
   if (!comm_) throw CommError("exchange: no NCCL communicator attached to the context");
   const i64 ns = plan_.send_total();
   if (ns > 0) {
-    pack_kernel<<<static_cast<unsigned>((ns + 255) / 256), 256, 0, stream>>>(y, d_send_index_, d_send_, ns);
+    pack_kernel<<<static_cast<unsigned>((ns + 255) / 256), 256, 0, stream>>>(y, d_send_index_, d_send_, ns,
+                                                                                 signed_values);
     check_launch("exchange_pack");
   }
   auto comm = static_cast<ncclComm_t>(comm_);
@@ -72,7 +74,8 @@ void Exchange::run(double* y, cudaStream_t stream) {
   const i64 ng = plan_.num_groups();
   if (ng > 0) {
     combine_kernel<<<static_cast<unsigned>((ng + 255) / 256), 256, 0, stream>>>(y, d_recv_, d_group_offsets_,
-                                                                                 d_group_entries_, ng);
+                                                                                 d_group_entries_, ng,
+                                                                                 signed_values);
     check_launch("exchange_combine");
   }
 }

@@ -52,24 +52,27 @@ ExchangePlan build_exchange_plan(const MacroMesh& mesh, const Topology& topo, co
 InterfaceGroups local_groups_only(const MacroMesh& mesh, const Topology& topo, const LevelLayout& lay,
                                   const std::vector<int>& rank_of, int rank);
 
-TM_HD void exchange_pack_one(const double* y, const i64* send_index, double* send, i64 i) {
+// signed_values = false: orientation signs ignored (operator diagonals)
+TM_HD void exchange_pack_one(const double* y, const i64* send_index, double* send, i64 i,
+                             bool signed_values = true) {
   const i64 e = send_index[i];
   const double v = y[e >> 1];
-  send[i] = (e & 1) ? -v : v;
+  send[i] = (signed_values && (e & 1)) ? -v : v;
 }
 
-TM_HD void exchange_combine_one(double* y, const double* recv, const i64* offsets, const i64* entries, i64 g) {
+TM_HD void exchange_combine_one(double* y, const double* recv, const i64* offsets, const i64* entries, i64 g,
+                                bool signed_values = true) {
   const i64 b = offsets[g], e = offsets[g + 1];
   double s = 0.0;
   for (i64 k = b; k < e; ++k) {
     const i64 c = entries[k];
     const double v = (c & 2) ? recv[c >> 2] : y[c >> 2];
-    s += (c & 1) ? -v : v;
+    s += (signed_values && (c & 1)) ? -v : v;
   }
   for (i64 k = b; k < e; ++k) {
     const i64 c = entries[k];
     if (c & 2) continue;
-    y[c >> 2] = (c & 1) ? -s : s;
+    y[c >> 2] = (signed_values && (c & 1)) ? -s : s;
   }
 }
 
@@ -93,8 +96,9 @@ class Exchange {
 public:
   Exchange(ExchangePlan plan, void* nccl_comm);
   ~Exchange();
-  // pack -> send/recv -> combine on `stream`
-  void run(double* y, cudaStream_t stream);
+  // pack -> send/recv -> combine on `stream` (signed_values = false: ND1
+  // orientation signs ignored, for operator diagonals)
+  void run(double* y, cudaStream_t stream, bool signed_values = true);
   const ExchangePlan& plan() const { return plan_; }
 
 private:

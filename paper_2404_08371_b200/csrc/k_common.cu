@@ -163,6 +163,9 @@ __global__ void export_ref_kernel(const double* lat, const i64* map, i64 total, 
 
 // K4: one thread per shared carrier; copies are summed in macro-id order so
 // every copy receives a bitwise-identical total.
+// SIGNED: ND1 copies carry their orientation sign relative to the owner;
+// unsigned sums (operator diagonals: sign^2 = 1) ignore it
+template <bool SIGNED>
 __global__ void interface_sum_kernel(double* y, const i64* offsets, const i64* copies, i64 ngroups) {
   const i64 g = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
   if (g >= ngroups) return;
@@ -171,11 +174,11 @@ __global__ void interface_sum_kernel(double* y, const i64* offsets, const i64* c
   for (i64 k = b; k < e; ++k) {
     const i64 c = copies[k];
     const double v = y[c >> 1];
-    s += (c & 1) ? -v : v;
+    s += (SIGNED && (c & 1)) ? -v : v;
   }
   for (i64 k = b; k < e; ++k) {
     const i64 c = copies[k];
-    y[c >> 1] = (c & 1) ? -s : s;
+    y[c >> 1] = (SIGNED && (c & 1)) ? -s : s;
   }
 }
 
@@ -230,9 +233,13 @@ void launch_export_ref(const double* lat, const i64* map, i64 total, double* ref
   check_launch("export_ref");
 }
 
-void launch_interface_sum(double* y, const i64* offsets, const i64* copies, i64 ngroups, cudaStream_t s) {
+void launch_interface_sum(double* y, const i64* offsets, const i64* copies, i64 ngroups, cudaStream_t s,
+                          bool signed_values) {
   if (ngroups <= 0) return;
-  interface_sum_kernel<<<grid_for(ngroups), kThreads, 0, s>>>(y, offsets, copies, ngroups);
+  if (signed_values)
+    interface_sum_kernel<true><<<grid_for(ngroups), kThreads, 0, s>>>(y, offsets, copies, ngroups);
+  else
+    interface_sum_kernel<false><<<grid_for(ngroups), kThreads, 0, s>>>(y, offsets, copies, ngroups);
   check_launch("interface_sum");
 }
 

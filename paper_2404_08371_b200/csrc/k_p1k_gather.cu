@@ -63,7 +63,7 @@ constexpr IncidentTable kInc = make_incident();
 
 // contribution of incident element K (template recursion: everything about the
 // element is a compile-time constant)
-template <int K>
+template <int K, bool DIAG>
 __device__ __forceinline__ void incident(const double (&xv)[27], const double (&kv)[27],
                                          const double* __restrict__ Kt, int px, int py, int pz, int n,
                                          double& acc) {
@@ -73,16 +73,20 @@ __device__ __forceinline__ void incident(const double (&xv)[27], const double (&
   // element (anchor p - d, orientation o) exists
   if (px >= dx && py >= dy && pz >= dz && px + py + pz - dx - dy - dz <= orient_sum_limit(o, n)) {
     const double ks = (kv[q0] + kv[q1]) + (kv[q2] + kv[q3]);
-    double row = __ldg(Kt + o * 10 + sym4(i, 0)) * xv[q0];
-    row = fma(__ldg(Kt + o * 10 + sym4(i, 1)), xv[q1], row);
-    row = fma(__ldg(Kt + o * 10 + sym4(i, 2)), xv[q2], row);
-    row = fma(__ldg(Kt + o * 10 + sym4(i, 3)), xv[q3], row);
-    acc = fma(0.25 * ks, row, acc);
+    if constexpr (DIAG) {  // operator diagonal: kbar_e (K_o)_ii
+      acc = fma(0.25 * ks, __ldg(Kt + o * 10 + sym4(i, i)), acc);
+    } else {
+      double row = __ldg(Kt + o * 10 + sym4(i, 0)) * xv[q0];
+      row = fma(__ldg(Kt + o * 10 + sym4(i, 1)), xv[q1], row);
+      row = fma(__ldg(Kt + o * 10 + sym4(i, 2)), xv[q2], row);
+      row = fma(__ldg(Kt + o * 10 + sym4(i, 3)), xv[q3], row);
+      acc = fma(0.25 * ks, row, acc);
+    }
   }
-  if constexpr (K + 1 < 24) incident<K + 1>(xv, kv, Kt, px, py, pz, n, acc);
+  if constexpr (K + 1 < 24) incident<K + 1, DIAG>(xv, kv, Kt, px, py, pz, n, acc);
 }
 
-template <int Q>
+template <int Q, bool DIAG>
 __device__ __forceinline__ void neighbour(double (&xv)[27], double (&kv)[27], const double* __restrict__ xm,
                                           const double* __restrict__ km, const i64 (&rs)[3][3], int px, int py,
                                           int pz, int n) {
@@ -91,13 +95,14 @@ __device__ __forceinline__ void neighbour(double (&xv)[27], double (&kv)[27], co
   if constexpr (((kInc.slots >> Q) & 1u) != 0) {
     if (px + rx >= 0 && py + ry >= 0 && pz + rz >= 0 && px + py + pz + rx + ry + rz <= n) {
       const i64 a = rs[rz + 1][ry + 1] + rx;
-      xv[Q] = __ldg(xm + a);
+      if constexpr (!DIAG) xv[Q] = __ldg(xm + a);
       kv[Q] = __ldg(km + a);
     }
   }
-  if constexpr (Q + 1 < 27) neighbour<Q + 1>(xv, kv, xm, km, rs, px, py, pz, n);
+  if constexpr (Q + 1 < 27) neighbour<Q + 1, DIAG>(xv, kv, xm, km, rs, px, py, pz, n);
 }
 
+template <bool DIAG>
 __global__ void __launch_bounds__(32 * kWarps)
 p1k_gather_kernel(const double* __restrict__ x, const double* __restrict__ kc, double* __restrict__ y,
                   const RowTask* __restrict__ tasks, int ntasks, i64 stride, int n,
@@ -121,9 +126,9 @@ p1k_gather_kernel(const double* __restrict__ x, const double* __restrict__ kc, d
   // all loads issued up front; out-of-lattice neighbours read as 0 (they
   // only belong to elements that are skipped)
   double xv[27], kv[27];
-  neighbour<0>(xv, kv, xm, km, rs, px, py, pz, n);
+  neighbour<0, DIAG>(xv, kv, xm, km, rs, px, py, pz, n);
   double acc = 0.0;
-  incident<0>(xv, kv, K, px, py, pz, n, acc);
+  incident<0, DIAG>(xv, kv, K, px, py, pz, n, acc);
   y[static_cast<i64>(t.macro) * stride + rs[1][1]] = acc;
 }
 
@@ -147,9 +152,19 @@ void launch_p1k_gather(const double* x, const double* k, double* y, const int* d
                        int n, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
   if (ntasks == 0) return;
   const unsigned grid = static_cast<unsigned>((ntasks + kWarps - 1) / kWarps);
-  p1k_gather_kernel<<<grid, 32 * kWarps, 0, s>>>(x, k, y, reinterpret_cast<const RowTask*>(d_tasks), ntasks,
-                                                 macro_stride, n, d_tables, d_macros);
+  p1k_gather_kernel<false><<<grid, 32 * kWarps, 0, s>>>(x, k, y, reinterpret_cast<const RowTask*>(d_tasks), ntasks,
+                                                        macro_stride, n, d_tables, d_macros);
   check_launch("p1k_gather");
+}
+
+// operator diagonal (per macro copy; interface copies are summed afterwards)
+void launch_p1k_diagonal(const double* k, double* d, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                         const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
+  if (ntasks == 0) return;
+  const unsigned grid = static_cast<unsigned>((ntasks + kWarps - 1) / kWarps);
+  p1k_gather_kernel<true><<<grid, 32 * kWarps, 0, s>>>(k, k, d, reinterpret_cast<const RowTask*>(d_tasks), ntasks,
+                                                       macro_stride, n, d_tables, d_macros);
+  check_launch("p1k_diagonal");
 }
 
 } // namespace tetmf

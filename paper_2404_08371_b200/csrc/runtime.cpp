@@ -409,6 +409,38 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
   if (ld.exchange) ld.exchange->run(y, s);
 }
 
+void Operator::diagonal(Function& d, int level) {
+  if (d.space() != info().trial || &d.ctx() != ctx_) fail_arg("diagonal: function not in the operator's trial space");
+  for (const Function* c : coeffs_)
+    if (!c->has_level(level)) fail_arg("diagonal: coefficient function has no data at this level");
+  auto& ld = ctx_->level(info().trial, level);
+  const int nm = static_cast<int>(ld.lay.macros.size());
+  double* y = d.data(level);
+  const cudaStream_t s = ctx_->stream();
+  if (nm > 0) {
+    auto& t = tables(level);
+    switch (form_) {
+      case Form::P1Diffusion:
+        launch_p1_diagonal(y, ld.macros.get(), nm, ld.lay.macro_stride, ld.lay.n, t.p1.get(), s);
+        break;
+      case Form::P1KDiffusion:
+        launch_p1k_diagonal(coeffs_[0]->data(level), y, ld.p1k_tasks.get(), ld.np1k_tasks, ld.lay.macro_stride,
+                            ld.lay.n, t.p1.get(), ld.macros.get(), s);
+        break;
+      case Form::N1CurlCurlMass: {
+        auto& cl = ctx_->level(Space::P1, level);
+        launch_n1_diagonal(y, coeffs_[0]->data(level), coeffs_[1]->data(level), ld.macros.get(), nm,
+                           ld.lay.macro_stride, ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, t.n1g.get(), s);
+        break;
+      }
+      default:
+        fail_internal("diagonal: unsupported form");
+    }
+  }
+  launch_interface_sum(y, ld.group_offsets.get(), ld.group_copies.get(), ld.groups.num_groups(), s, false);
+  if (ld.exchange) ld.exchange->run(y, s, false);
+}
+
 Operator::~Operator() {
   for (auto& e : events_) {
     cudaEventDestroy(e.first);

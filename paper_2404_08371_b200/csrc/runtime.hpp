@@ -163,6 +163,9 @@ public:
   Form form() const { return form_; }
   const FormInfo& info() const { return form_info(form_); }
   void apply(const Function& src, Function& dst, int level, Update upd);
+  // operator diagonal d_i = A_ii (every interface copy holds the full sum;
+  // Jacobi / Chebyshev smoothing, Jacobi-preconditioned CG)
+  void diagonal(Function& d, int level);
 
   // bench instrumentation: CUDA events around the element kernel (K1-K3)
   // on the context stream; stats() synchronizes and sums the durations.

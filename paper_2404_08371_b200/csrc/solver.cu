@@ -136,6 +136,16 @@ __global__ void __launch_bounds__(kThreads) xpby_kernel(double* __restrict__ y, 
     y[i] = fma(beta, y[i], x[i]);
 }
 
+// z = r / d where d != 0 (Jacobi preconditioner; Dirichlet carriers have r = 0)
+__global__ void __launch_bounds__(kThreads) jacobi_kernel(double* __restrict__ z, const double* __restrict__ r,
+                                                          const double* __restrict__ d, i64 count) {
+  for (i64 i = blockIdx.x * static_cast<i64>(kThreads) + threadIdx.x; i < count;
+       i += static_cast<i64>(kThreads) * gridDim.x) {
+    const double di = d[i];
+    z[i] = di != 0.0 ? r[i] / di : 0.0;
+  }
+}
+
 unsigned stream_grid(i64 count) {
   const i64 g = (count + kThreads - 1) / kThreads;
   return static_cast<unsigned>(g < 1 ? 1 : (g > 148 * 32 ? 148 * 32 : g));
@@ -161,6 +171,11 @@ void launch_sum_ordered(const double* d_values, int count, double* d_out, cudaSt
 void launch_mask_dirichlet(double* y, const SlotSpace& sp, const unsigned char* d_table, i64 count, cudaStream_t s) {
   mask_dirichlet_kernel<<<stream_grid(count), kThreads, 0, s>>>(y, sp, d_table, count);
   check_launch("mask_dirichlet");
+}
+
+void launch_jacobi(double* z, const double* r, const double* d, i64 count, cudaStream_t s) {
+  jacobi_kernel<<<stream_grid(count), kThreads, 0, s>>>(z, r, d, count);
+  check_launch("jacobi");
 }
 
 void launch_xpby(double* y, const double* x, double beta, i64 count, cudaStream_t s) {

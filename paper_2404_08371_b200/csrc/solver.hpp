@@ -30,6 +30,7 @@ void launch_masked_dot(const double* a, const double* b, const SlotSpace& sp, co
 void launch_sum_ordered(const double* d_values, int count, double* d_out, cudaStream_t s);
 void launch_mask_dirichlet(double* y, const SlotSpace& sp, const unsigned char* d_table, i64 count, cudaStream_t s);
 void launch_xpby(double* y, const double* x, double beta, i64 count, cudaStream_t s);
+void launch_jacobi(double* z, const double* r, const double* d, i64 count, cudaStream_t s);
 
 class Context;
 class Function;
@@ -47,7 +48,9 @@ struct CgResult {
 };
 // x: initial guess in, solution out (Dirichlet carriers forced to 0); b is
 // read-only (its Dirichlet carriers are ignored). Stops when
-// ||r_k|| <= rtol ||r_0|| or after max_iter iterations.
-CgResult cg_solve(Operator& op, const Function& b, Function& x, int level, double rtol, int max_iter);
+// ||r_k|| <= rtol ||r_0|| or after max_iter iterations. diag (optional): the
+// operator diagonal (Operator::diagonal) -> Jacobi-preconditioned CG.
+CgResult cg_solve(Operator& op, const Function& b, Function& x, int level, double rtol, int max_iter,
+                  const Function* diag = nullptr);
 
 } // namespace tetmf

@@ -205,3 +205,63 @@ def test_n1_manufactured_solution_converges(tm):
     print("N1 relative DoF errors", errs, "rates", rates)
     # at least first order (O(h) for ND1)
     assert min(rates[-2:]) > 0.9, (errs, rates)
+
+
+# ---- operator diagonal and Jacobi-preconditioned CG
+
+def _owner_values(tm, ctx, fn, space, level):
+    """Owner-copy values in reference numbering WITHOUT ND1 orientation signs
+    (a diagonal is invariant under basis sign flips)."""
+    ref, nd = ctx.ref_map(space, level)
+    raw = fn.download(level)
+    sel = (ref >= 0) & ((ref & 1) == 1)
+    out = np.full(nd, np.nan)
+    out[ref[sel] >> 2] = raw[sel]
+    return out
+
+
+@pytest.mark.parametrize("mesh,form,level", [("single-tet", "P1", 2), ("cube6", "P1", 2), ("cube6", "P1K", 2),
+                                             ("single-tet", "P1K", 2), ("cube6", "N1", 1), ("single-tet", "N1", 2),
+                                             ("cubes1x1x2", "N1", 1)])
+def test_diagonal_matches_probed_oracle(tm, tmp_path, mesh, form, level):
+    port_mesh = mesh
+    if mesh.startswith("cubes"):
+        dims = [int(v) for v in mesh[5:].split("x")]
+        port_mesh = str(tmp_path / "kuhn.mesh")
+        write_kuhn_mesh(port_mesh, *dims)
+    port = PortSystem(port_mesh, form, level)
+    c0, c1 = port.coefficients()
+    nd = port.num_dofs
+    want = np.empty(nd)
+    for i in range(nd):  # d_i = (A e_i)_i through the oracle's apply
+        e = np.zeros(nd)
+        e[i] = 1.0
+        w, _ = port.apply(e, c0, c1)
+        want[i] = w[i]
+    ctx = tm.Context(mesh, device=0)
+    op, sid = make_op(tm, ctx, form, level)
+    d = tm.Function(ctx, sid)
+    op.diagonal(d, level)
+    got = _owner_values(tm, ctx, d, sid, level)
+    assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+    assert (want > 0).all()
+
+
+@pytest.mark.parametrize("mesh,form,level", [("cube6", "N1", 3), ("single-tet", "P1K", 4), ("cubes2", "N1", 2)])
+def test_jacobi_pcg_recovers_known_solution(tm, mesh, form, level):
+    ctx = tm.Context(mesh, device=0)
+    op, sid = make_op(tm, ctx, form, level)
+    xs = tm.Function(ctx, sid)
+    xs.fill_seeded(level, 3, True)
+    b = tm.Function(ctx, sid)
+    op.apply(xs, b, level)
+    b.mask_dirichlet(level)
+    d = tm.Function(ctx, sid)
+    op.diagonal(d, level)
+    x_cg, x_pcg = tm.Function(ctx, sid), tm.Function(ctx, sid)
+    it_cg, _, ok_cg = op.cg_solve(b, x_cg, level, rtol=1e-12, max_iter=3000)
+    it_pcg, rel, ok = op.cg_solve(b, x_pcg, level, rtol=1e-12, max_iter=3000, diag=d)
+    print(mesh, form, level, "CG iterations", it_cg, "Jacobi-PCG iterations", it_pcg)
+    assert ok and ok_cg and rel <= 1e-12
+    want, got = xs.export_ref(level), x_pcg.export_ref(level)
+    assert np.abs(got - want).max() <= 1e-8 * np.abs(want).max()
