@@ -135,6 +135,12 @@ int tetmf_op_diagonal(tetmf_op* op, tetmf_fn* diag, int level);
 int tetmf_pcg_solve(tetmf_op* op, const tetmf_fn* b, tetmf_fn* x, const tetmf_fn* diag, int level, double rtol,
                     int max_iter, int* iterations, double* rel_residual, int* converged);
 
+/* P1 <-> ND1 discrete gradient (the transfer of the
+ * hybrid smoother): nd1 = G p1 with (G p)_e = p(tip) - p(base) along the
+ * edge (the ND1 interpolant of grad p); p1 = G^T nd1 (its transpose) */
+int tetmf_gradient(const tetmf_fn* p1, tetmf_fn* nd1, int level);
+int tetmf_gradient_transpose(const tetmf_fn* nd1, tetmf_fn* p1, int level);
+
 /* instrumentation: CUDA events around the element kernel of every apply on
  * the context stream (enable resets the totals); stats synchronize. */
 int tetmf_op_profile(tetmf_op* op, int enable);

@@ -101,6 +101,8 @@ _SIGS = {
     "tetmf_op_diagonal": (ctypes.c_int, [_c_vp, _c_vp, ctypes.c_int]),
     "tetmf_pcg_solve": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp, ctypes.c_int, ctypes.c_double, ctypes.c_int, _c_ip,
                                        _c_dp, _c_ip]),
+    "tetmf_gradient": (ctypes.c_int, [_c_vp, _c_vp, ctypes.c_int]),
+    "tetmf_gradient_transpose": (ctypes.c_int, [_c_vp, _c_vp, ctypes.c_int]),
     "tetmf_op_profile": (ctypes.c_int, [_c_vp, ctypes.c_int]),
     "tetmf_op_set_variant": (ctypes.c_int, [_c_vp, ctypes.c_int]),
     "tetmf_op_kernel_stats": (ctypes.c_int, [_c_vp, _c_dp, _c_i64p]),
@@ -407,6 +409,16 @@ class Operator:
         n = ctypes.c_int64()
         _check(lib().tetmf_op_kernel_stats(self._h, ctypes.byref(ms), ctypes.byref(n)))
         return ms.value, n.value
+
+
+def gradient(p1: Function, nd1: Function, level: int):
+    """nd1 = G p1: (G p)_e = p(tip) - p(base) (ND1 interpolant of grad p)."""
+    _check(lib().tetmf_gradient(p1.handle, nd1.handle, level))
+
+
+def gradient_transpose(nd1: Function, p1: Function, level: int):
+    """p1 = G^T nd1."""
+    _check(lib().tetmf_gradient_transpose(nd1.handle, p1.handle, level))
 
 
 def host_local_sum(offsets, copies, y):

@@ -346,6 +346,22 @@ int tetmf_pcg_solve(tetmf_op* op, const tetmf_fn* b, tetmf_fn* x, const tetmf_fn
   });
 }
 
+int tetmf_gradient(const tetmf_fn* p1, tetmf_fn* nd1, int level) {
+  return guard([&] {
+    need(p1, "p1");
+    need(nd1, "nd1");
+    gradient(*p1->impl, *nd1->impl, level);
+  });
+}
+
+int tetmf_gradient_transpose(const tetmf_fn* nd1, tetmf_fn* p1, int level) {
+  return guard([&] {
+    need(nd1, "nd1");
+    need(p1, "p1");
+    gradient_transpose(*nd1->impl, *p1->impl, level);
+  });
+}
+
 int tetmf_op_profile(tetmf_op* op, int enable) {
   return guard([&] {
     need(op, "op");

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <memory>
 
+#include "exchange.hpp"
 #include "runtime.hpp"
 #include "runtime_check.hpp"
 #include "solver.hpp"
@@ -57,6 +58,29 @@ void mask_dirichlet(Function& f, int level) {
   auto& ld = f.ctx().level(f.space(), level);
   if (ld.lay.macros.empty()) return;
   launch_mask_dirichlet(f.data(level), slot_space(ld), ld.slot_table.get(), ld.lay.total(), f.ctx().stream());
+}
+
+void gradient(const Function& p1, Function& nd1, int level) {
+  if (p1.space() != Space::P1 || nd1.space() != Space::ND1 || &p1.ctx() != &nd1.ctx())
+    fail_arg("gradient: expects a P1 and an ND1 function of one context");
+  Context& ctx = p1.ctx();
+  auto& le = ctx.level(Space::ND1, level);
+  auto& lp = ctx.level(Space::P1, level);
+  launch_gradient(p1.data(level), nd1.data(level), static_cast<int>(le.lay.macros.size()), le.lay.macro_stride,
+                  le.lay.class_stride, lp.lay.macro_stride, le.lay.n, ctx.stream());
+}
+
+void gradient_transpose(const Function& nd1, Function& p1, int level) {
+  if (p1.space() != Space::P1 || nd1.space() != Space::ND1 || &p1.ctx() != &nd1.ctx())
+    fail_arg("gradient_transpose: expects an ND1 and a P1 function of one context");
+  Context& ctx = p1.ctx();
+  auto& le = ctx.level(Space::ND1, level);
+  auto& lp = ctx.level(Space::P1, level);
+  double* y = p1.data(level);
+  launch_gradient_t(nd1.data(level), y, static_cast<int>(le.lay.macros.size()), le.lay.macro_stride,
+                    le.lay.class_stride, lp.lay.macro_stride, le.lay.n, le.slot_table.get(), ctx.stream());
+  launch_interface_sum(y, lp.group_offsets.get(), lp.group_copies.get(), lp.groups.num_groups(), ctx.stream());
+  if (lp.exchange) lp.exchange->run(y, ctx.stream());
 }
 
 CgResult cg_solve(Operator& op, const Function& b, Function& x, int level, double rtol, int max_iter,

@@ -90,6 +90,12 @@ void launch_n1_diagonal(double* d, const double* alpha, const double* beta, cons
                         i64 macro_stride, i64 class_stride, i64 coeff_stride, int n, const N1GramTable* d_gram,
                         cudaStream_t s);
 
+// P1 <-> ND1 discrete gradient and its transpose (k_transfer.cu)
+void launch_gradient(const double* phi, double* u, int nmacros, i64 stride_nd1, i64 class_stride, i64 stride_p1,
+                     int n, cudaStream_t s);
+void launch_gradient_t(const double* u, double* phi, int nmacros, i64 stride_nd1, i64 class_stride, i64 stride_p1,
+                       int n, const unsigned char* d_nd1_slot_table, cudaStream_t s);
+
 // FP64 DFMA-chain peak probe (used by bench.py to measure the FP64 roof).
 void launch_fp64_peak(double* out, int blocks, int threads, int iters, cudaStream_t s);
 

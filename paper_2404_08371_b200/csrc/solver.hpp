@@ -41,6 +41,10 @@ double masked_dot(const Function& a, const Function& b, int level);
 // zero the Dirichlet carriers of f
 void mask_dirichlet(Function& f, int level);
 
+// P1 <-> ND1 discrete gradient (k_transfer.cu): nd1 = G p1, p1 = G^T nd1
+void gradient(const Function& p1, Function& nd1, int level);
+void gradient_transpose(const Function& nd1, Function& p1, int level);
+
 struct CgResult {
   int iterations = 0;
   double rel_residual = 0.0;  // ||r_k|| / ||r_0|| (masked norm)

@@ -265,3 +265,45 @@ def test_jacobi_pcg_recovers_known_solution(tm, mesh, form, level):
     assert ok and ok_cg and rel <= 1e-12
     want, got = xs.export_ref(level), x_pcg.export_ref(level)
     assert np.abs(got - want).max() <= 1e-8 * np.abs(want).max()
+
+
+# ---- P1 <-> ND1 discrete gradient (hybrid-smoother transfer)
+
+@pytest.mark.parametrize("mesh,level", [("cube6", 3), ("cubes2", 2), ("single-tet", 4)])
+def test_gradient_transfer(tm, tmp_path, mesh, level):
+    port_mesh = mesh
+    if mesh.startswith("cubes"):
+        port_mesh = str(tmp_path / "kuhn.mesh")
+        write_kuhn_mesh(port_mesh, int(mesh[5:]))
+    ctx = tm.Context(mesh, device=0)
+    # (1) G of a linear field = exact edge differences (reference orientation)
+    _, p_xyz, _ = PortSystem(port_mesh, "P1", level).dof_geometry()
+    _, ea, eb = PortSystem(port_mesh, "N1", level).dof_geometry()
+    lin = lambda q: 0.3 * q[:, 0] - 1.7 * q[:, 1] + 2.2 * q[:, 2] + 0.5
+    phi = tm.Function(ctx, tm.SPACE_P1)
+    phi.import_ref(level, lin(p_xyz))
+    u = tm.Function(ctx, tm.SPACE_ND1)
+    tm.gradient(phi, u, level)
+    assert np.abs(u.export_ref(level) - (lin(eb) - lin(ea))).max() <= 1e-13
+    # (2) <G p, v> = <p, G^T v> for random p, v (reference numbering, full sums)
+    p = tm.Function(ctx, tm.SPACE_P1)
+    v = tm.Function(ctx, tm.SPACE_ND1)
+    p.fill_seeded(level, 21)
+    v.fill_seeded(level, 22)
+    gp = tm.Function(ctx, tm.SPACE_ND1)
+    gtv = tm.Function(ctx, tm.SPACE_P1)
+    tm.gradient(p, gp, level)
+    tm.gradient_transpose(v, gtv, level)
+    lhs = float(np.dot(gp.export_ref(level), v.export_ref(level)))
+    rhs = float(np.dot(p.export_ref(level), gtv.export_ref(level)))
+    assert abs(lhs - rhs) <= 1e-12 * np.abs(gp.export_ref(level) * v.export_ref(level)).sum()
+    # (3) curl grad = 0: the curl-curl operator annihilates G p
+    one, zero = tm.Function(ctx, tm.SPACE_P1), tm.Function(ctx, tm.SPACE_P1)
+    one.fill_coefficient(level, tm.COEFF_CONST, 1.0)
+    zero.fill_coefficient(level, tm.COEFF_CONST, 0.0)
+    curlcurl = tm.Operator(ctx, tm.FORM_N1, [one, zero])
+    w = tm.Function(ctx, tm.SPACE_ND1)
+    curlcurl.apply(gp, w, level)
+    wv = tm.Function(ctx, tm.SPACE_ND1)
+    curlcurl.apply(v, wv, level)
+    assert np.abs(w.export_ref(level)).max() <= 1e-12 * np.abs(wv.export_ref(level)).max()
