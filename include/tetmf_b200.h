@@ -141,6 +141,14 @@ int tetmf_pcg_solve(tetmf_op* op, const tetmf_fn* b, tetmf_fn* x, const tetmf_fn
 int tetmf_gradient(const tetmf_fn* p1, tetmf_fn* nd1, int level);
 int tetmf_gradient_transpose(const tetmf_fn* nd1, tetmf_fn* p1, int level);
 
+/* Chebyshev-Jacobi smoothing (the smoother of the paper's
+ * multigrid): *lambda_max = largest eigenvalue of D^-1 A
+ * (power iteration); degree Chebyshev steps on [lambda_max / eig_ratio,
+ * lambda_max] update x towards A x = b */
+int tetmf_estimate_lambda_max(tetmf_op* op, const tetmf_fn* diag, int level, int iterations, double* lambda_max);
+int tetmf_chebyshev_smooth(tetmf_op* op, const tetmf_fn* diag, const tetmf_fn* b, tetmf_fn* x, int level,
+                           int degree, double lambda_max, double eig_ratio);
+
 /* instrumentation: CUDA events around the element kernel of every apply on
  * the context stream (enable resets the totals); stats synchronize. */
 int tetmf_op_profile(tetmf_op* op, int enable);

@@ -103,6 +103,9 @@ _SIGS = {
                                        _c_dp, _c_ip]),
     "tetmf_gradient": (ctypes.c_int, [_c_vp, _c_vp, ctypes.c_int]),
     "tetmf_gradient_transpose": (ctypes.c_int, [_c_vp, _c_vp, ctypes.c_int]),
+    "tetmf_estimate_lambda_max": (ctypes.c_int, [_c_vp, _c_vp, ctypes.c_int, ctypes.c_int, _c_dp]),
+    "tetmf_chebyshev_smooth": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, _c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                              ctypes.c_double]),
     "tetmf_op_profile": (ctypes.c_int, [_c_vp, ctypes.c_int]),
     "tetmf_op_set_variant": (ctypes.c_int, [_c_vp, ctypes.c_int]),
     "tetmf_op_kernel_stats": (ctypes.c_int, [_c_vp, _c_dp, _c_i64p]),
@@ -392,6 +395,18 @@ class Operator:
             _check(lib().tetmf_pcg_solve(self._h, b.handle, x.handle, diag.handle, level, rtol, max_iter,
                                          ctypes.byref(it), ctypes.byref(rr), ctypes.byref(cv)))
         return it.value, rr.value, bool(cv.value)
+
+    def lambda_max(self, diag: Function, level: int, iterations: int = 30) -> float:
+        """Largest eigenvalue of D^-1 A (power iteration)."""
+        out = ctypes.c_double()
+        _check(lib().tetmf_estimate_lambda_max(self._h, diag.handle, level, iterations, ctypes.byref(out)))
+        return out.value
+
+    def chebyshev_smooth(self, diag: Function, b: Function, x: Function, level: int, degree: int,
+                         lambda_max: float, eig_ratio: float = 30.0):
+        """degree Chebyshev-Jacobi steps towards A x = b (x updated in place)."""
+        _check(lib().tetmf_chebyshev_smooth(self._h, diag.handle, b.handle, x.handle, level, degree, lambda_max,
+                                            eig_ratio))
 
     def diagonal(self, d: Function, level: int):
         """d = diag(A) (the assembled operator's diagonal; all copies hold the sum)."""

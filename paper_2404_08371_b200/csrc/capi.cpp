@@ -362,6 +362,26 @@ int tetmf_gradient_transpose(const tetmf_fn* nd1, tetmf_fn* p1, int level) {
   });
 }
 
+int tetmf_estimate_lambda_max(tetmf_op* op, const tetmf_fn* diag, int level, int iterations, double* lambda_max) {
+  return guard([&] {
+    need(op, "op");
+    need(diag, "diag");
+    need(lambda_max, "lambda_max");
+    *lambda_max = estimate_lambda_max(*op->impl, *diag->impl, level, iterations);
+  });
+}
+
+int tetmf_chebyshev_smooth(tetmf_op* op, const tetmf_fn* diag, const tetmf_fn* b, tetmf_fn* x, int level,
+                           int degree, double lambda_max, double eig_ratio) {
+  return guard([&] {
+    need(op, "op");
+    need(diag, "diag");
+    need(b, "b");
+    need(x, "x");
+    chebyshev_smooth(*op->impl, *diag->impl, *b->impl, *x->impl, level, degree, lambda_max, eig_ratio);
+  });
+}
+
 int tetmf_op_profile(tetmf_op* op, int enable) {
   return guard([&] {
     need(op, "op");

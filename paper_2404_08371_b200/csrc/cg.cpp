@@ -150,4 +150,70 @@ CgResult cg_solve(Operator& op, const Function& b, Function& x, int level, doubl
   return res;
 }
 
+double estimate_lambda_max(Operator& op, const Function& diag, int level, int iterations) {
+  const Space sp = op.info().trial;
+  if (diag.space() != sp || !diag.has_level(level)) fail_arg("lambda_max: diagonal not in the trial space");
+  if (iterations < 1) fail_arg("lambda_max: iterations must be >= 1");
+  Context& ctx = diag.ctx();
+  const cudaStream_t s = ctx.stream();
+  const i64 count = diag.size(level);
+  Function v(ctx, sp), q(ctx, sp), w(ctx, sp);
+  const double* D = diag.data(level);
+  v.fill_seeded(level, 0x5eedULL, true);
+  mask_dirichlet(v, level);
+  double lambda = 0.0;
+  for (int it = 0; it < iterations; ++it) {
+    op.apply(v, q, level, Update::Replace);  // q = A v
+    mask_dirichlet(q, level);
+    launch_mul(w.data(level), v.data(level), D, count, s);  // w = D v
+    const double vav = masked_dot(v, q, level), vdv = masked_dot(v, w, level);
+    if (!(vdv > 0.0)) fail_internal("lambda_max: degenerate start vector");
+    lambda = vav / vdv;
+    launch_jacobi(v.data(level), q.data(level), D, count, s);  // v = D^-1 A v
+    launch_mul(w.data(level), v.data(level), D, count, s);
+    const double nrm = std::sqrt(masked_dot(v, w, level));  // ||v||_D
+    if (!(nrm > 0.0)) break;
+    launch_scale(v.data(level), 1.0 / nrm, count, s);
+  }
+  return lambda;
+}
+
+void chebyshev_smooth(Operator& op, const Function& diag, const Function& b, Function& x, int level, int degree,
+                      double lambda_max, double eig_ratio) {
+  const Space sp = op.info().trial;
+  if (diag.space() != sp || b.space() != sp || x.space() != sp) fail_arg("chebyshev: functions not in the trial space");
+  if (degree < 1 || !(lambda_max > 0.0) || !(eig_ratio > 1.0)) fail_arg("chebyshev: bad degree / eigenvalue bounds");
+  Context& ctx = x.ctx();
+  const cudaStream_t s = ctx.stream();
+  const i64 count = x.size(level);
+  const double hi = lambda_max, lo = lambda_max / eig_ratio;
+  const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
+  Function r(ctx, sp), z(ctx, sp), d(ctx, sp), q(ctx, sp);
+  const double* D = diag.data(level);
+  double* X = x.data(level);
+  double* R = r.data(level);
+  double* Z = z.data(level);
+  double* Dd = d.data(level);
+  double* Q = q.data(level);
+  mask_dirichlet(x, level);
+  op.apply(x, q, level, Update::Replace);
+  TETMF_CUDA(cudaMemcpyAsync(R, b.data(level), sizeof(double) * count, cudaMemcpyDeviceToDevice, s));
+  launch_axpy(R, Q, -1.0, count, s);  // r = b - A x
+  mask_dirichlet(r, level);
+  launch_jacobi(Z, R, D, count, s);
+  launch_axpby(Dd, Z, 1.0 / theta, 0.0, count, s);  // d = z / theta
+  double rho = 1.0 / sigma;
+  for (int k = 0; k < degree; ++k) {
+    launch_axpy(X, Dd, 1.0, count, s);  // x += d
+    if (k + 1 == degree) break;
+    op.apply(d, q, level, Update::Replace);
+    mask_dirichlet(q, level);
+    launch_axpy(R, Q, -1.0, count, s);  // r -= A d
+    launch_jacobi(Z, R, D, count, s);
+    const double rho_new = 1.0 / (2.0 * sigma - rho);
+    launch_axpby(Dd, Z, 2.0 * rho_new / delta, rho_new * rho, count, s);  // d = rho' rho d + 2 rho' / delta z
+    rho = rho_new;
+  }
+}
+
 } // namespace tetmf

@@ -146,6 +146,29 @@ __global__ void __launch_bounds__(kThreads) jacobi_kernel(double* __restrict__ z
   }
 }
 
+// y = a x + b y
+__global__ void __launch_bounds__(kThreads) axpby_kernel(double* __restrict__ y, const double* __restrict__ x,
+                                                         double a, double b, i64 count) {
+  for (i64 i = blockIdx.x * static_cast<i64>(kThreads) + threadIdx.x; i < count;
+       i += static_cast<i64>(kThreads) * gridDim.x)
+    y[i] = fma(a, x[i], b * y[i]);
+}
+
+// y = a y
+__global__ void __launch_bounds__(kThreads) scale_kernel(double* __restrict__ y, double a, i64 count) {
+  for (i64 i = blockIdx.x * static_cast<i64>(kThreads) + threadIdx.x; i < count;
+       i += static_cast<i64>(kThreads) * gridDim.x)
+    y[i] *= a;
+}
+
+// z = x .* d
+__global__ void __launch_bounds__(kThreads) mul_kernel(double* __restrict__ z, const double* __restrict__ x,
+                                                       const double* __restrict__ d, i64 count) {
+  for (i64 i = blockIdx.x * static_cast<i64>(kThreads) + threadIdx.x; i < count;
+       i += static_cast<i64>(kThreads) * gridDim.x)
+    z[i] = x[i] * d[i];
+}
+
 unsigned stream_grid(i64 count) {
   const i64 g = (count + kThreads - 1) / kThreads;
   return static_cast<unsigned>(g < 1 ? 1 : (g > 148 * 32 ? 148 * 32 : g));
@@ -176,6 +199,21 @@ void launch_mask_dirichlet(double* y, const SlotSpace& sp, const unsigned char* 
 void launch_jacobi(double* z, const double* r, const double* d, i64 count, cudaStream_t s) {
   jacobi_kernel<<<stream_grid(count), kThreads, 0, s>>>(z, r, d, count);
   check_launch("jacobi");
+}
+
+void launch_axpby(double* y, const double* x, double a, double b, i64 count, cudaStream_t s) {
+  axpby_kernel<<<stream_grid(count), kThreads, 0, s>>>(y, x, a, b, count);
+  check_launch("axpby");
+}
+
+void launch_scale(double* y, double a, i64 count, cudaStream_t s) {
+  scale_kernel<<<stream_grid(count), kThreads, 0, s>>>(y, a, count);
+  check_launch("scale");
+}
+
+void launch_mul(double* z, const double* x, const double* d, i64 count, cudaStream_t s) {
+  mul_kernel<<<stream_grid(count), kThreads, 0, s>>>(z, x, d, count);
+  check_launch("mul");
 }
 
 void launch_xpby(double* y, const double* x, double beta, i64 count, cudaStream_t s) {

@@ -31,6 +31,9 @@ void launch_sum_ordered(const double* d_values, int count, double* d_out, cudaSt
 void launch_mask_dirichlet(double* y, const SlotSpace& sp, const unsigned char* d_table, i64 count, cudaStream_t s);
 void launch_xpby(double* y, const double* x, double beta, i64 count, cudaStream_t s);
 void launch_jacobi(double* z, const double* r, const double* d, i64 count, cudaStream_t s);
+void launch_axpby(double* y, const double* x, double a, double b, i64 count, cudaStream_t s);
+void launch_mul(double* z, const double* x, const double* d, i64 count, cudaStream_t s);
+void launch_scale(double* y, double a, i64 count, cudaStream_t s);
 
 class Context;
 class Function;
@@ -56,5 +59,15 @@ struct CgResult {
 // operator diagonal (Operator::diagonal) -> Jacobi-preconditioned CG.
 CgResult cg_solve(Operator& op, const Function& b, Function& x, int level, double rtol, int max_iter,
                   const Function* diag = nullptr);
+
+// Largest eigenvalue of D^-1 A on the interior carriers (power iteration with
+// the Rayleigh quotient <v, A v> / <v, D v>, seeded start vector).
+double estimate_lambda_max(Operator& op, const Function& diag, int level, int iterations);
+
+// Chebyshev-Jacobi smoother (the smoother of the reference paper's
+// multigrid): `degree` steps of the Chebyshev iteration for
+// D^-1 A targeting [lambda_max / eig_ratio, lambda_max]; x updated in place.
+void chebyshev_smooth(Operator& op, const Function& diag, const Function& b, Function& x, int level, int degree,
+                      double lambda_max, double eig_ratio);
 
 } // namespace tetmf

@@ -307,3 +307,59 @@ def test_gradient_transfer(tm, tmp_path, mesh, level):
     wv = tm.Function(ctx, tm.SPACE_ND1)
     curlcurl.apply(v, wv, level)
     assert np.abs(w.export_ref(level)).max() <= 1e-12 * np.abs(wv.export_ref(level)).max()
+
+
+# ---- Chebyshev-Jacobi smoothing
+
+@pytest.mark.parametrize("mesh,form,level", [("cube6", "P1", 2), ("cube6", "N1", 1), ("single-tet", "P1K", 2)])
+def test_lambda_max_matches_dense_eigenvalue(tm, mesh, form, level):
+    port = PortSystem(mesh, form, level)
+    c0, c1 = port.coefficients()
+    nd = port.num_dofs
+    A = np.empty((nd, nd))
+    for i in range(nd):
+        e = np.zeros(nd)
+        e[i] = 1.0
+        A[:, i], _ = port.apply(e, c0, c1)
+    I = port.interior().astype(bool)
+    Aii = A[np.ix_(I, I)]
+    want = float(np.max(np.linalg.eigvals(Aii / np.diag(Aii)[:, None]).real))
+    ctx = tm.Context(mesh, device=0)
+    op, sid = make_op(tm, ctx, form, level)
+    d = tm.Function(ctx, sid)
+    op.diagonal(d, level)
+    got = op.lambda_max(d, level, iterations=200)
+    assert got <= want * (1 + 1e-10) and got >= 0.97 * want, (got, want)
+
+
+def _energy_error(tm, op, ctx, sid, x, xs, level):
+    e, ae = tm.Function(ctx, sid), tm.Function(ctx, sid)
+    e.upload(level, x.download(level) - xs.download(level))
+    op.apply(e, ae, level)
+    return math.sqrt(e.dot(ae, level))
+
+
+@pytest.mark.parametrize("mesh,form,level,bound", [("cube6", "P1", 4, 0.5), ("cube6", "N1", 3, 1.0),
+                                                   ("single-tet", "P1K", 4, 0.5)])
+def test_chebyshev_smoother_reduces_energy_error(tm, mesh, form, level, bound):
+    ctx = tm.Context(mesh, device=0)
+    op, sid = make_op(tm, ctx, form, level)
+    xs = tm.Function(ctx, sid)
+    xs.fill_seeded(level, 3, True)
+    b = tm.Function(ctx, sid)
+    op.apply(xs, b, level)
+    b.mask_dirichlet(level)
+    d = tm.Function(ctx, sid)
+    op.diagonal(d, level)
+    lmax = 1.1 * op.lambda_max(d, level, iterations=30)
+    x = tm.Function(ctx, sid)
+    noise = tm.Function(ctx, sid)
+    noise.fill_seeded(level, 9, True)
+    x.upload(level, xs.download(level) + noise.download(level))
+    errs = [_energy_error(tm, op, ctx, sid, x, xs, level)]
+    for _ in range(3):
+        op.chebyshev_smooth(d, b, x, level, degree=4, lambda_max=lmax, eig_ratio=30.0)
+        errs.append(_energy_error(tm, op, ctx, sid, x, xs, level))
+    print(mesh, form, level, "energy errors", errs)
+    assert all(errs[i + 1] < errs[i] for i in range(3))
+    assert errs[1] < bound * errs[0]
