@@ -68,9 +68,11 @@ void launch_n1_cubes_v2(const N1DeviceTable* table, const N1GramTable* gram, int
                         i64 class_stride, i64 coeff_stride, int n, cudaStream_t s);
 // K3 default: folded cube walk (k_n1_fold.cu); same task-list / launch contract
 void build_n1_fold_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out);
-void launch_n1_fold(const N1GramTable* gram, int pass, const double* x, const double* alpha, const double* beta,
-                    double* y, const int* d_tasks, int ntasks, i64 macro_stride, i64 class_stride, i64 coeff_stride,
-                    int n, cudaStream_t s);
+void pad_n1_fold_tasks(std::vector<int>& tasks);
+void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, const double* x, const double* alpha,
+                    const double* beta, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
+                    i64 class_stride, i64 coeff_stride, int n, cudaStream_t s);
+int n1_kernel_mode();
 // K2 default: per-point gather over the 24 incident elements (k_p1k_gather.cu)
 void build_p1k_tasks(int nmacros, int n, std::vector<int>& out);
 void launch_p1k_gather(const double* x, const double* k, double* y, const int* d_tasks, int ntasks, i64 macro_stride,

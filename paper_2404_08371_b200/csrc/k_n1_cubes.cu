@@ -531,9 +531,7 @@ void launch_n1_cubes_v2(const N1DeviceTable* table, const N1GramTable* gram, int
   // A kernel-parameter constant-bank variant measured 3.3x slower (ptxas
   // either hoists and spills the constants or emits an indexed LDC each).
   const int mode = n1_kernel_mode();
-  if (mode == 3)
-    return launch_n1_fold(gram, pass, x, alpha, beta, y, d_tasks, ntasks, macro_stride, class_stride, coeff_stride,
-                          n, s);
+  if (mode == 3) fail_internal("n1 fold kernel: launched per pass by the runtime (launch_n1_fold)");
   auto go = [&](auto kern) {
     kern<<<grid, 32 * kWarps, 0, s>>>(gram, table, x, alpha, beta, y, tk, ntasks, macro_stride, class_stride,
                                       coeff_stride, n);

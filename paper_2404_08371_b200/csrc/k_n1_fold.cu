@@ -110,12 +110,17 @@ struct FoldIn {
 
 template <int PASS>
 __global__ void __launch_bounds__(32 * kWarps, TETMF_N1F_MIN_BLOCKS)
-n1_fold_kernel(const N1GramTable* __restrict__ gram, const double* __restrict__ xin,
-               const double* __restrict__ alpha, const double* __restrict__ beta, double* __restrict__ yout,
-               const FoldTask* __restrict__ tasks, int ntasks, i64 stride, i64 cstride, i64 cf_stride, int n) {
+n1_fold_kernel(const N1GramTable* __restrict__ gram, const MacroDesc* __restrict__ macros,
+               const double* __restrict__ xin, const double* __restrict__ alpha, const double* __restrict__ beta,
+               double* __restrict__ yout, const FoldTask* __restrict__ tasks, int ntasks, i64 stride, i64 cstride,
+               i64 cf_stride, int n) {
   extern __shared__ __align__(16) double dsm[];
   N1GramTable& sg = *reinterpret_cast<N1GramTable*>(dsm);
-  for (int i = threadIdx.x; i < 6 * kGramRow; i += blockDim.x) (&sg.o[0][0])[i] = __ldg(&gram->o[0][0] + i);
+  // one launch covers every geometry group of a pass; task lists are padded
+  // per group to whole CTAs, so the CTA's first task (always real) names
+  // the group of all its warps
+  const N1GramTable* gt = gram + macros[tasks[blockIdx.x * kWarps].macro].group;
+  for (int i = threadIdx.x; i < 6 * kGramRow; i += blockDim.x) (&sg.o[0][0])[i] = __ldg(&gt->o[0][0] + i);
   const int lane = threadIdx.x & 31;
   double* ring = dsm + sizeof(N1GramTable) / sizeof(double) + (threadIdx.x >> 5) * kWarpSmem;
   for (int i = lane; i < kRing; i += 32) ring[i] = 0.0;  // unfilled positions must read finite
@@ -124,6 +129,7 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram, const double* __restrict__ 
   const int warp = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (warp >= ntasks) return;
   const FoldTask tk = tasks[warp];
+  if (tk.macro < 0) return;  // padding task
   const int z = tk.z, m = n - 1, L = n - 1 - z;
   const int K = (L + 1) / kSeg;  // full segments of the layer (a partial one walks alone)
   const int kn = tk.k, kf = K - 1 - kn;
@@ -373,9 +379,20 @@ void build_n1_fold_tasks(const std::vector<int>& local_macros, int n, int parity
   }
 }
 
-void launch_n1_fold(const N1GramTable* gram, int pass, const double* x, const double* alpha, const double* beta,
-                    double* y, const int* d_tasks, int ntasks, i64 macro_stride, i64 class_stride, i64 coeff_stride,
-                    int n, cudaStream_t s) {
+// Padding of one group's task list to whole CTAs (dummy tasks macro = -1).
+void pad_n1_fold_tasks(std::vector<int>& tasks) {
+  while ((tasks.size() / 4) % kWarps) {
+    tasks.push_back(-1);
+    tasks.push_back(0);
+    tasks.push_back(0);
+    tasks.push_back(0);
+  }
+}
+
+// gram: tables of all geometry groups; macros: local macro descriptors
+void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, const double* x, const double* alpha,
+                    const double* beta, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
+                    i64 class_stride, i64 coeff_stride, int n, cudaStream_t s) {
   if (ntasks == 0) return;
   constexpr int smem = static_cast<int>(sizeof(N1GramTable) + sizeof(double) * kWarpSmem * kWarps);
   static const bool attr = [] {
@@ -386,8 +403,8 @@ void launch_n1_fold(const N1GramTable* gram, int pass, const double* x, const do
   (void)attr;
   const unsigned grid = static_cast<unsigned>((ntasks + kWarps - 1) / kWarps);
   auto kern = pass == 0 ? n1_fold_kernel<0> : n1_fold_kernel<1>;
-  kern<<<grid, 32 * kWarps, smem, s>>>(gram, x, alpha, beta, y, reinterpret_cast<const FoldTask*>(d_tasks), ntasks,
-                                       macro_stride, class_stride, coeff_stride, n);
+  kern<<<grid, 32 * kWarps, smem, s>>>(gram, macros, x, alpha, beta, y, reinterpret_cast<const FoldTask*>(d_tasks),
+                                       ntasks, macro_stride, class_stride, coeff_stride, n);
   check_launch("n1_fold");
 }
 

@@ -163,6 +163,21 @@ Context::LevelData& Context::level(Space s, int level) {
     }
     ld->ntasks = static_cast<int>(all.size() / 4);
     ld->tasks.upload(all.data(), all.size(), stream_);
+    if (n1_kernel_mode() == 3) {
+      std::vector<int> merged;
+      for (int pass = 0; pass < 2; ++pass) {
+        ld->fold_range[2 * pass] = static_cast<int>(merged.size() / 4);
+        for (int g = 0; g < ngroups_; ++g) {
+          const auto& gt = ld->group_tasks[g];
+          std::vector<int> part(all.begin() + 4 * gt[2 * pass], all.begin() + 4 * (gt[2 * pass] + gt[2 * pass + 1]));
+          if (part.empty()) continue;
+          pad_n1_fold_tasks(part);
+          merged.insert(merged.end(), part.begin(), part.end());
+        }
+        ld->fold_range[2 * pass + 1] = static_cast<int>(merged.size() / 4) - ld->fold_range[2 * pass];
+      }
+      ld->fold_tasks.upload(merged.data(), merged.size(), stream_);
+    }
   }
   {
     // solver slot classes (solver.cu): interior = not in a boundary face plane
@@ -390,6 +405,11 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
       if (kernel_variant_ == 1) {
         launch_n1_cubes(x, coeffs_[0]->data(level), coeffs_[1]->data(level), y, ld.macros.get(), nm,
                         ld.lay.macro_stride, ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, t.n1.get(), s);
+      } else if (n1_kernel_mode() == 3) {
+        for (int pass = 0; pass < 2; ++pass)
+          launch_n1_fold(t.n1g.get(), ld.macros.get(), pass, x, coeffs_[0]->data(level), coeffs_[1]->data(level), y,
+                         ld.fold_tasks.get() + 4 * ld.fold_range[2 * pass], ld.fold_range[2 * pass + 1],
+                         ld.lay.macro_stride, ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, s);
       } else {
         for (int pass = 0; pass < 2; ++pass)
           for (std::size_t g = 0; g < ld.group_tasks.size(); ++g) {

@@ -113,6 +113,9 @@ public:
     DeviceBuffer<double> dot_scratch;
     // ND1: task ranges (offset, count) per (geometry group, parity pass)
     std::vector<std::array<int, 4>> group_tasks;  // {offset0, count0, offset1, count1}
+    // ND1, folded kernel: per pass, all groups' tasks padded to whole CTAs
+    DeviceBuffer<int> fold_tasks;
+    std::array<int, 4> fold_range{0, 0, 0, 0};    // {offset0, count0, offset1, count1}
   };
   LevelData& level(Space s, int level);
   LevelData& ref_level(Space s, int level);  // level() + reference numbering
