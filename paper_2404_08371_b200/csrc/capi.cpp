@@ -153,7 +153,7 @@ int tetmf_fn_create(tetmf_ctx* ctx, int space, tetmf_fn** out) {
     need(ctx, "ctx");
     need(out, "out");
     const Space s = space_of(space);
-    if (s == Space::P2) fail_arg("P2 functions are not implemented (SURVEY.md 8(f) next item)");
+
     auto f = std::make_unique<tetmf_fn>();
     f->impl = std::make_unique<Function>(*ctx->impl, s);
     *out = f.release();

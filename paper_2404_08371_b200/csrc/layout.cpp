@@ -15,8 +15,7 @@ namespace tetmf {
 
 LevelLayout LevelLayout::make(Space s, int level, int num_macros_global, const std::vector<int>& macros) {
   if (level < 0 || level > 14) fail_arg("level out of range (0..14)");
-  if (s == Space::P2) fail_arg("P2 storage is not implemented (out of scope, DESIGN.md)");
-  if (s == Space::ND1 && level < 1) fail_arg("ND1 storage requires level >= 1");
+  if ((s == Space::ND1 || s == Space::P2) && level < 1) fail_arg("ND1 / P2 storage requires level >= 1");
   LevelLayout l;
   l.space = s;
   l.level = level;
@@ -26,7 +25,7 @@ LevelLayout LevelLayout::make(Space s, int level, int num_macros_global, const s
     l.macro_stride = round_up(tet_count(l.n), 32);
   } else {
     l.class_stride = round_up(tet_count(l.n - 1), 32);
-    l.macro_stride = 7 * l.class_stride;
+    l.macro_stride = 7 * l.class_stride + (s == Space::P2 ? p2_vertex_stride(l.n) : 0);
   }
   l.macros = macros;
   std::sort(l.macros.begin(), l.macros.end());
@@ -61,16 +60,17 @@ namespace {
 template <typename F>
 void point_carriers(Space s, int n, i64 cs, int x, int y, int z, F&& f) {
   const unsigned mb = support_mask(bary(n, x, y, z));
-  if (s == Space::P1) {
+  if (s == Space::P1 || s == Space::P2) {
     f(-1, mb, std::array<int, 3>{x, y, z}, lattice_index(n, x, y, z));
-    return;
+    if (s == Space::P1) return;
   }
+  const i64 eoff = s == Space::P2 ? p2_vertex_stride(n) : 0;
   for (int c = 0; c < 7; ++c) {
     const int tx = x + kEdgeDir[c][0], ty = y + kEdgeDir[c][1], tz = z + kEdgeDir[c][2];
     if (tx < 0 || ty < 0 || tz < 0 || tx + ty + tz > n) continue;
     const Off3 b = edge_base_from_anchor(c);
     const std::array<int, 3> a = {x - b.x, y - b.y, z - b.z};
-    f(c, mb | support_mask(bary(n, tx, ty, tz)), a, c * cs + lattice_index(n - 1, a[0], a[1], a[2]));
+    f(c, mb | support_mask(bary(n, tx, ty, tz)), a, eoff + c * cs + lattice_index(n - 1, a[0], a[1], a[2]));
   }
 }
 
@@ -193,7 +193,10 @@ Mapped map_carrier(const MacroMesh& mesh, const LevelLayout& lay, int m, int cls
   const int c2 = edge_class_of(t2[0] - b2[0], t2[1] - b2[1], t2[2] - b2[2], &flipped);
   if (c2 < 0) fail_internal("map_carrier: not a lattice edge after mapping");
   const std::array<int, 3> a2 = {std::min(b2[0], t2[0]), std::min(b2[1], t2[1]), std::min(b2[2], t2[2])};
-  return {a2[0], a2[1], a2[2], c2, c2 * lay.class_stride + lattice_index(n - 1, a2[0], a2[1], a2[2]), flipped};
+  const bool p2 = lay.space == Space::P2;  // P2 edge DoFs are unsigned
+  return {a2[0], a2[1], a2[2], c2,
+          (p2 ? p2_vertex_stride(n) : 0) + c2 * lay.class_stride + lattice_index(n - 1, a2[0], a2[1], a2[2]),
+          p2 ? false : flipped};
 }
 
 // unshifted base (record coordinates) of a carrier given its anchor
@@ -270,7 +273,7 @@ RefNumbering build_ref_numbering(const MacroMesh& mesh, const Topology& topo, co
     for (int c = 0; c < 7; ++c) signCache[c] = -1;
     for_each_carrier(lay.space, n, [&](const Carrier& c) {
       bool neg = false;
-      if (c.cls >= 0) {
+      if (c.cls >= 0 && lay.space == Space::ND1) {  // P2 edge DoFs carry no orientation
         std::array<int, 3> b, t;
         edge_endpoints(c.cls, {c.x, c.y, c.z}, b, t);
         const bool inner = support_mask(bary(n, b[0], b[1], b[2])) == 15u &&

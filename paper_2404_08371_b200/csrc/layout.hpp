@@ -64,6 +64,10 @@ bool carrier_interior(const Topology& topo, int m, int n, const Carrier& c);
 
 // Visits every carrier of macro m in the reference's record order
 // (z, y, x, kindClass) with the unshifted base point (fespace.cpp:236-281).
+// P2 storage: the vertex block (P1 layout) then the 7 edge-class blocks (ND1
+// layout), both 32-padded; edge DoFs are unsigned (midpoint values).
+inline i64 p2_vertex_stride(int n) { return round_up(tet_count(n), 32); }
+
 template <typename F>
 void for_each_carrier(Space s, int n, F&& f) {
   if (s == Space::P1) {
@@ -75,17 +79,19 @@ void for_each_carrier(Space s, int n, F&& f) {
     return;
   }
   const i64 cs = round_up(tet_count(n - 1), 32);
+  const i64 eoff = s == Space::P2 ? p2_vertex_stride(n) : 0;  // edge blocks follow the P2 vertex block
   for (int z = 0; z <= n; ++z)
     for (int y = 0; y <= n - z; ++y)
       for (int x = 0; x <= n - z - y; ++x) {
         const unsigned mb = support_mask(bary(n, x, y, z));
+        if (s == Space::P2) f(Carrier{lattice_index(n, x, y, z), x, y, z, -1, mb});  // kindClass 0 first
         for (int c = 0; c < 7; ++c) {
           const int tx = x + kEdgeDir[c][0], ty = y + kEdgeDir[c][1], tz = z + kEdgeDir[c][2];
           if (tx < 0 || ty < 0 || tz < 0 || tx + ty + tz > n) continue;
           const Off3 b = edge_base_from_anchor(c);
           const int ax = x - b.x, ay = y - b.y, az = z - b.z;
           const unsigned mask = mb | support_mask(bary(n, tx, ty, tz));
-          f(Carrier{c * cs + lattice_index(n - 1, ax, ay, az), ax, ay, az, c, mask});
+          f(Carrier{eoff + c * cs + lattice_index(n - 1, ax, ay, az), ax, ay, az, c, mask});
         }
       }
 }

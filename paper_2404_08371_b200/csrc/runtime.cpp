@@ -147,7 +147,7 @@ Context::LevelData& Context::level(Space s, int level) {
     build_p1k_tasks(static_cast<int>(macros_.size()), n, tasks);
     ld->np1k_tasks = static_cast<int>(tasks.size() / 4);
     ld->p1k_tasks.upload(tasks.data(), tasks.size(), stream_);
-  } else {
+  } else if (s == Space::ND1) {
     std::vector<int> all, part;
     ld->group_tasks.assign(ngroups_, {0, 0, 0, 0});
     for (int g = 0; g < ngroups_; ++g) {

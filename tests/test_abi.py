@@ -66,10 +66,15 @@ def slot_geometry(ctx, space, level, mesh):
             pts = lattice_points(n)
             out.append((li * ms + np.arange(len(pts)), v0 + pts @ E / n, None))
         else:
+            eoff = 0
+            if space == 1:  # P2: vertex block (32-padded) before the edge blocks
+                pts = lattice_points(n)
+                out.append((li * ms + np.arange(len(pts)), v0 + pts @ E / n, None))
+                eoff = -(-len(pts) // 32) * 32
             for c in range(7):
                 pts = lattice_points(n - 1)
                 valid = np.ones(len(pts), bool) if c < 6 else pts.sum(1) <= n - 2
-                idx = li * ms + c * cs + np.arange(len(pts))
+                idx = li * ms + eoff + c * cs + np.arange(len(pts))
                 P = pts + BASE[c]
                 out.append((idx[valid], (v0 + P @ E / n)[valid], (v0 + (P + DIRS[c]) @ E / n)[valid]))
     return out
@@ -122,7 +127,36 @@ def test_dirichlet_mask_matches_reference_interior(tm, tmp_path, mesh, form):
     assert np.array_equal(got, want), (int((got != want).sum()), got.size)
 
 
-@pytest.mark.parametrize("space", [0, 2])
+@pytest.mark.parametrize("mesh", ["single-tet", "cube6"])
+@pytest.mark.parametrize("level", [1, 2, 3])
+def test_p2_ref_numbering_matches_reference_geometry(tm, mesh, level):
+    """P2 (the P2V form's space): vertex + unsigned edge-midpoint DoFs in the
+    reference's record order (fespace.cpp:233-307), against the fixed
+    reference build's DoF geometry."""
+    from oracle.refapi import RefSystem
+    ctx = tm.Context(mesh, device=-1)
+    m, nd = ctx.ref_map(tm.SPACE_P2, level)
+    ref = RefSystem(mesh, "P2V", level)
+    assert nd == ref.num_dofs
+    kind, a, b = ref.dof_geometry()
+    owners = np.zeros(nd, int)
+    for idx, base, tip in slot_geometry(ctx, tm.SPACE_P2, level, mesh):
+        e = m[idx]
+        assert (e >= 0).all()
+        assert not (e & 2).any()  # no orientation signs on P2 edges
+        ids = e >> 2
+        if tip is None:
+            assert (kind[ids] == 0).all() and np.allclose(a[ids], base)
+        else:
+            assert (kind[ids] == 1).all()
+            same = np.isclose(a[ids], base).all(1) & np.isclose(b[ids], tip).all(1)
+            swap = np.isclose(a[ids], tip).all(1) & np.isclose(b[ids], base).all(1)
+            assert (same | swap).all()
+        np.add.at(owners, ids[(e & 1) == 1], 1)
+    assert (owners == 1).all()
+
+
+@pytest.mark.parametrize("space", [0, 1, 2])
 def test_interface_groups_are_geometric_copies(tm, space):
     ctx = tm.Context("cube6", device=-1)
     level = 3
@@ -145,7 +179,11 @@ def test_interface_groups_are_geometric_copies(tm, space):
             a0, b0 = geo[st[0], :3], geo[st[0], 3:]
             if neg[0]:
                 a0, b0 = b0, a0
-            assert np.allclose(a, a0) and np.allclose(b, b0)
+            if space == 1:  # P2 edge DoFs are unsigned: same carrier, any direction, no sign
+                assert not neg.any()
+                assert (np.allclose(a, a0) and np.allclose(b, b0)) or (np.allclose(a, b0) and np.allclose(b, a0))
+            else:
+                assert np.allclose(a, a0) and np.allclose(b, b0)
 
 
 @pytest.mark.parametrize("mesh", ["single-tet", "cube6"])
@@ -201,11 +239,9 @@ def test_error_model(tm):
         tm.Context("no-such-mesh-file", device=-1)
     ctx = tm.Context("cube6", device=-1)
     with pytest.raises(tm.InvalidArgument):
-        tm.Function(ctx, tm.SPACE_P2)
-    with pytest.raises(tm.InvalidArgument):
         tm.Operator(ctx, tm.FORM_N1, [])           # N1 expects 2 coefficient fields
     with pytest.raises(tm.InvalidArgument):
-        tm.Operator(ctx, tm.FORM_P2V, [])
+        tm.Operator(ctx, tm.FORM_P2V, [])          # P2V expects k in P2
     x = tm.Function(ctx, tm.SPACE_P1)
     e = tm.Function(ctx, tm.SPACE_ND1)
     with pytest.raises(tm.InvalidArgument):
