@@ -251,7 +251,7 @@ class Context:
                 "send_index": si[: ns.value], "group_offsets": go, "group_entries": ge[: ne.value]}
 
     def local_matrix(self, form: int, level: int, macro: int, orientation: int, c0=None, c1=None) -> np.ndarray:
-        nloc = 6 if form == FORM_N1 else 4
+        nloc = 6 if form == FORM_N1 else (10 if form == FORM_P2V else 4)
         out = np.empty(nloc * nloc)
         a = None if c0 is None else np.ascontiguousarray(c0, dtype=np.float64)
         b = None if c1 is None else np.ascontiguousarray(c1, dtype=np.float64)

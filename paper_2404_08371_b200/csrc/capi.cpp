@@ -558,6 +558,15 @@ int tetmf_plan_local_matrix(tetmf_ctx* ctx, int form, int level, int macro, int 
       }
       for (int j = 0; j < 4; ++j)
         for (int i = 0; i < 4; ++i) out[j * 4 + i] = kb * t.K[orientation][sym4(i, j)];
+    } else if (form == TETMF_FORM_P2V) {
+      need(c0, "k");  // k at the element's 10 local P2 DoFs (vertices, then edges)
+      const P2VTable t = p2v_table(c.mesh(), macro, level);
+      for (int j = 0; j < 10; ++j)
+        for (int i = 0; i < 10; ++i) {
+          double a = 0.0;
+          for (int m = 0; m < 10; ++m) a += c0[m] * t.T[orientation][m][sym10(i, j)];
+          out[j * 10 + i] = a;
+        }
     } else {
       fail_arg("plan_local_matrix: unsupported form");
     }

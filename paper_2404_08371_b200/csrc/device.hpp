@@ -33,10 +33,12 @@ struct CoeffSpec {
   double value;      // for which == 3
 };
 
+// space: 0 P1, 1 P2, 2 ND1 (Space enum values)
 void launch_fill_seeded(double* out, const MacroDesc* d_macros, int nmacros, i64 macro_stride, int n,
-                        bool nd1, i64 class_stride, std::uint64_t seed, bool dirichlet, cudaStream_t s);
+                        int space, i64 class_stride, std::uint64_t seed, bool dirichlet, cudaStream_t s);
+// P1 (class_stride 0) or P2 (class_stride > 0: vertex block + edge midpoints)
 void launch_fill_coeff(double* out, const MacroDesc* d_macros, int nmacros, i64 macro_stride, int n,
-                       CoeffSpec spec, cudaStream_t s);
+                       CoeffSpec spec, cudaStream_t s, i64 class_stride = 0);
 void launch_import_ref(double* lat, const i64* map, i64 total, const double* ref, cudaStream_t s);
 void launch_export_ref(const double* lat, const i64* map, i64 total, double* ref, cudaStream_t s);
 void launch_interface_sum(double* y, const i64* offsets, const i64* copies, i64 ngroups, cudaStream_t s,

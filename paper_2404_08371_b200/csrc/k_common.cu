@@ -60,12 +60,15 @@ __device__ unsigned support_mask_dev(int n, int x, int y, int z) {
   return (n - x - y - z > 0 ? 1u : 0u) | (x > 0 ? 2u : 0u) | (y > 0 ? 4u : 0u) | (z > 0 ? 8u : 0u);
 }
 
-__global__ void fill_seeded_p1_kernel(double* out, const MacroDesc* macros, int nmacros, i64 stride, int n,
-                                      std::uint64_t seed, bool dirichlet) {
+// region: entries per macro this fill covers (the P2 vertex block, or the
+// whole P1 block); stride: entries per macro of the function
+__global__ void fill_seeded_p1_kernel(double* out, const MacroDesc* macros, int nmacros, i64 stride, i64 region,
+                                      int n, std::uint64_t seed, bool dirichlet) {
   const i64 tid = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
-  if (tid >= stride * nmacros) return;
-  const int li = static_cast<int>(tid / stride);
-  const i64 slot = tid - li * stride;
+  if (tid >= region * nmacros) return;
+  const int li = static_cast<int>(tid / region);
+  const i64 slot = tid - li * region;
+  out += static_cast<i64>(li) * stride - static_cast<i64>(li) * region;  // out[tid] = macro li, slot
   const MacroDesc& m = macros[li];
   int x, y, z;
   if (!decode_lattice(n, slot, x, y, z)) {
@@ -81,12 +84,15 @@ __global__ void fill_seeded_p1_kernel(double* out, const MacroDesc* macros, int 
   out[tid] = seeded_uniform(seed, key_hash_vertex(W[0], W[1], W[2]));
 }
 
-__global__ void fill_seeded_nd1_kernel(double* out, const MacroDesc* macros, int nmacros, i64 stride,
-                                       i64 cstride, int n, std::uint64_t seed, bool dirichlet) {
+// unsigned_edges (P2 midpoint DoFs): the value of the key-ascending edge,
+// whatever the storage direction; ND1: signed along the storage direction
+__global__ void fill_seeded_nd1_kernel(double* out, const MacroDesc* macros, int nmacros, i64 stride, i64 region,
+                                       i64 cstride, int n, std::uint64_t seed, bool dirichlet, bool unsigned_edges) {
   const i64 tid = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
-  if (tid >= stride * nmacros) return;
-  const int li = static_cast<int>(tid / stride);
-  const i64 r = tid - li * stride;
+  if (tid >= region * nmacros) return;
+  const int li = static_cast<int>(tid / region);
+  const i64 r = tid - li * region;
+  out += static_cast<i64>(li) * stride - static_cast<i64>(li) * region;
   const int c = static_cast<int>(r / cstride);
   const i64 slot = r - c * cstride;
   const MacroDesc& m = macros[li];
@@ -111,7 +117,7 @@ __global__ void fill_seeded_nd1_kernel(double* out, const MacroDesc* macros, int
   if (lex_less(B[0], B[1], B[2], T[0], T[1], T[2]))
     v = seeded_uniform(seed, key_hash_edge(B[0], B[1], B[2], T[0], T[1], T[2]));
   else
-    v = -seeded_uniform(seed, key_hash_edge(T[0], T[1], T[2], B[0], B[1], B[2]));
+    v = seeded_uniform(seed, key_hash_edge(T[0], T[1], T[2], B[0], B[1], B[2])) * (unsigned_edges ? 1.0 : -1.0);
   out[tid] = v;
 }
 
@@ -124,12 +130,13 @@ __device__ double coeff_value(int which, double c, const double P[3]) {
   }
 }
 
-__global__ void fill_coeff_kernel(double* out, const MacroDesc* macros, int nmacros, i64 stride, int n,
+__global__ void fill_coeff_kernel(double* out, const MacroDesc* macros, int nmacros, i64 stride, i64 region, int n,
                                   CoeffSpec spec) {
   const i64 tid = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
-  if (tid >= stride * nmacros) return;
-  const int li = static_cast<int>(tid / stride);
-  const i64 slot = tid - li * stride;
+  if (tid >= region * nmacros) return;
+  const int li = static_cast<int>(tid / region);
+  const i64 slot = tid - li * region;
+  out += static_cast<i64>(li) * stride - static_cast<i64>(li) * region;
   int x, y, z;
   if (!decode_lattice(n, slot, x, y, z)) {
     out[tid] = 0.0;
@@ -137,6 +144,30 @@ __global__ void fill_coeff_kernel(double* out, const MacroDesc* macros, int nmac
   }
   double P[3];
   world_pos(macros[li], n, x, y, z, P);
+  out[tid] = coeff_value(spec.which, spec.value, P);
+}
+
+// P2 coefficient edge DoFs: nodal value at the edge midpoint (fespace.cpp:
+// 494-506)
+__global__ void fill_coeff_edges_kernel(double* out, const MacroDesc* macros, int nmacros, i64 stride, i64 region,
+                                        i64 cstride, int n, CoeffSpec spec) {
+  const i64 tid = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (tid >= region * nmacros) return;
+  const int li = static_cast<int>(tid / region);
+  const i64 r = tid - li * region;
+  out += static_cast<i64>(li) * stride - static_cast<i64>(li) * region;
+  const int c = static_cast<int>(r / cstride);
+  int ax, ay, az;
+  if (c >= 7 || !decode_lattice(n - 1, r - c * cstride, ax, ay, az) || (c == 6 && ax + ay + az > n - 2)) {
+    out[tid] = 0.0;
+    return;
+  }
+  const Off3 bo = edge_base_from_anchor(c), dc = edge_dir(c);
+  const int bx = ax + bo.x, by = ay + bo.y, bz = az + bo.z;
+  double PB[3], PT[3];
+  world_pos(macros[li], n, bx, by, bz, PB);
+  world_pos(macros[li], n, bx + dc.x, by + dc.y, bz + dc.z, PT);
+  const double P[3] = {0.5 * (PB[0] + PT[0]), 0.5 * (PB[1] + PT[1]), 0.5 * (PB[2] + PT[2])};
   out[tid] = coeff_value(spec.which, spec.value, P);
 }
 
@@ -204,23 +235,37 @@ __global__ void fp64_peak_kernel(double* out, int iters) {
 
 } // namespace
 
-void launch_fill_seeded(double* out, const MacroDesc* d_macros, int nmacros, i64 macro_stride, int n, bool nd1,
+// space: 0 P1, 1 P2 (vertex block + unsigned edge blocks), 2 ND1
+void launch_fill_seeded(double* out, const MacroDesc* d_macros, int nmacros, i64 macro_stride, int n, int space,
                         i64 class_stride, std::uint64_t seed, bool dirichlet, cudaStream_t s) {
-  const i64 total = macro_stride * nmacros;
-  if (nd1)
-    fill_seeded_nd1_kernel<<<grid_for(total), kThreads, 0, s>>>(out, d_macros, nmacros, macro_stride,
-                                                                 class_stride, n, seed, dirichlet);
-  else
-    fill_seeded_p1_kernel<<<grid_for(total), kThreads, 0, s>>>(out, d_macros, nmacros, macro_stride, n, seed,
-                                                                dirichlet);
-  check_launch("fill_seeded");
+  const i64 vstride = space == 2 ? 0 : (space == 1 ? ((tet_count(n) + 31) / 32 * 32) : macro_stride);
+  if (vstride > 0) {
+    fill_seeded_p1_kernel<<<grid_for(vstride * nmacros), kThreads, 0, s>>>(out, d_macros, nmacros, macro_stride,
+                                                                            vstride, n, seed, dirichlet);
+    check_launch("fill_seeded");
+  }
+  if (space != 0) {
+    const i64 region = 7 * class_stride;
+    fill_seeded_nd1_kernel<<<grid_for(region * nmacros), kThreads, 0, s>>>(
+        out + vstride, d_macros, nmacros, macro_stride, region, class_stride, n, seed, dirichlet, space == 1);
+    check_launch("fill_seeded");
+  }
 }
 
+// P1 (class_stride 0) or P2 coefficient functions
 void launch_fill_coeff(double* out, const MacroDesc* d_macros, int nmacros, i64 macro_stride, int n,
-                       CoeffSpec spec, cudaStream_t s) {
-  const i64 total = macro_stride * nmacros;
-  fill_coeff_kernel<<<grid_for(total), kThreads, 0, s>>>(out, d_macros, nmacros, macro_stride, n, spec);
+                       CoeffSpec spec, cudaStream_t s, i64 class_stride) {
+  const i64 vstride = class_stride > 0 ? ((tet_count(n) + 31) / 32 * 32) : macro_stride;
+  fill_coeff_kernel<<<grid_for(vstride * nmacros), kThreads, 0, s>>>(out, d_macros, nmacros, macro_stride, vstride,
+                                                                      n, spec);
   check_launch("fill_coeff");
+  if (class_stride > 0) {
+    const i64 region = 7 * class_stride;
+    fill_coeff_edges_kernel<<<grid_for(region * nmacros), kThreads, 0, s>>>(out + vstride, d_macros, nmacros,
+                                                                            macro_stride, region, class_stride, n,
+                                                                            spec);
+    check_launch("fill_coeff");
+  }
 }
 
 void launch_import_ref(double* lat, const i64* map, i64 total, const double* ref, cudaStream_t s) {

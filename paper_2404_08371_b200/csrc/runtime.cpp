@@ -250,17 +250,17 @@ void Function::fill_seeded(int level, std::uint64_t seed, bool dirichlet_zero) {
   double* p = data(level);
   if (ld.lay.macros.empty()) return;
   launch_fill_seeded(p, ld.macros.get(), static_cast<int>(ld.lay.macros.size()), ld.lay.macro_stride, ld.lay.n,
-                     space_ == Space::ND1, ld.lay.class_stride, seed, dirichlet_zero, ctx_->stream());
+                     static_cast<int>(space_), ld.lay.class_stride, seed, dirichlet_zero, ctx_->stream());
 }
 
 void Function::fill_coefficient(int level, CoeffSpec spec) {
-  if (space_ != Space::P1) fail_arg("fill_coefficient: coefficient functions live in P1");
+  if (space_ == Space::ND1) fail_arg("fill_coefficient: coefficient functions live in P1 or P2");
   if (spec.which < 0 || spec.which > 3) fail_arg("fill_coefficient: unknown coefficient");
   auto& ld = ctx_->level(space_, level);
   double* p = data(level);
   if (ld.lay.macros.empty()) return;
   launch_fill_coeff(p, ld.macros.get(), static_cast<int>(ld.lay.macros.size()), ld.lay.macro_stride, ld.lay.n, spec,
-                    ctx_->stream());
+                    ctx_->stream(), space_ == Space::P2 ? ld.lay.class_stride : 0);
 }
 
 i64 Function::num_ref_dofs(int level) { return ctx_->ref_level(space_, level).ref->num_dofs; }

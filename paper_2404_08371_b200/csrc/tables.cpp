@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <mutex>
 
 #include "common.hpp"
 
@@ -191,6 +192,119 @@ N1GramTable n1_gram_table(const MacroMesh& mesh, int macro, int level) {
       for (int y = x; y < 4; ++y) out.o[o][22 + sym4(x, y)] = g.vol / 120.0 * dot(G[x], G[y]);
     for (int e = 0; e < 6; ++e)
       out.o[o][32 + e] = -2.0 * out.o[o][22 + sym4(local_edge_vertex(e, 0), local_edge_vertex(e, 1))];
+  }
+  return out;
+}
+
+namespace {
+
+// polynomials in the four barycentric coordinates (exponent tuple -> coeff)
+using Mono = std::array<int, 4>;
+using Poly = std::map<Mono, double>;
+
+Poly pmul(const Poly& a, const Poly& b) {
+  Poly c;
+  for (const auto& [ea, ca] : a)
+    for (const auto& [eb, cb] : b) {
+      Mono e{ea[0] + eb[0], ea[1] + eb[1], ea[2] + eb[2], ea[3] + eb[3]};
+      c[e] += ca * cb;
+    }
+  return c;
+}
+
+double fact(int k) {
+  double f = 1.0;
+  for (int i = 2; i <= k; ++i) f *= i;
+  return f;
+}
+
+// int over a tetrahedron of volume vol of prod lambda_i^e_i = 6 vol prod e_i! / (sum e_i + 3)!
+double pint(const Poly& p, double vol) {
+  double s = 0.0;
+  for (const auto& [e, c] : p)
+    s += c * 6.0 * vol * fact(e[0]) * fact(e[1]) * fact(e[2]) * fact(e[3]) / fact(e[0] + e[1] + e[2] + e[3] + 3);
+  return s;
+}
+
+Mono unit(int i) {
+  Mono e{0, 0, 0, 0};
+  e[i] = 1;
+  return e;
+}
+
+// P2 basis (vertices 0-3, edges 4-9) and d phi_i / d lambda_p
+Poly p2_basis(int i) {
+  Poly p;
+  if (i < 4) {
+    Mono e2 = unit(i);
+    e2[i] = 2;
+    p[e2] = 2.0;
+    p[unit(i)] = -1.0;
+  } else {
+    const int a = kLocalEdge[i - 4][0], b = kLocalEdge[i - 4][1];
+    Mono e = unit(a);
+    e[b] += 1;
+    p[e] = 4.0;
+  }
+  return p;
+}
+Poly p2_dbasis(int i, int pvar) {
+  Poly p;
+  if (i < 4) {
+    if (pvar == i) {
+      p[unit(i)] = 4.0;
+      p[Mono{0, 0, 0, 0}] = -1.0;
+    }
+  } else {
+    const int a = kLocalEdge[i - 4][0], b = kLocalEdge[i - 4][1];
+    if (pvar == a) p[unit(b)] = 4.0;
+    if (pvar == b) p[unit(a)] = 4.0;
+  }
+  return p;
+}
+
+} // namespace
+
+P2VTable p2v_table(const MacroMesh& mesh, int macro, int level) {
+  P2VTable out;
+  std::memset(&out, 0, sizeof(out));
+  // orientation-independent reference integrals: I[m][i][j][p][q] = int psi_m
+  // d_p phi_i d_q phi_j over a unit-volume element (scaled by vol below)
+  static std::vector<double> ref;  // [m][i][j][p][q]
+  static std::once_flag once;
+  std::call_once(once, [] {
+    ref.assign(10 * 10 * 10 * 16, 0.0);
+    for (int m = 0; m < 10; ++m) {
+      const Poly psi = p2_basis(m);
+      for (int i = 0; i < 10; ++i)
+        for (int p = 0; p < 4; ++p) {
+          const Poly di = p2_dbasis(i, p);
+          if (di.empty()) continue;
+          const Poly pd = pmul(psi, di);
+          for (int j = 0; j < 10; ++j)
+            for (int q = 0; q < 4; ++q) {
+              const Poly dj = p2_dbasis(j, q);
+              if (dj.empty()) continue;
+              ref[(((m * 10 + i) * 10 + j) * 4 + p) * 4 + q] = pint(pmul(pd, dj), 1.0);
+            }
+        }
+    }
+  });
+  for (int o = 0; o < 6; ++o) {
+    const OrientGeom g = orient_geometry(mesh, macro, level, o);
+    V3 G[4];
+    for (int i = 0; i < 4; ++i) G[i] = mat_vec(g.JinvT, kGradRef[i]);
+    double GG[4][4];
+    for (int p = 0; p < 4; ++p)
+      for (int q = 0; q < 4; ++q) GG[p][q] = dot(G[p], G[q]);
+    for (int m = 0; m < 10; ++m)
+      for (int i = 0; i < 10; ++i)
+        for (int j = i; j < 10; ++j) {
+          double v = 0.0;
+          for (int p = 0; p < 4; ++p)
+            for (int q = 0; q < 4; ++q) v += GG[p][q] * ref[(((m * 10 + i) * 10 + j) * 4 + p) * 4 + q];
+          out.T[o][m][sym10(i, j)] = g.vol * v;
+        }
   }
   return out;
 }

@@ -94,6 +94,21 @@ TM_HD constexpr int sym4(int i, int j) {
   return i * 4 - i * (i - 1) / 2 + (j - i);
 }
 
+// P2V form (P2 trial/test, k in P2; forms.cpp:12): per orientation o the ten
+// coefficient-basis tables T_m[ij] = int psi_m grad phi_i . grad phi_j over
+// the micro element (exact; local DoFs 0-3 vertices, 4-9 edges in local-edge
+// order (0,1),(0,2),(0,3),(1,2),(1,3),(2,3); psi = phi = the P2 basis
+// lambda_i (2 lambda_i - 1), 4 lambda_a lambda_b), so A_e = sum_m k_m T_m.
+struct P2VTable {
+  double T[6][10][56];  // [orientation][coefficient DoF m][packed upper triangle (55) + pad]
+};
+P2VTable p2v_table(const MacroMesh& mesh, int macro, int level);
+// packed index of (i, j), i <= j < 10
+TM_HD constexpr int sym10(int i, int j) {
+  if (i > j) { const int t = i; i = j; j = t; }
+  return i * 10 - i * (i - 1) / 2 + (j - i);
+}
+
 // Groups macros with bitwise-identical tables (translated copies, e.g. all
 // cubes of a Kuhn mesh share six geometries). Returns per-macro group id.
 std::vector<int> geometry_groups(const MacroMesh& mesh, const std::vector<int>& macros, int* num_groups);

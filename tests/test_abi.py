@@ -223,6 +223,38 @@ def test_tables_match_reference_local_matrix(tm, mesh):
                 assert np.abs(A - B).max() <= 1e-14 * np.abs(A).max()
 
 
+@pytest.mark.parametrize("mesh", ["single-tet", "cube6"])
+def test_p2v_tables_match_reference_local_matrix(tm, mesh):
+    """P2V exact tables (k in P2, degree-4 integrand) vs the reference's
+    local_matrix with the degree-4 (Keast, 11-point) rule; local DoF order
+    vertices then edges (0,1),(0,2),(0,3),(1,2),(1,3),(2,3) (fespace.hpp:27-28)."""
+    import ctypes
+    from oracle.refapi import REF_FIXED_LIB, RefSystem, ref_fixed_lib
+    if not os.path.exists(REF_FIXED_LIB):
+        pytest.skip("oracle/_ref not built")
+    L = ref_fixed_lib().L
+    L.ref_local_matrix.restype = ctypes.c_int
+    dp = ctypes.POINTER(ctypes.c_double)
+    L.ref_local_matrix.argtypes = [ctypes.c_void_p] + [ctypes.c_int] * 5 + [dp, dp, ctypes.c_int, dp]
+    ctx = tm.Context(mesh, device=-1)
+    level = 2
+    ref = RefSystem(mesh, "P2V", level)
+    nc = int(ref.lib.coeff_num_dofs(ref.h))
+    k = np.random.default_rng(1).uniform(1, 2, nc)
+    for m in range(ctx.num_macros()[0]):
+        for o in range(6):
+            for (x, y, z) in [(0, 0, 0), (1, 0, 0)]:
+                out = np.empty(100)
+                rc = L.ref_local_matrix(ref.h, m, o, x, y, z, k.ctypes.data_as(dp), None, 4, out.ctypes.data_as(dp))
+                assert rc == 10
+                ids = (ctypes.c_longlong * 10)()
+                sg = (ctypes.c_double * 10)()
+                assert L.ref_local_dofs(ref.h, m, o, x, y, z, ids, sg) == 10
+                B = ctx.local_matrix(tm.FORM_P2V, level, m, o, k[np.array(list(ids))], None)
+                A = out.reshape(10, 10)
+                assert np.abs(A - B).max() <= 1e-13 * np.abs(A).max()
+
+
 def test_stencil_properties(tm):
     ctx = tm.Context("single-tet", device=-1)
     S = ctx.stencil(4, 0)
