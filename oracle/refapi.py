@@ -62,10 +62,12 @@ def _uniform(seed, h):
     return 2.0 * ((r >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)) - 1.0
 
 
-def seeded_values(kind: np.ndarray, a: np.ndarray, b: np.ndarray, scale: int, seed: int) -> np.ndarray:
+def seeded_values(kind: np.ndarray, a: np.ndarray, b: np.ndarray, scale: int, seed: int,
+                  signed_edges: bool = True) -> np.ndarray:
     """Seeded uniform[-1,1] value per DoF from its geometry.
 
-    kind 0: vertex at a; kind 1: edge a -> b (value along a -> b).
+    kind 0: vertex at a; kind 1: edge a -> b (value along a -> b; with
+    signed_edges=False -- P2 midpoint DoFs -- the key-ascending edge's value).
     scale: integer such that scale * coordinates are integers (n * D).
     """
     A = np.rint(a * scale).astype(np.int64)
@@ -82,7 +84,7 @@ def seeded_values(kind: np.ndarray, a: np.ndarray, b: np.ndarray, scale: int, se
         lo = np.where(less[:, None], Ae, B)
         hi = np.where(less[:, None], B, Ae)
         val = _uniform(seed, _hash_edge(lo, hi))
-        out[e] = np.where(less, val, -val)
+        out[e] = np.where(less, val, -val) if signed_edges else val
     return out
 
 

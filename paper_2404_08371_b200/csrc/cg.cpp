@@ -21,7 +21,8 @@ void nccl_allgather_doubles(void* comm, const double* d_in, double* d_out, int c
 namespace {
 
 SlotSpace slot_space(const Context::LevelData& ld) {
-  return SlotSpace{ld.lay.n, ld.lay.space == Space::ND1 ? 1 : 0, ld.lay.macro_stride, ld.lay.class_stride};
+  const int kind = ld.lay.space == Space::ND1 ? 1 : (ld.lay.space == Space::P2 ? 2 : 0);
+  return SlotSpace{ld.lay.n, kind, ld.lay.macro_stride, ld.lay.class_stride};
 }
 
 } // namespace

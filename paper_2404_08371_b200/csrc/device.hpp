@@ -85,6 +85,10 @@ void launch_n1_cubes(const double* x, const double* alpha, const double* beta, d
                      const MacroDesc* d_macros, int nmacros, i64 macro_stride, i64 class_stride,
                      i64 coeff_stride, int n, const N1DeviceTable* d_tables, cudaStream_t s);
 
+// P2V apply, first version (k_p2v.cu): cube loop + FP64 atomics into a zeroed y
+void launch_p2v_cubes(const double* x, const double* k, double* y, const MacroDesc* d_macros, int nmacros,
+                      i64 macro_stride, i64 class_stride, int n, const P2VTable* d_tables, cudaStream_t s);
+
 // operator diagonals per stored macro copy (k_diagonal.cu, k_p1k_gather.cu)
 void launch_p1_diagonal(double* d, const MacroDesc* d_macros, int nmacros, i64 macro_stride, int n,
                         const P1DeviceTable* d_tables, cudaStream_t s);

@@ -46,6 +46,7 @@ template class DeviceBuffer<MacroDesc>;
 template class DeviceBuffer<P1DeviceTable>;
 template class DeviceBuffer<N1DeviceTable>;
 template class DeviceBuffer<N1GramTable>;
+template class DeviceBuffer<P2VTable>;
 
 // ---------------------------------------------------------------- forms
 const FormInfo& form_info(Form f) {
@@ -296,7 +297,7 @@ void Function::export_ref(int level, double* host_ref) {
 Operator::Operator(Context& ctx, Form form, std::vector<const Function*> coeffs)
     : ctx_(&ctx), form_(form), coeffs_(std::move(coeffs)) {
   const FormInfo& fi = form_info(form);
-  if (form == Form::P2VDiffusion) fail_arg("form P2V is not implemented (SURVEY.md 8(f) next item)");
+
   if (coeffs_.size() != fi.coeffSpaces.size())
     fail_arg(std::string("form ") + fi.name + " expects " + std::to_string(fi.coeffSpaces.size()) +
              " coefficient field(s)");
@@ -314,7 +315,16 @@ Operator::LevelTables& Operator::tables(int level) {
   const int ng = ctx_->num_geometry_groups();
   const auto& macros = ctx_->macros();
   const auto& grp = ctx_->geometry_group();
-  if (form_ == Form::N1CurlCurlMass) {
+  if (form_ == Form::P2VDiffusion) {
+    std::vector<P2VTable> t(ng);
+    std::vector<bool> done(ng, false);
+    for (std::size_t li = 0; li < macros.size(); ++li)
+      if (!done[grp[li]]) {
+        t[grp[li]] = p2v_table(ctx_->mesh(), macros[li], level);
+        done[grp[li]] = true;
+      }
+    lt->p2v.upload(t.data(), t.size(), ctx_->stream());
+  } else if (form_ == Form::N1CurlCurlMass) {
     std::vector<N1DeviceTable> t(ng);
     std::vector<bool> done(ng, false);
     for (std::size_t li = 0; li < macros.size(); ++li)
@@ -421,6 +431,10 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
       }
       break;
     }
+    case Form::P2VDiffusion:
+      launch_p2v_cubes(x, coeffs_[0]->data(level), y, ld.macros.get(), nm, ld.lay.macro_stride, ld.lay.class_stride,
+                       ld.lay.n, t.p2v.get(), s);
+      break;
     default:
       fail_internal("kernel_apply: unsupported form");
   }
@@ -454,7 +468,7 @@ void Operator::diagonal(Function& d, int level) {
         break;
       }
       default:
-        fail_internal("diagonal: unsupported form");
+        fail_arg("diagonal: not available for this form");
     }
   }
   launch_interface_sum(y, ld.group_offsets.get(), ld.group_copies.get(), ld.groups.num_groups(), s, false);

@@ -184,6 +184,7 @@ private:
     DeviceBuffer<P1DeviceTable> p1;
     DeviceBuffer<N1DeviceTable> n1;
     DeviceBuffer<N1GramTable> n1g;       // Gram form per geometry group (K3 v2)
+    DeviceBuffer<P2VTable> p2v;          // P2V coefficient-basis tables per geometry group
   };
   LevelTables& tables(int level);
   void check(const Function& src, const Function& dst, int level) const;

@@ -57,14 +57,16 @@ __device__ bool decode_point(int n, i64 idx, int& x, int& y, int& z) {
 // and non-existent carriers
 __device__ unsigned slot_class(const SlotSpace& sp, const unsigned char* __restrict__ table, i64 i) {
   const int li = static_cast<int>(i / sp.macro_stride);
-  const i64 s = i - static_cast<i64>(li) * sp.macro_stride;
+  i64 s = i - static_cast<i64>(li) * sp.macro_stride;
   const int n = sp.n;
   unsigned mask;
-  if (!sp.nd1) {
+  const i64 vstride = sp.nd1 == 2 ? (tet_count(n) + 31) / 32 * 32 : 0;  // P2: vertex block first
+  if (sp.nd1 == 0 || (sp.nd1 == 2 && s < vstride)) {
     int x, y, z;
     if (!decode_point(n, s, x, y, z)) return 0;
     mask = point_mask(n, x, y, z);
   } else {
+    s -= vstride;
     const int c = static_cast<int>(s / sp.class_stride);
     int ax, ay, az;
     if (c >= 7 || !decode_point(n - 1, s - c * sp.class_stride, ax, ay, az)) return 0;

@@ -19,7 +19,7 @@ namespace tetmf {
 // geometry of a function's storage as the slot-class kernels see it
 struct SlotSpace {
   int n;             // lattice extent (2^level)
-  int nd1;           // 0 P1 points, 1 ND1 edges
+  int nd1;           // 0 P1 points, 1 ND1 edges, 2 P2 (vertex block, then edge blocks)
   i64 macro_stride;  // entries per macro
   i64 class_stride;  // ND1: entries per edge-class block
 };

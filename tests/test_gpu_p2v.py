@@ -1,0 +1,57 @@
+"""P2V: -div(k grad u) with u, k in P2 (forms.cpp:12), on
+the GPU against the fixed reference build's FormSystem::reference_apply
+(degree 6 >= the exact degree 4), on single-tet, cube6 and a Kuhn-cube mesh.
+Seeded x: vertex values at vertex keys, edge-midpoint values at the
+key-ascending edge keys (unsigned); k nodally interpolated at vertices and
+edge midpoints (fespace.cpp:494-506)."""
+import numpy as np
+import pytest
+
+from oracle.refapi import RefSystem, seeded_values, write_kuhn_mesh
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(tm, mesh, level, seed):
+    ctx = tm.Context(mesh, device=0)
+    k = tm.Function(ctx, tm.SPACE_P2)
+    k.fill_coefficient(level, tm.COEFF_K)
+    x = tm.Function(ctx, tm.SPACE_P2)
+    x.fill_seeded(level, seed)
+    return ctx, k, x, tm.Operator(ctx, tm.FORM_P2V, [k])
+
+
+@pytest.mark.parametrize("mesh,level", [("single-tet", 1), ("single-tet", 2), ("single-tet", 3), ("cube6", 1),
+                                        ("cube6", 2), ("cubes2", 1), ("cubes2", 2)])
+def test_p2v_parity_with_reference(tm, tmp_path, mesh, level):
+    port_mesh = mesh
+    if mesh.startswith("cubes"):
+        port_mesh = str(tmp_path / "kuhn.mesh")
+        write_kuhn_mesh(port_mesh, int(mesh[5:]))
+    ctx, k, x, op = _setup(tm, mesh, level, 42)
+    y = tm.Function(ctx, tm.SPACE_P2)
+    op.apply(x, y, level)
+    ctx.synchronize()
+    ref = RefSystem(port_mesh, "P2V", level)
+    kind, a, b = ref.dof_geometry()
+    x_ref = seeded_values(kind, a, b, 1 << level, 42, signed_edges=False)
+    assert np.array_equal(x.export_ref(level), x_ref)        # seeded input reproduced
+    k_ref = ref.interpolate(2)
+    assert np.abs(k.export_ref(level) - k_ref).max() <= 1e-15 * np.abs(k_ref).max()
+    w, _ = ref.apply(x_ref, k_ref, None, degree=0)
+    got = y.export_ref(level)
+    assert np.abs(got - w).max() <= 1e-12 * np.abs(w).max()
+
+
+def test_p2v_cg_recovers_known_solution(tm):
+    level = 3
+    ctx, k, xs, op = _setup(tm, "cube6", level, 3)
+    xs.fill_seeded(level, 3, True)
+    b = tm.Function(ctx, tm.SPACE_P2)
+    op.apply(xs, b, level)
+    b.mask_dirichlet(level)
+    x = tm.Function(ctx, tm.SPACE_P2)
+    it, rel, ok = op.cg_solve(b, x, level, rtol=1e-12, max_iter=3000)
+    assert ok
+    want, got = xs.export_ref(level), x.export_ref(level)
+    assert np.abs(got - want).max() <= 1e-8 * np.abs(want).max()
