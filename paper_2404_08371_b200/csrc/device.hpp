@@ -86,6 +86,12 @@ void launch_n1_cubes(const double* x, const double* alpha, const double* beta, d
                      i64 coeff_stride, int n, const N1DeviceTable* d_tables, cudaStream_t s);
 
 // P2V apply, first version (k_p2v.cu): cube loop + FP64 atomics into a zeroed y
+// P2V operator diagonal per stored macro copy (k_p2v.cu)
+void launch_p2v_diagonal(const double* k, double* d, const MacroDesc* d_macros, int nmacros, i64 macro_stride,
+                         i64 class_stride, int n, const P2VTable* d_tables, cudaStream_t s);
+// P2V factored cube kernel (default; k_p2v.cu v2)
+void launch_p2v_cubes2(const double* x, const double* k, double* y, const MacroDesc* d_macros, int nmacros,
+                       i64 macro_stride, i64 class_stride, int n, const P2VTable* d_tables, cudaStream_t s);
 void launch_p2v_cubes(const double* x, const double* k, double* y, const MacroDesc* d_macros, int nmacros,
                       i64 macro_stride, i64 class_stride, int n, const P2VTable* d_tables, cudaStream_t s);
 

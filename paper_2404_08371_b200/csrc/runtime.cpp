@@ -432,8 +432,12 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
       break;
     }
     case Form::P2VDiffusion:
-      launch_p2v_cubes(x, coeffs_[0]->data(level), y, ld.macros.get(), nm, ld.lay.macro_stride, ld.lay.class_stride,
-                       ld.lay.n, t.p2v.get(), s);
+      if (kernel_variant_ == 1)
+        launch_p2v_cubes(x, coeffs_[0]->data(level), y, ld.macros.get(), nm, ld.lay.macro_stride,
+                         ld.lay.class_stride, ld.lay.n, t.p2v.get(), s);
+      else
+        launch_p2v_cubes2(x, coeffs_[0]->data(level), y, ld.macros.get(), nm, ld.lay.macro_stride,
+                          ld.lay.class_stride, ld.lay.n, t.p2v.get(), s);
       break;
     default:
       fail_internal("kernel_apply: unsupported form");
@@ -467,6 +471,10 @@ void Operator::diagonal(Function& d, int level) {
                            ld.lay.macro_stride, ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, t.n1g.get(), s);
         break;
       }
+      case Form::P2VDiffusion:
+        launch_p2v_diagonal(coeffs_[0]->data(level), y, ld.macros.get(), nm, ld.lay.macro_stride,
+                            ld.lay.class_stride, ld.lay.n, t.p2v.get(), s);
+        break;
       default:
         fail_arg("diagonal: not available for this form");
     }

@@ -297,6 +297,8 @@ P2VTable p2v_table(const MacroMesh& mesh, int macro, int level) {
     double GG[4][4];
     for (int p = 0; p < 4; ++p)
       for (int q = 0; q < 4; ++q) GG[p][q] = dot(G[p], G[q]);
+    for (int p = 0; p < 4; ++p)
+      for (int q = p; q < 4; ++q) out.G[o][sym4(p, q)] = g.vol * GG[p][q];
     for (int m = 0; m < 10; ++m)
       for (int i = 0; i < 10; ++i)
         for (int j = i; j < 10; ++j) {
@@ -307,6 +309,18 @@ P2VTable p2v_table(const MacroMesh& mesh, int macro, int level) {
         }
   }
   return out;
+}
+
+void p2v_moments(double C[10][10]) {
+  for (int m = 0; m < 10; ++m) {
+    const Poly psi = p2_basis(m);
+    for (int r = 0; r < 4; ++r)
+      for (int s = r; s < 4; ++s) {
+        Mono e = unit(r);
+        e[s] += 1;
+        C[m][sym4(r, s)] = pint(pmul(psi, Poly{{e, 1.0}}), 1.0);
+      }
+  }
 }
 
 std::vector<int> geometry_groups(const MacroMesh& mesh, const std::vector<int>& macros, int* num_groups) {

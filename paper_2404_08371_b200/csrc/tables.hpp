@@ -99,10 +99,19 @@ TM_HD constexpr int sym4(int i, int j) {
 // the micro element (exact; local DoFs 0-3 vertices, 4-9 edges in local-edge
 // order (0,1),(0,2),(0,3),(1,2),(1,3),(2,3); psi = phi = the P2 basis
 // lambda_i (2 lambda_i - 1), 4 lambda_a lambda_b), so A_e = sum_m k_m T_m.
+//
+// The factored kernel (k_p2v.cu) uses instead, per orientation, the metric
+// G[o][sym4(p, q)] = vol grad lambda_p . grad lambda_q and the universal
+// moments C[m][sym4(r, s)] = (1 / vol) int psi_m lambda_r lambda_s (p2v_moments):
+// int k grad u . grad phi_i = sum_pq G_pq int k (du/dlambda_p)(dphi_i/dlambda_q)
+// (chain rule in barycentrics; any polynomial representation of u works
+// because sum_p grad lambda_p = 0).
 struct P2VTable {
   double T[6][10][56];  // [orientation][coefficient DoF m][packed upper triangle (55) + pad]
+  double G[6][10];      // [orientation][sym4(p, q)]
 };
 P2VTable p2v_table(const MacroMesh& mesh, int macro, int level);
+void p2v_moments(double C[10][10]);
 // packed index of (i, j), i <= j < 10
 TM_HD constexpr int sym10(int i, int j) {
   if (i > j) { const int t = i; i = j; j = t; }

@@ -55,3 +55,66 @@ def test_p2v_cg_recovers_known_solution(tm):
     assert ok
     want, got = xs.export_ref(level), x.export_ref(level)
     assert np.abs(got - want).max() <= 1e-8 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("mesh,level", [("single-tet", 2), ("cube6", 1), ("cubes2", 1)])
+def test_p2v_diagonal_matches_probed_reference(tm, tmp_path, mesh, level):
+    """tetmf_op_diagonal for P2V: d_i = (A e_i)_i through the reference's
+    apply, on the owner copies (interface copies hold the same summed value)."""
+    port_mesh = mesh
+    if mesh.startswith("cubes"):
+        port_mesh = str(tmp_path / "kuhn.mesh")
+        write_kuhn_mesh(port_mesh, int(mesh[5:]))
+    ctx, k, _, op = _setup(tm, mesh, level, 1)
+    ref = RefSystem(port_mesh, "P2V", level)
+    k_ref = ref.interpolate(2)
+    nd = len(k_ref)
+    want = np.empty(nd)
+    for i in range(nd):
+        e = np.zeros(nd)
+        e[i] = 1.0
+        w, _ = ref.apply(e, k_ref, None, degree=0)
+        want[i] = w[i]
+    d = tm.Function(ctx, tm.SPACE_P2)
+    op.diagonal(d, level)
+    ctx.synchronize()
+    rmap, nref = ctx.ref_map(tm.SPACE_P2, level)
+    assert nref == nd
+    raw = d.download(level)
+    sel = (rmap >= 0) & ((rmap & 1) == 1)
+    got = np.full(nd, np.nan)
+    got[rmap[sel] >> 2] = raw[sel]
+    assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+    assert (want > 0).all()
+
+
+def test_p2v_jacobi_pcg(tm):
+    """Jacobi-PCG on P2V. cube6 (z <= 1): the BASELINE coefficient
+    k = 1 + sin(2 pi x) cos(2 pi y) (1 + z) / 2 is >= 0 there; on the 2x2x2
+    Kuhn mesh (z up to 2) it turns negative and the form is indefinite."""
+    level = 3
+    ctx, k, xs, op = _setup(tm, "cube6", level, 5)
+    xs.fill_seeded(level, 5, True)
+    b = tm.Function(ctx, tm.SPACE_P2)
+    op.apply(xs, b, level)
+    b.mask_dirichlet(level)
+    d = tm.Function(ctx, tm.SPACE_P2)
+    op.diagonal(d, level)
+    x = tm.Function(ctx, tm.SPACE_P2)
+    it, rel, ok = op.cg_solve(b, x, level, rtol=1e-12, max_iter=3000, diag=d)
+    assert ok and rel <= 1e-12
+    want, got = xs.export_ref(level), x.export_ref(level)
+    assert np.abs(got - want).max() <= 1e-8 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("mesh,level", [("cube6", 6), ("cubes2", 5), ("single-tet", 7), ("cubes1x1x2", 4)])
+def test_p2v_factored_vs_first_version(tm, mesh, level):
+    """A/B at sizes beyond the oracle's reach: the factored cube kernel
+    (variant 0) against the first-version table kernel (variant 1)."""
+    ctx, k, x, op = _setup(tm, mesh, level, 9)
+    y0, y1 = tm.Function(ctx, tm.SPACE_P2), tm.Function(ctx, tm.SPACE_P2)
+    op.apply(x, y0, level)
+    op.set_variant(1)
+    op.apply(x, y1, level)
+    a, b = y0.download(level), y1.download(level)
+    assert np.abs(a - b).max() <= 1e-13 * np.abs(b).max()
