@@ -154,6 +154,15 @@ int tetmf_chebyshev_smooth(tetmf_op* op, const tetmf_fn* diag, const tetmf_fn* b
 int tetmf_op_profile(tetmf_op* op, int enable);
 /* 0 = optimized kernels (default); 1 = first-version kernels (A/B tests) */
 int tetmf_op_set_variant(tetmf_op* op, int variant);
+
+/* Integration rule of tetmf_apply / tetmf_op_diagonal: 0 = exact (default;
+ * equals FormSystem::reference_apply, forms.cpp:257-260), d = 1..6 = the
+ * reference's quadrature(d) (quadrature.cpp:135-147), i.e.
+ * FormSystem::apply(v, coeffs, quadrature(d)) (forms.hpp:65-66). P1 and P1K
+ * integrate exactly under every rule; N1 is under-integrated for d <= 2 and
+ * P2V for d <= 3 (the paper's "U" optimization, forms.cpp:12). TETMF_EINVAL
+ * for d outside 0..6. */
+int tetmf_op_set_quadrature(tetmf_op* op, int degree);
 int tetmf_op_kernel_stats(tetmf_op* op, double* total_ms, int64_t* launches);
 /* kernels launched by this library so far (process-wide) */
 int tetmf_launch_count(int64_t* count);

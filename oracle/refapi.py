@@ -240,7 +240,7 @@ class _System:
         """Coefficient fields of the form via the system's own interpolate()."""
         if self.form == "N1":
             return self.interpolate(0), self.interpolate(1)
-        if self.form == "P1K":
+        if self.form in ("P1K", "P2V"):  # k (P1 for P1K, P2 for P2V: the system's coefficient space)
             return self.interpolate(2), None
         return None, None
 

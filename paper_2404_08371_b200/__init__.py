@@ -108,6 +108,7 @@ _SIGS = {
                                               ctypes.c_double]),
     "tetmf_op_profile": (ctypes.c_int, [_c_vp, ctypes.c_int]),
     "tetmf_op_set_variant": (ctypes.c_int, [_c_vp, ctypes.c_int]),
+    "tetmf_op_set_quadrature": (ctypes.c_int, [_c_vp, ctypes.c_int]),
     "tetmf_op_kernel_stats": (ctypes.c_int, [_c_vp, _c_dp, _c_i64p]),
     "tetmf_launch_count": (ctypes.c_int, [_c_i64p]),
 }
@@ -415,6 +416,11 @@ class Operator:
     def set_variant(self, variant: int):
         """0 = optimized kernels (default), 1 = first-version kernels."""
         _check(lib().tetmf_op_set_variant(self._h, variant))
+
+    def set_quadrature(self, degree: int):
+        """0 = exact integration (default), 1..6 = the reference's
+        quadrature(degree) (FormSystem::apply(v, coeffs, quadrature(d)))."""
+        _check(lib().tetmf_op_set_quadrature(self._h, degree))
 
     def profile(self, enable: bool = True):
         _check(lib().tetmf_op_profile(self._h, int(enable)))

@@ -397,6 +397,13 @@ int tetmf_op_set_variant(tetmf_op* op, int variant) {
   });
 }
 
+int tetmf_op_set_quadrature(tetmf_op* op, int degree) {
+  return guard([&] {
+    need(op, "op");
+    op->impl->set_quadrature(degree);
+  });
+}
+
 int tetmf_op_kernel_stats(tetmf_op* op, double* total_ms, int64_t* launches) {
   return guard([&] {
     need(op, "op");

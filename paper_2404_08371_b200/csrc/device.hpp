@@ -73,7 +73,7 @@ void build_n1_fold_tasks(const std::vector<int>& local_macros, int n, int parity
 void pad_n1_fold_tasks(std::vector<int>& tasks);
 void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, const double* x, const double* alpha,
                     const double* beta, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
-                    i64 class_stride, i64 coeff_stride, int n, cudaStream_t s);
+                    i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s);
 int n1_kernel_mode();
 // K2 default: per-point gather over the 24 incident elements (k_p1k_gather.cu)
 void build_p1k_tasks(int nmacros, int n, std::vector<int>& out);
@@ -88,10 +88,12 @@ void launch_n1_cubes(const double* x, const double* alpha, const double* beta, d
 // P2V apply, first version (k_p2v.cu): cube loop + FP64 atomics into a zeroed y
 // P2V operator diagonal per stored macro copy (k_p2v.cu)
 void launch_p2v_diagonal(const double* k, double* d, const MacroDesc* d_macros, int nmacros, i64 macro_stride,
-                         i64 class_stride, int n, const P2VTable* d_tables, cudaStream_t s);
+                         i64 class_stride, int n, const P2VTable* d_tables, int rule, cudaStream_t s);
 // P2V factored cube kernel (default; k_p2v.cu v2)
+// rule: 0 exact, 1..3 quadrature(rule) (under-integration; forms.cpp:12 "U")
 void launch_p2v_cubes2(const double* x, const double* k, double* y, const MacroDesc* d_macros, int nmacros,
-                       i64 macro_stride, i64 class_stride, int n, const P2VTable* d_tables, cudaStream_t s);
+                       i64 macro_stride, i64 class_stride, int n, const P2VTable* d_tables, int rule,
+                       cudaStream_t s);
 void launch_p2v_cubes(const double* x, const double* k, double* y, const MacroDesc* d_macros, int nmacros,
                       i64 macro_stride, i64 class_stride, int n, const P2VTable* d_tables, cudaStream_t s);
 
@@ -102,7 +104,7 @@ void launch_p1k_diagonal(const double* k, double* d, const int* d_tasks, int nta
                          const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
 void launch_n1_diagonal(double* d, const double* alpha, const double* beta, const MacroDesc* d_macros, int nmacros,
                         i64 macro_stride, i64 class_stride, i64 coeff_stride, int n, const N1GramTable* d_gram,
-                        cudaStream_t s);
+                        int rule, cudaStream_t s);
 
 // P1 <-> ND1 discrete gradient and its transpose (k_transfer.cu)
 void launch_gradient(const double* phi, double* u, int nmacros, i64 stride_nd1, i64 class_stride, i64 stride_p1,

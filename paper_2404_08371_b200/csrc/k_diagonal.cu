@@ -81,6 +81,11 @@ p1_diagonal_kernel(double* __restrict__ d, const MacroDesc* __restrict__ macros,
   d[tid] = tabs[macros[li].group].stencil[type][0];  // weight of the point itself
 }
 
+// N1 mass moments under quadrature(1) / quadrature(2) (tables.hpp
+// n1_rule_moments): B_pq = sum_m beta_m R[m][pq] replaces S + beta_p + beta_q
+__constant__ double kDiagRule[2][4][10];
+
+template <int RULE>
 __global__ void __launch_bounds__(kThreads)
 n1_diagonal_kernel(double* __restrict__ d, const double* __restrict__ alpha, const double* __restrict__ beta,
                    const MacroDesc* __restrict__ macros, int nmacros, i64 stride, i64 cstride, i64 cf_stride, int n,
@@ -111,9 +116,21 @@ n1_diagonal_kernel(double* __restrict__ d, const double* __restrict__ alpha, con
       al += __ldg(A + q);
       bv[j] = __ldg(B + q);
     }
-    const double S = (bv[0] + bv[1]) + (bv[2] + bv[3]);
     const int la = local_edge_vertex(i, 0), lb = local_edge_vertex(i, 1);
-    const double Baa = 2.0 * S + 4.0 * bv[la], Bbb = 2.0 * S + 4.0 * bv[lb], Bab = S + bv[la] + bv[lb];
+    double Baa, Bbb, Bab;
+    if (RULE == 0) {
+      const double S = (bv[0] + bv[1]) + (bv[2] + bv[3]);
+      Baa = 2.0 * S + 4.0 * bv[la];
+      Bbb = 2.0 * S + 4.0 * bv[lb];
+      Bab = S + bv[la] + bv[lb];
+    } else {
+      Baa = Bbb = Bab = 0.0;
+      for (int m = 0; m < 4; ++m) {
+        Baa = fma(bv[m], kDiagRule[RULE - 1][m][sym4(la, la)], Baa);
+        Bbb = fma(bv[m], kDiagRule[RULE - 1][m][sym4(lb, lb)], Bbb);
+        Bab = fma(bv[m], kDiagRule[RULE - 1][m][sym4(la, lb)], Bab);
+      }
+    }
     const double* tb = tb0 + o * kGramRow;
     double m = Baa * tb[22 + sym4(lb, lb)];
     m = fma(Bbb, tb[22 + sym4(la, la)], m);
@@ -140,10 +157,26 @@ void launch_p1_diagonal(double* d, const MacroDesc* d_macros, int nmacros, i64 m
 
 void launch_n1_diagonal(double* d, const double* alpha, const double* beta, const MacroDesc* d_macros, int nmacros,
                         i64 macro_stride, i64 class_stride, i64 coeff_stride, int n, const N1GramTable* d_gram,
-                        cudaStream_t s) {
+                        int rule, cudaStream_t s) {
   if (nmacros == 0) return;
-  n1_diagonal_kernel<<<grid_for(macro_stride * nmacros), kThreads, 0, s>>>(
-      d, alpha, beta, d_macros, nmacros, macro_stride, class_stride, coeff_stride, n, d_gram);
+  static const bool ready = [] {
+    double R[2][4][10];
+    n1_rule_moments(1, R[0]);
+    n1_rule_moments(2, R[1]);
+    TETMF_CUDA(cudaMemcpyToSymbol(kDiagRule, R, sizeof(R)));
+    return true;
+  }();
+  (void)ready;
+  const unsigned grid = grid_for(macro_stride * nmacros);
+  if (rule == 0)
+    n1_diagonal_kernel<0><<<grid, kThreads, 0, s>>>(d, alpha, beta, d_macros, nmacros, macro_stride, class_stride,
+                                                    coeff_stride, n, d_gram);
+  else if (rule == 1)
+    n1_diagonal_kernel<1><<<grid, kThreads, 0, s>>>(d, alpha, beta, d_macros, nmacros, macro_stride, class_stride,
+                                                    coeff_stride, n, d_gram);
+  else
+    n1_diagonal_kernel<2><<<grid, kThreads, 0, s>>>(d, alpha, beta, d_macros, nmacros, macro_stride, class_stride,
+                                                    coeff_stride, n, d_gram);
   check_launch("n1_diagonal");
 }
 

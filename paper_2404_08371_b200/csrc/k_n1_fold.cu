@@ -108,7 +108,7 @@ struct FoldIn {
   }
 };
 
-template <int PASS>
+template <int PASS, int RULE>
 __global__ void __launch_bounds__(32 * kWarps, TETMF_N1F_MIN_BLOCKS)
 n1_fold_kernel(const N1GramTable* __restrict__ gram, const MacroDesc* __restrict__ macros,
                const double* __restrict__ xin, const double* __restrict__ alpha, const double* __restrict__ beta,
@@ -273,8 +273,8 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram, const MacroDesc* __restrict
 #pragma unroll
     for (int k = 0; k < 19; ++k) Y[k] = 0.0;
     const int s = X + y + z;
-    cube_elements(SmemTabs{sg}, FoldIn{r0, r1, r0 + dq, r1 + dq}, Y, cube && s <= n - 1, cube && s <= n - 2,
-                  cube && s <= n - 3);
+    cube_elements<RULE>(SmemTabs{sg}, FoldIn{r0, r1, r0 + dq, r1 + dq}, Y, cube && s <= n - 1, cube && s <= n - 2,
+                        cube && s <= n - 3);
     __syncwarp();  // ring slot tt mod 3 is refilled by the next step's copies
 
     // contributions of the x-1 neighbour cube (same row)
@@ -392,19 +392,31 @@ void pad_n1_fold_tasks(std::vector<int>& tasks) {
 // gram: tables of all geometry groups; macros: local macro descriptors
 void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, const double* x, const double* alpha,
                     const double* beta, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
-                    i64 class_stride, i64 coeff_stride, int n, cudaStream_t s) {
+                    i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s) {
   if (ntasks == 0) return;
+  if (rule < 0 || rule > 2) fail_internal("n1_fold: rule index out of range");
   constexpr int smem = static_cast<int>(sizeof(N1GramTable) + sizeof(double) * kWarpSmem * kWarps);
   static const bool attr = [] {
-    cudaFuncSetAttribute(n1_fold_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(n1_fold_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(n1_fold_kernel<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(n1_fold_kernel<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(n1_fold_kernel<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(n1_fold_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(n1_fold_kernel<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(n1_fold_kernel<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    double R[2][4][10];
+    n1_rule_moments(1, R[0]);
+    n1_rule_moments(2, R[1]);
+    cudaMemcpyToSymbol(n1::kN1Rule, R, sizeof(R));
     return true;
   }();
   (void)attr;
   const unsigned grid = static_cast<unsigned>((ntasks + kWarps - 1) / kWarps);
-  auto kern = pass == 0 ? n1_fold_kernel<0> : n1_fold_kernel<1>;
-  kern<<<grid, 32 * kWarps, smem, s>>>(gram, macros, x, alpha, beta, y, reinterpret_cast<const FoldTask*>(d_tasks),
-                                       ntasks, macro_stride, class_stride, coeff_stride, n);
+  using K = decltype(&n1_fold_kernel<0, 0>);
+  static const K kerns[2][3] = {{n1_fold_kernel<0, 0>, n1_fold_kernel<0, 1>, n1_fold_kernel<0, 2>},
+                                {n1_fold_kernel<1, 0>, n1_fold_kernel<1, 1>, n1_fold_kernel<1, 2>}};
+  kerns[pass][rule]<<<grid, 32 * kWarps, smem, s>>>(gram, macros, x, alpha, beta, y,
+                                                    reinterpret_cast<const FoldTask*>(d_tasks), ntasks, macro_stride,
+                                                    class_stride, coeff_stride, n);
   check_launch("n1_fold");
 }
 

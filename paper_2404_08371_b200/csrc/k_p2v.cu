@@ -110,7 +110,9 @@ p2v_cubes_kernel(const double* __restrict__ x, const double* __restrict__ kc, do
 // elements and spills at any occupancy (one element alone needs ~54
 // registers plus the accumulators), and the code outgrows the I-cache.
 
-__constant__ double kC[10][10];  // p2v_moments: [m][sym4(r, s)]
+// [rule][m][sym4(r, s)]: 0 exact (p2v_moments), 1..3 quadrature(degree)
+// (p2v_rule_moments; degrees >= 4 integrate P2V exactly)
+__constant__ double kC[4][10][10];
 
 // cube edge id (n1_common.cuh numbering) -> (owner offset, class)
 struct CubeEdgeRef {
@@ -198,6 +200,7 @@ __constant__ OrientConsts kOc = make_orient_consts();
 #ifndef TETMF_P2V_MINB
 #define TETMF_P2V_MINB 1
 #endif
+template <int RULE>
 __global__ void __launch_bounds__(kThreads, TETMF_P2V_MINB)
 p2v_cubes2_kernel(const double* __restrict__ x, const double* __restrict__ kc, double* __restrict__ y,
                   const MacroDesc* __restrict__ macros, int nmacros, i64 stride, i64 cstride, int n,
@@ -242,9 +245,9 @@ p2v_cubes2_kernel(const double* __restrict__ x, const double* __restrict__ kc, d
     double K[10];
 #pragma unroll
     for (int rs = 0; rs < 10; ++rs) {
-      double a = kv[0] * kC[0][rs];
+      double a = kv[0] * kC[RULE][0][rs];
 #pragma unroll
-      for (int m = 1; m < 10; ++m) a = fma(kv[m], kC[m][rs], a);
+      for (int m = 1; m < 10; ++m) a = fma(kv[m], kC[RULE][m][rs], a);
       K[rs] = a;
     }
     // U_qr: coefficients of du/dlambda_q
@@ -297,8 +300,11 @@ p2v_cubes2_kernel(const double* __restrict__ x, const double* __restrict__ kc, d
   }
 }
 
-// operator diagonal per stored macro copy: d_i = sum over the valid elements
-// containing DoF i of (A_e)_ii = sum_m k_m T_m[ii] (exact tables)
+// operator diagonal per stored macro copy, factored form (rule-aware like
+// the apply): per element, with K from kC[RULE] and the orientation's G,
+//   vertex i:   A_ii = G_ii sum_rs d_r d_s K_rs,  d = (3 at i, -1 elsewhere)
+//   edge (a,b): A_ee = 16 (G_aa K_bb + G_bb K_aa + 2 G_ab K_ab)
+template <int RULE>
 __global__ void __launch_bounds__(kThreads)
 p2v_diagonal_kernel(const double* __restrict__ kc, double* __restrict__ d, const MacroDesc* __restrict__ macros,
                     int nmacros, i64 stride, i64 cstride, int n, const P2VTable* __restrict__ tabs) {
@@ -308,58 +314,113 @@ p2v_diagonal_kernel(const double* __restrict__ kc, double* __restrict__ d, const
   const int li = static_cast<int>(tid / anchors);
   int ax, ay, az;
   decode_anchor(n - 1, tid - li * anchors, ax, ay, az);
-  const i64 vstride = (tet_count(n) + 31) / 32 * 32;
+  const int vstride = static_cast<int>((tet_count(n) + 31) / 32 * 32);
+  const int cs = static_cast<int>(cstride);
   const double* __restrict__ km = kc + static_cast<i64>(li) * stride;
   double* __restrict__ dm = d + static_cast<i64>(li) * stride;
-  const P2VTable& T = tabs[macros[li].group];
+  const P2VTable* __restrict__ T = tabs + macros[li].group;
   const int s = ax + ay + az;
+  const CubeRows cr = cube_rows(n, ay, az);
+#pragma unroll 1
   for (int o = 0; o < 6; ++o) {
-    if (s > orient_sum_limit(o, n)) continue;
-    i64 idx[10];
-    for (int i = 0; i < 4; ++i) {
-      const Off3 v = orient_offset(o, i);
-      idx[i] = lattice_index(n, ax + v.x, ay + v.y, az + v.z);
-    }
-    for (int e = 0; e < 6; ++e) {
-      const LocalEdgeRef r = local_edge_ref(o, e);
-      idx[4 + e] = vstride + r.cls * cstride + lattice_index(n - 1, ax + r.ax, ay + r.ay, az + r.az);
-    }
-    double ke[10];
-    for (int i = 0; i < 10; ++i) ke[i] = __ldg(km + idx[i]);
+    if (s > (o == WU ? n - 1 : o == WD ? n - 3 : n - 2)) continue;
+    int idx[10];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) idx[i] = cr.Rv[kOc.vz[o][i]][kOc.vy[o][i]] + ax + kOc.vx[o][i];
+#pragma unroll
+    for (int e = 0; e < 6; ++e)
+      idx[4 + e] = vstride + kOc.ecls[o][e] * cs + cr.Re[kOc.ez[o][e]][kOc.ey[o][e]] + ax + kOc.ex[o][e];
+    double kv[10], g[10], K[10];
+#pragma unroll
     for (int i = 0; i < 10; ++i) {
-      double a = 0.0;
-      for (int m = 0; m < 10; ++m) a = fma(ke[m], T.T[o][m][sym10(i, i)], a);
-      atomicAdd(dm + idx[i], a);
+      kv[i] = __ldg(km + idx[i]);
+      g[i] = __ldg(T->G[o] + i);
+    }
+#pragma unroll
+    for (int rs = 0; rs < 10; ++rs) {
+      double a = kv[0] * kC[RULE][0][rs];
+#pragma unroll
+      for (int m = 1; m < 10; ++m) a = fma(kv[m], kC[RULE][m][rs], a);
+      K[rs] = a;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      double q = 0.0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) q = fma((r == i ? 3.0 : -1.0) * (t == i ? 3.0 : -1.0), K[sym4(r, t)], q);
+      atomicAdd(dm + idx[i], g[sym4(i, i)] * q);
+    }
+#pragma unroll
+    for (int e = 0; e < 6; ++e) {
+      const int a = local_edge_vertex(e, 0), b = local_edge_vertex(e, 1);
+      const double v = g[sym4(a, a)] * K[sym4(b, b)] + g[sym4(b, b)] * K[sym4(a, a)] +
+                       2.0 * g[sym4(a, b)] * K[sym4(a, b)];
+      atomicAdd(dm + idx[4 + e], 16.0 * v);
     }
   }
+}
+
+// exact and quadrature(1..3) moment tables into constant memory (once)
+void load_p2v_moments() {
+  static const bool ready = [] {
+    double C[4][10][10];
+    for (int r = 0; r < 4; ++r) p2v_rule_moments(r, C[r]);
+    TETMF_CUDA(cudaMemcpyToSymbol(kC, C, sizeof(C)));
+    return true;
+  }();
+  (void)ready;
 }
 
 } // namespace
 
 void launch_p2v_diagonal(const double* k, double* d, const MacroDesc* d_macros, int nmacros, i64 macro_stride,
-                         i64 class_stride, int n, const P2VTable* d_tables, cudaStream_t s) {
+                         i64 class_stride, int n, const P2VTable* d_tables, int rule, cudaStream_t s) {
+  load_p2v_moments();
+  if (rule < 0 || rule > 3) fail_internal("p2v: rule index out of range");
   TETMF_CUDA(cudaMemsetAsync(d, 0, sizeof(double) * macro_stride * nmacros, s));
   const i64 total = tet_count(n - 1) * nmacros;
   if (total == 0) return;
-  p2v_diagonal_kernel<<<static_cast<unsigned>((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(
-      k, d, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
+  const unsigned grid = static_cast<unsigned>((total + kThreads - 1) / kThreads);
+  switch (rule) {
+    case 0:
+      p2v_diagonal_kernel<0><<<grid, kThreads, 0, s>>>(k, d, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
+      break;
+    case 1:
+      p2v_diagonal_kernel<1><<<grid, kThreads, 0, s>>>(k, d, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
+      break;
+    case 2:
+      p2v_diagonal_kernel<2><<<grid, kThreads, 0, s>>>(k, d, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
+      break;
+    default:
+      p2v_diagonal_kernel<3><<<grid, kThreads, 0, s>>>(k, d, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
+  }
   check_launch("p2v_diagonal");
 }
 
 void launch_p2v_cubes2(const double* x, const double* k, double* y, const MacroDesc* d_macros, int nmacros,
-                       i64 macro_stride, i64 class_stride, int n, const P2VTable* d_tables, cudaStream_t s) {
-  static bool moments_ready = false;
-  if (!moments_ready) {
-    double C[10][10];
-    p2v_moments(C);
-    TETMF_CUDA(cudaMemcpyToSymbol(kC, C, sizeof(C)));
-    moments_ready = true;
-  }
+                       i64 macro_stride, i64 class_stride, int n, const P2VTable* d_tables, int rule,
+                       cudaStream_t s) {
+  load_p2v_moments();
+  if (rule < 0 || rule > 3) fail_internal("p2v: rule index out of range");
   TETMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * macro_stride * nmacros, s));
   const i64 total = tet_count(n - 1) * nmacros;
   if (total == 0) return;
-  p2v_cubes2_kernel<<<static_cast<unsigned>((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(
-      x, k, y, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
+  const unsigned grid = static_cast<unsigned>((total + kThreads - 1) / kThreads);
+  switch (rule) {
+    case 0:
+      p2v_cubes2_kernel<0><<<grid, kThreads, 0, s>>>(x, k, y, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
+      break;
+    case 1:
+      p2v_cubes2_kernel<1><<<grid, kThreads, 0, s>>>(x, k, y, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
+      break;
+    case 2:
+      p2v_cubes2_kernel<2><<<grid, kThreads, 0, s>>>(x, k, y, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
+      break;
+    default:
+      p2v_cubes2_kernel<3><<<grid, kThreads, 0, s>>>(x, k, y, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
+  }
   check_launch("p2v_cubes2");
 }
 

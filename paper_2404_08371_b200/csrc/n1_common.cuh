@@ -97,7 +97,12 @@ __device__ __forceinline__ void gram_pairs(const Tab& tb, const double (&Bt)[4][
 //     template <int V, int W> double c()  (cube vertex V; W 0 alpha, 1 beta).
 // Tab: template <int I> double get()  (entry I of the orientation's row).
 // An invalid element gets zero coefficients -> A_e = 0 (inputs are finite).
-template <int O, typename Tab, typename In>
+// N1 mass moments under quadrature(1) / quadrature(2) (tables.hpp
+// n1_rule_moments; degrees >= 3 integrate the N1 form exactly): with rule R
+// the Gram form's B_pq = sum_m beta_m R[m][pq]. Filled by the launching TU.
+__constant__ double kN1Rule[2][4][10];
+
+template <int O, int RULE = 0, typename Tab, typename In>
 __device__ __forceinline__ void element_gram(const Tab& tb, const In& in, double (&Y)[19], bool valid) {
   constexpr int v0 = cube_vertex(O, 0), v1 = cube_vertex(O, 1), v2 = cube_vertex(O, 2), v3 = cube_vertex(O, 3);
   const double a4 = (in.template c<v0, 0>() + in.template c<v1, 0>()) +
@@ -105,15 +110,27 @@ __device__ __forceinline__ void element_gram(const Tab& tb, const In& in, double
   const double sa = valid ? a4 : 0.0;
   const double bv[4] = {valid ? in.template c<v0, 1>() : 0.0, valid ? in.template c<v1, 1>() : 0.0,
                         valid ? in.template c<v2, 1>() : 0.0, valid ? in.template c<v3, 1>() : 0.0};
-  const double S = (bv[0] + bv[1]) + (bv[2] + bv[3]);
-  const double S2 = S + S;
   double Bt[4][4];
+  if constexpr (RULE == 0) {
+    const double S = (bv[0] + bv[1]) + (bv[2] + bv[3]);
+    const double S2 = S + S;
 #pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const double u = S + bv[p];
+    for (int p = 0; p < 4; ++p) {
+      const double u = S + bv[p];
 #pragma unroll
-    for (int q = p + 1; q < 4; ++q) Bt[p][q] = Bt[q][p] = u + bv[q];
-    Bt[p][p] = fma(4.0, bv[p], S2);
+      for (int q = p + 1; q < 4; ++q) Bt[p][q] = Bt[q][p] = u + bv[q];
+      Bt[p][p] = fma(4.0, bv[p], S2);
+    }
+  } else {
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int q = p; q < 4; ++q) {
+        double b = bv[0] * kN1Rule[RULE - 1][0][sym4(p, q)];
+#pragma unroll
+        for (int m = 1; m < 4; ++m) b = fma(bv[m], kN1Rule[RULE - 1][m][sym4(p, q)], b);
+        Bt[p][q] = Bt[q][p] = b;
+      }
   }
   double xe[6];
   xe[0] = in.template x<cube_edge(O, 0)>();
@@ -127,15 +144,15 @@ __device__ __forceinline__ void element_gram(const Tab& tb, const In& in, double
 
 // the six elements of the cube (validity by anchor sum class); Tabs:
 // template <int O> tab() -> the orientation's table accessor
-template <typename Tabs, typename In>
+template <int RULE = 0, typename Tabs, typename In>
 __device__ __forceinline__ void cube_elements(const Tabs& ts, const In& in, double (&Y)[19], bool vWU, bool vMid,
                                               bool vWD) {
-  element_gram<WU>(ts.template tab<WU>(), in, Y, vWU);
-  element_gram<BU>(ts.template tab<BU>(), in, Y, vMid);
-  element_gram<BD>(ts.template tab<BD>(), in, Y, vMid);
-  element_gram<GU>(ts.template tab<GU>(), in, Y, vMid);
-  element_gram<GD>(ts.template tab<GD>(), in, Y, vMid);
-  element_gram<WD>(ts.template tab<WD>(), in, Y, vWD);
+  element_gram<WU, RULE>(ts.template tab<WU>(), in, Y, vWU);
+  element_gram<BU, RULE>(ts.template tab<BU>(), in, Y, vMid);
+  element_gram<BD, RULE>(ts.template tab<BD>(), in, Y, vMid);
+  element_gram<GU, RULE>(ts.template tab<GU>(), in, Y, vMid);
+  element_gram<GD, RULE>(ts.template tab<GD>(), in, Y, vMid);
+  element_gram<WD, RULE>(ts.template tab<WD>(), in, Y, vWD);
 }
 
 // the six orientation rows of an N1GramTable in shared memory

@@ -416,10 +416,11 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
         launch_n1_cubes(x, coeffs_[0]->data(level), coeffs_[1]->data(level), y, ld.macros.get(), nm,
                         ld.lay.macro_stride, ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, t.n1.get(), s);
       } else if (n1_kernel_mode() == 3) {
+        const int rule = rule_index();
         for (int pass = 0; pass < 2; ++pass)
           launch_n1_fold(t.n1g.get(), ld.macros.get(), pass, x, coeffs_[0]->data(level), coeffs_[1]->data(level), y,
                          ld.fold_tasks.get() + 4 * ld.fold_range[2 * pass], ld.fold_range[2 * pass + 1],
-                         ld.lay.macro_stride, ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, s);
+                         ld.lay.macro_stride, ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, rule, s);
       } else {
         for (int pass = 0; pass < 2; ++pass)
           for (std::size_t g = 0; g < ld.group_tasks.size(); ++g) {
@@ -432,12 +433,12 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
       break;
     }
     case Form::P2VDiffusion:
-      if (kernel_variant_ == 1)
+      if (kernel_variant_ == 1 && rule_index() == 0)
         launch_p2v_cubes(x, coeffs_[0]->data(level), y, ld.macros.get(), nm, ld.lay.macro_stride,
                          ld.lay.class_stride, ld.lay.n, t.p2v.get(), s);
       else
         launch_p2v_cubes2(x, coeffs_[0]->data(level), y, ld.macros.get(), nm, ld.lay.macro_stride,
-                          ld.lay.class_stride, ld.lay.n, t.p2v.get(), s);
+                          ld.lay.class_stride, ld.lay.n, t.p2v.get(), rule_index(), s);
       break;
     default:
       fail_internal("kernel_apply: unsupported form");
@@ -445,6 +446,20 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
   if (ev_stop) TETMF_CUDA(cudaEventRecord(ev_stop, s));
   launch_interface_sum(y, ld.group_offsets.get(), ld.group_copies.get(), ld.groups.num_groups(), s);
   if (ld.exchange) ld.exchange->run(y, s);
+}
+
+void Operator::set_quadrature(int degree) {
+  if (degree < 0 || degree > 6) fail_arg("quadrature: degree must be 0 (exact) or 1..6");
+  quad_degree_ = degree;
+}
+
+int Operator::rule_index() const {
+  int r = 0;
+  if (form_ == Form::N1CurlCurlMass && (quad_degree_ == 1 || quad_degree_ == 2)) r = quad_degree_;
+  if (form_ == Form::P2VDiffusion && quad_degree_ >= 1 && quad_degree_ <= 3) r = quad_degree_;
+  if (r != 0 && (kernel_variant_ != 0 || (form_ == Form::N1CurlCurlMass && n1_kernel_mode() != 3)))
+    fail_arg("quadrature: under-integrating rules run on the default kernels only");
+  return r;
 }
 
 void Operator::diagonal(Function& d, int level) {
@@ -468,12 +483,13 @@ void Operator::diagonal(Function& d, int level) {
       case Form::N1CurlCurlMass: {
         auto& cl = ctx_->level(Space::P1, level);
         launch_n1_diagonal(y, coeffs_[0]->data(level), coeffs_[1]->data(level), ld.macros.get(), nm,
-                           ld.lay.macro_stride, ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, t.n1g.get(), s);
+                           ld.lay.macro_stride, ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, t.n1g.get(),
+                           rule_index(), s);
         break;
       }
       case Form::P2VDiffusion:
         launch_p2v_diagonal(coeffs_[0]->data(level), y, ld.macros.get(), nm, ld.lay.macro_stride,
-                            ld.lay.class_stride, ld.lay.n, t.p2v.get(), s);
+                            ld.lay.class_stride, ld.lay.n, t.p2v.get(), rule_index(), s);
         break;
       default:
         fail_arg("diagonal: not available for this form");

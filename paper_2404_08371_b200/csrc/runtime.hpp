@@ -178,8 +178,17 @@ public:
   // 0 = optimized kernels (default), 1 = first-version kernels (k_apply_v1.cu),
   // kept selectable for A/B parity tests and the bench's history
   void set_kernel_variant(int v) { kernel_variant_ = v; }
+  // integration rule of apply / diagonal: 0 = exact (default; equals the
+  // reference's reference_apply), d = 1..6: the reference's quadrature(d)
+  // (FormSystem::apply(v, coeffs, quadrature(d)), forms.cpp:195-255). P1 and
+  // P1K are exact for every d; N1 is under-integrated for d <= 2, P2V for
+  // d <= 3 ("U", forms.cpp:12)
+  void set_quadrature(int degree);
+  int quadrature() const { return quad_degree_; }
 
 private:
+  // rule index of the element kernels: 0 exact, else the degree
+  int rule_index() const;
   struct LevelTables {
     DeviceBuffer<P1DeviceTable> p1;
     DeviceBuffer<N1DeviceTable> n1;
@@ -198,6 +207,7 @@ private:
   DeviceBuffer<double> ref_scratch_;
   bool profiling_ = false;
   int kernel_variant_ = 0;
+  int quad_degree_ = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events_;
   std::size_t events_used_ = 0;
   double prof_ms_ = 0.0;

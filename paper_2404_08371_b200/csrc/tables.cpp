@@ -1,5 +1,6 @@
 // tables.cpp -- exact per-orientation tensors (host).
 #include "tables.hpp"
+#include "quadrature.hpp"
 
 #include <cmath>
 #include <cstring>
@@ -309,6 +310,64 @@ P2VTable p2v_table(const MacroMesh& mesh, int macro, int level) {
         }
   }
   return out;
+}
+
+namespace {
+// barycentric coordinates of a reference point
+void bary(double x, double y, double z, double l[4]) {
+  l[0] = 1.0 - x - y - z;
+  l[1] = x;
+  l[2] = y;
+  l[3] = z;
+}
+} // namespace
+
+void p2v_rule_moments(int degree, double C[10][10]) {
+  if (degree == 0) {
+    p2v_moments(C);
+    return;
+  }
+  const QuadRule r = quadrature_rule(degree);
+  for (int m = 0; m < 10; ++m)
+    for (int k = 0; k < 10; ++k) C[m][k] = 0.0;
+  for (int q = 0; q < r.size(); ++q) {
+    double l[4];
+    bary(r.x[q], r.y[q], r.z[q], l);
+    for (int m = 0; m < 10; ++m) {
+      const double psi = m < 4 ? l[m] * (2.0 * l[m] - 1.0)
+                               : 4.0 * l[kLocalEdge[m - 4][0]] * l[kLocalEdge[m - 4][1]];
+      for (int a = 0; a < 4; ++a)
+        for (int b = a; b < 4; ++b) C[m][sym4(a, b)] += 6.0 * r.w[q] * psi * l[a] * l[b];
+    }
+  }
+}
+
+void n1_rule_moments(int degree, double R[4][10]) {
+  for (int m = 0; m < 4; ++m)
+    for (int k = 0; k < 10; ++k) R[m][k] = 0.0;
+  if (degree == 0) {  // exact: 120 (1/vol) int lambda_m lambda_p lambda_q = alpha!
+    for (int m = 0; m < 4; ++m)
+      for (int a = 0; a < 4; ++a)
+        for (int b = a; b < 4; ++b) {
+          int e[4] = {0, 0, 0, 0};
+          ++e[m];
+          ++e[a];
+          ++e[b];
+          double f = 1.0;
+          for (int i = 0; i < 4; ++i)
+            for (int j = 2; j <= e[i]; ++j) f *= j;
+          R[m][sym4(a, b)] = f;
+        }
+    return;
+  }
+  const QuadRule r = quadrature_rule(degree);
+  for (int q = 0; q < r.size(); ++q) {
+    double l[4];
+    bary(r.x[q], r.y[q], r.z[q], l);
+    for (int m = 0; m < 4; ++m)
+      for (int a = 0; a < 4; ++a)
+        for (int b = a; b < 4; ++b) R[m][sym4(a, b)] += 720.0 * r.w[q] * l[m] * l[a] * l[b];
+  }
 }
 
 void p2v_moments(double C[10][10]) {

@@ -112,6 +112,13 @@ struct P2VTable {
 };
 P2VTable p2v_table(const MacroMesh& mesh, int macro, int level);
 void p2v_moments(double C[10][10]);
+// the same moments under quadrature(degree) (degree 0: exact): C[m][sym4(r, s)]
+// = 6 sum_q w_q psi_m lambda_r lambda_s at the rule's points
+void p2v_rule_moments(int degree, double C[10][10]);
+// N1 mass moments: R[m][sym4(p, q)] = 120 (1/vol) int lambda_m lambda_p lambda_q
+// (exact: alpha!, so sum_m beta_m R[m][pq] = S + beta_p + beta_q, 2S + 4 beta_p
+// on the diagonal -- the Gram form's B); degree > 0: under quadrature(degree)
+void n1_rule_moments(int degree, double R[4][10]);
 // packed index of (i, j), i <= j < 10
 TM_HD constexpr int sym10(int i, int j) {
   if (i > j) { const int t = i; i = j; j = t; }
