@@ -48,13 +48,18 @@ CONFIGS = {
     "c4": dict(name="P1 -Laplace cube6 L8 (config 4, strong scaling)", mesh="cube6", form="P1", level=8),
     "c5": dict(name="N1 alpha curl curl + beta, 48 macros/GPU L8 (config 5, weak scaling)", mesh=None,
                form="N1", level=8),
+    # SURVEY.md 8(f) #2 (not a BASELINE config): the paper's P2V form
+    "p2v": dict(name="P2V -div(k grad), u and k in P2, cube6 L8 (SURVEY 8(f) #2)", mesh="cube6", form="P2V",
+                level=8),
 }
 WEAK_MESH = {1: "cubes2x2x2", 2: "cubes2x2x4", 4: "cubes2x4x4", 8: "cubes4x4x4"}
 CPU_SAMPLE = {  # bounded sample of each workload for the CPU reference leg
     "c1": ("single-tet", 6), "c2": ("single-tet", 6), "c3": ("single-tet", 5),
-    "c4": ("cube6", 6), "c5": ("cubes2x2x2", 4),
+    "c4": ("cube6", 6), "c5": ("cubes2x2x2", 4), "p2v": ("cube6", 4),
 }
-FLOP_PER_ELEM = {"P1": None, "P1K": None, "N1": 264.0}
+# P2V: the factored algorithm's count (k_p2v.cu: K 190, U 28, W 112, Z 112,
+# contractions 28, accumulation 10 flop); the table form needs 1300
+FLOP_PER_ELEM = {"P1": None, "P1K": None, "N1": 264.0, "P2V": 480.0}
 
 
 def lattice_counts(mesh_macros: int, level: int, form: str):
@@ -135,8 +140,8 @@ def cpu_reference_sample(cfg_key: str, seconds: float = 12.0, verbatim: bool = T
     r = RefSystem(mesh_arg, cfg["form"], level, fixed=not verbatim)
     x = r.seeded_input(42)
     c0, c1 = r.coefficients()
-    # same rule class as the GPU: exact, cheapest (P1: 2, N1: 3)
-    degree = 3 if cfg["form"] == "N1" else 2
+    # same rule class as the GPU: exact, cheapest (P1: 2, N1: 3, P2V: 4)
+    degree = {"N1": 3, "P2V": 4}.get(cfg["form"], 2)
     r.apply(x, c0, c1, degree)  # warm-up fills the star / map caches
     times = []
     t_end = time.time() + seconds
@@ -208,7 +213,7 @@ def run_gpu(a):
             raise SystemExit(f"config c5 supports 1/2/4/8 GPUs, got {ws}")
         cfg["mesh"] = WEAK_MESH[ws]
     level, form = cfg["level"], cfg["form"]
-    fid = {"P1": tm.FORM_P1, "P1K": tm.FORM_P1K, "N1": tm.FORM_N1}[form]
+    fid = {"P1": tm.FORM_P1, "P1K": tm.FORM_P1K, "N1": tm.FORM_N1, "P2V": tm.FORM_P2V}[form]
     sid = tm.FORM_SPACE[fid]
 
     nccl_id = None
@@ -228,8 +233,8 @@ def run_gpu(a):
         al.fill_coefficient(level, tm.COEFF_ALPHA)
         be.fill_coefficient(level, tm.COEFF_BETA)
         coeffs = [al, be]
-    elif form == "P1K":
-        k = tm.Function(ctx, tm.SPACE_P1)
+    elif form in ("P1K", "P2V"):
+        k = tm.Function(ctx, tm.SPACE_P1 if form == "P1K" else tm.SPACE_P2)
         k.fill_coefficient(level, tm.COEFF_K)
         coeffs = [k]
     op = tm.Operator(ctx, fid, coeffs)
@@ -303,18 +308,19 @@ def run_gpu(a):
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     local_counts = lattice_counts(nmac_local, level, form)
-    if form == "N1":
+    if form in ("N1", "P2V"):
         nd1_local = local_counts["nd1_edges"]
         p1_local = local_counts["p1_points"]
-        flops = FLOP_PER_ELEM["N1"] * local_counts["elements"]
+        flops = FLOP_PER_ELEM[form] * local_counts["elements"]
         fp64_peak = ctx.fp64_peak(1.0) if a.fp64_peak else None
-        bytes_alg = 8.0 * (2 * nd1_local + 2 * p1_local)
+        # N1: x, y (edges) + alpha, beta (points); P2V: x, k, y (points + edges)
+        bytes_alg = 8.0 * ((2 * nd1_local + 2 * p1_local) if form == "N1" else 3 * (nd1_local + p1_local))
         roof = {"bound": "fp64", "achieved": flops / (kern_avg_ms * 1e-3) / 1e12,
                 "peak": fp64_peak, "unit": "TFLOP/s",
                 "traffic": traffic["bytes_per_launch"] if traffic else None,
                 "traffic_source": traffic["source"] if traffic else None,
                 "frac": (flops / (kern_avg_ms * 1e-3) / 1e12) / fp64_peak if fp64_peak else None,
-                "flop_per_launch": flops, "flop_per_element": FLOP_PER_ELEM["N1"],
+                "flop_per_launch": flops, "flop_per_element": FLOP_PER_ELEM[form],
                 "peak_source": "measured FP64 DFMA-chain probe (tetmf_measure_fp64_peak) on this GPU",
                 "hbm": {"achieved": bytes_alg / (kern_avg_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                         "bytes_per_launch": bytes_alg}}
@@ -348,7 +354,7 @@ def run_gpu(a):
             "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": ws, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak" if a.config == "c5" else "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: x seeded uniform[-1,1] by canonical DoF key (SURVEY 8(d)); nodal P1 coefficients",
+            "data": "synthetic: x seeded uniform[-1,1] by canonical DoF key (SURVEY 8(d)); nodal coefficients (P1; P2 for P2V)",
             "config": {"workload": cfg["name"], "mesh": cfg["mesh"], "level": level, "form": form,
                        "macros": nmac_global, "dofs": n_unique, "elements": counts["elements"],
                        "parallelism": f"macro partition over {ws} GPU(s)",
@@ -366,6 +372,8 @@ def unique_dofs(mesh: str, form: str, level: int) -> int:
     """Unique DoFs of a Kuhn cube mesh / built-in mesh (closed forms,
     SURVEY.md Appendix B): P1 (N+1)^3 vertices; ND1 7N^3 + 9N^2 + 3N edges."""
     import re
+    if form == "P2V":  # P2: vertices + edge midpoints
+        return unique_dofs(mesh, "P1", level) + unique_dofs(mesh, "N1", level)
     n = 1 << level
     if mesh == "single-tet":
         tet = lambda k: (k + 1) * (k + 2) * (k + 3) // 6
