@@ -55,6 +55,21 @@ void launch_p1_stencil_v2(const double* x, double* y, const int* d_tasks, int nt
 void build_stencil2_tasks(int nmacros, int n, std::vector<int>& out);
 void launch_p1_stencil2(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
                         const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
+// K1 variant 5: interior-only row walk + face pass, L2 bulk prefetch (k_p1_stencil5.cu)
+void build_stencil5_tasks(int nmacros, int n, std::vector<int>& out);
+void launch_p1_stencil5(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
+// K1 variant 6: shared-memory boxes filled by per-row TMA bulk copies (k_p1_stencil5.cu)
+void build_stencil6_tasks(int nmacros, int n, std::vector<int>& out);
+void launch_p1_stencil6(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
+// K1 variant 7: persistent double-buffered shared-memory boxes (k_p1_stencil5.cu)
+void build_stencil7_tasks(int nmacros, int n, std::vector<int>& out);
+void launch_p1_stencil7(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
+// K1 variant 8: variant 7's boxes filled by 16-byte cp.async chunks (k_p1_stencil5.cu)
+void launch_p1_stencil8(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
 // K1 variant 4: 32 x 4 register tiles (k_p1_stencil_tile.cu)
 void build_stencil_tile_tasks(int nmacros, int n, std::vector<int>& out);
 void launch_p1_stencil_tile(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,

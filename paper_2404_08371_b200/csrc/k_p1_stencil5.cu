@@ -1,0 +1,782 @@
+// k_p1_stencil5.cu -- K1 variant 5: P1 -Laplace, interior stencil only +
+// separate face pass; CTA-wide L2 bulk prefetch of the block's plane slabs.
+//
+// Why (ncu of the two-plane row walk, profiles/r1_k1_v2_ncu_summary.txt):
+// ~220 warp instructions per 32 points, because every 32-column segment that
+// touches a macro face (x = 0, y = 0, z = 0 or the diagonal x+y+z = n) took
+// the per-lane stencil-variant path (30 table loads per row step) -- with
+// rows ~100 points long on average that is most segments. Here:
+//   * main kernel: the interior 15-point stencil (weights uniform per geometry
+//     group, in registers) for every point; stores are masked to interior
+//     points (x, y, z >= 1, x+y+z <= n-1), where all 15 neighbours exist;
+//   * face kernel: one thread per face point (4.6 % of the points at L8)
+//     gathers its neighbours with the point-type variant (tables.cpp) in the
+//     same summation order as the row walks (bitwise-equal results).
+//   * memory-level parallelism: a CTA = (macro, row block [y0, y0+kChunk),
+//     block of 2*kWarps planes); its planes' row slabs are contiguous stretches
+//     of the plane-major storage, so one thread per plane issues ONE
+//     cp.async.bulk.prefetch.L2 for the whole slab at CTA start: the CTA's
+//     whole read set is requested from DRAM at once instead of one row step
+//     (~2.5 KB per warp) at a time. The row walks then mostly hit L2.
+//
+// Warp w of a CTA walks the plane pair (z0 + 2w, z0 + 2w + 1) over all
+// 32-column segments of the block (register window along y, 10 coalesced
+// loads per row step for 2 points, 15 DFMA per point), as k_p1_stencil2.cu.
+#include "device.hpp"
+#include "runtime_check.hpp"
+
+namespace tetmf {
+
+namespace {
+
+#ifndef TETMF_P1F_WARPS
+#define TETMF_P1F_WARPS 4
+#endif
+#ifndef TETMF_P1F_CHUNK
+#define TETMF_P1F_CHUNK 8
+#endif
+#ifndef TETMF_P1F_PREFETCH
+#define TETMF_P1F_PREFETCH 1  // 0: no L2 bulk prefetch (A/B)
+#endif
+#ifndef TETMF_P1F_MINB
+#define TETMF_P1F_MINB 0
+#endif
+constexpr int kWarps = TETMF_P1F_WARPS;
+constexpr int kChunk = TETMF_P1F_CHUNK;
+constexpr int kPlanes = 2 * kWarps;
+#ifndef TETMF_P1F_AHEAD
+#define TETMF_P1F_AHEAD 0  // prefetch the slabs of the CTA this many places later (0: own)
+#endif
+constexpr int kAhead = TETMF_P1F_AHEAD;
+#ifndef TETMF_P1F_NEXTSEG
+#define TETMF_P1F_NEXTSEG 0  // 1: warm L1 with the next 32-column segment's rows while walking this one
+#endif
+
+struct Task5 {
+  int macro, z0, y0, pad;
+};
+
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// the same summation order as stencil_sum / stencil_var (k_p1_stencil2.cu)
+__device__ __forceinline__ double sum15(const double* __restrict__ w, double c00, double c01, double c0m, double cp0,
+                                        double cm0, double u00, double l00, double cm1, double cpm, double l01,
+                                        double u0m, double lp0, double um0, double lp1, double umm) {
+  double a0 = w[0] * c00, a1 = w[1] * c01, a2 = w[2] * c0m, a3 = w[3] * cp0;
+  a0 = fma(w[4], cm0, a0);
+  a1 = fma(w[5], u00, a1);
+  a2 = fma(w[6], l00, a2);
+  a3 = fma(w[7], cm1, a3);
+  a0 = fma(w[8], cpm, a0);
+  a1 = fma(w[9], l01, a1);
+  a2 = fma(w[10], u0m, a2);
+  a3 = fma(w[11], lp0, a3);
+  a0 = fma(w[12], um0, a0);
+  a1 = fma(w[13], lp1, a1);
+  a2 = fma(w[14], umm, a2);
+  return (a0 + a1) + (a2 + a3);
+}
+
+// One face point (x, y, z) of type `type` as a direct 15-point gather with
+// the variant weights, in the summation order of sum15. 32-bit incremental
+// indexing from the point's own index (neighbour offsets depend only on y
+// and the plane side m = n - z). Neighbours outside the lattice have zero
+// weights and are not read.
+__device__ __forceinline__ double gather_point(const double* __restrict__ X, const double* __restrict__ wt, int n,
+                                               int x, int y, int z) {
+  const int m = n - z;
+  const int i0 = static_cast<int>(plane_offset(n, z)) + y * (m + 1) - y * (y - 1) / 2 + x;
+  const int lr = m + 1 - y;              // row y length, plane z
+  const int tz = (m + 1) * (m + 2) / 2;  // points of plane z
+  const int up = i0 + tz - y;            // (x, y, z+1)
+  const int dn = i0 - (tz + m + 2) + y;  // (x, y, z-1): plane z-1 holds tz + m + 2 points
+  const bool xm = x > 0, ym = y > 0, zm = z > 0, pp = x + y + z < n;
+  // stencil_offset order (tables.hpp): centre, then +/- of the 7 edge directions
+  double v[15];
+  v[0] = __ldg(X + i0);
+  v[1] = pp ? __ldg(X + i0 + 1) : 0.0;                // (+1, 0, 0)
+  v[2] = xm ? __ldg(X + i0 - 1) : 0.0;                // (-1, 0, 0)
+  v[3] = pp ? __ldg(X + i0 + lr) : 0.0;               // (0, +1, 0)
+  v[4] = ym ? __ldg(X + i0 - lr - 1) : 0.0;           // (0, -1, 0): row y-1 holds lr + 1 points
+  v[5] = pp ? __ldg(X + up) : 0.0;                    // (0, 0, +1)
+  v[6] = zm ? __ldg(X + dn) : 0.0;                    // (0, 0, -1)
+  v[7] = ym ? __ldg(X + i0 - lr) : 0.0;               // (+1, -1, 0)
+  v[8] = xm ? __ldg(X + i0 + lr - 1) : 0.0;           // (-1, +1, 0)
+  v[9] = zm ? __ldg(X + dn + 1) : 0.0;                // (+1, 0, -1)
+  v[10] = xm ? __ldg(X + up - 1) : 0.0;               // (-1, 0, +1)
+  v[11] = zm ? __ldg(X + dn + lr + 1) : 0.0;          // (0, +1, -1): row y of plane z-1 holds lr + 1 points
+  v[12] = ym ? __ldg(X + up - lr) : 0.0;              // (0, -1, +1): row y-1 of plane z+1 holds lr points
+  v[13] = zm ? __ldg(X + dn + lr + 2) : 0.0;          // (+1, +1, -1)
+  v[14] = (xm && ym) ? __ldg(X + up - lr - 1) : 0.0;  // (-1, -1, +1)
+  double w[15];
+#pragma unroll
+  for (int k = 0; k < 15; ++k) w[k] = __ldg(wt + k);
+  return sum15(w, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9], v[10], v[11], v[12], v[13], v[14]);
+}
+
+#if TETMF_P1F_MINB > 0
+__global__ void __launch_bounds__(32 * kWarps, TETMF_P1F_MINB)
+#else
+__global__ void __launch_bounds__(32 * kWarps)
+#endif
+p1_interior_kernel(const double* __restrict__ xin, double* __restrict__ yout, const Task5* __restrict__ tasks,
+                   int ntasks, i64 stride, int n, const P1DeviceTable* __restrict__ tabs, const MacroDesc* __restrict__ macros) {
+  const Task5 t = tasks[blockIdx.x];
+  const int y0 = t.y0;
+  const double* __restrict__ Xm = xin + static_cast<i64>(t.macro) * stride;
+  double* __restrict__ Ym = yout + static_cast<i64>(t.macro) * stride;
+  if (TETMF_P1F_PREFETCH && threadIdx.x < kPlanes + 2) {
+    // slabs of the CTA kAhead places later in the task list (a later wave:
+    // its data lands in L2 while this CTA works), or this CTA's own (kAhead 0;
+    // the first wave also takes its own): plane p rows max(y0-1, 0) ..
+    // min(y0+kChunk, n-p), one contiguous stretch
+    auto prefetch = [&](const Task5& u) {
+      const int p = u.z0 - 1 + static_cast<int>(threadIdx.x);
+      const int ya = u.y0 > 0 ? u.y0 - 1 : 0;
+      if (p >= 0 && p <= n - ya) {
+        const int yb = min(u.y0 + kChunk, n - p);
+        const i64 P = plane_offset(n, p);
+        const i64 g0 = (P + row_offset(n, p, ya)) & ~i64(1);
+        const i64 g1 = (P + row_offset(n, p, yb + 1) + 1) & ~i64(1);
+        bulk_prefetch_l2(xin + static_cast<i64>(u.macro) * stride + g0, static_cast<unsigned>((g1 - g0) * 8));
+      }
+    };
+    if (kAhead == 0 || static_cast<int>(blockIdx.x) < kAhead) prefetch(t);
+    if (kAhead > 0 && static_cast<int>(blockIdx.x) + kAhead < ntasks) prefetch(tasks[blockIdx.x + kAhead]);
+  }
+  const int lane = threadIdx.x & 31;
+  const int z = t.z0 + 2 * static_cast<int>(threadIdx.x >> 5);
+  if (z > n - y0) return;  // no rows of the block in this plane
+  const double* __restrict__ tab = &tabs[macros[t.macro].group].stencil[0][0];
+
+  const bool hasL = z > 0, hasB = z + 1 <= n, hasU = z + 2 <= n;
+  const int ra00 = static_cast<int>(plane_offset(n, z) + row_offset(n, z, y0));
+  const int rl00 = hasL ? static_cast<int>(plane_offset(n, z - 1) + row_offset(n, z - 1, y0)) : ra00;
+  const int rb00 = hasB ? static_cast<int>(plane_offset(n, z + 1) + row_offset(n, z + 1, y0)) : ra00;
+  const int ru00 = hasU ? static_cast<int>(plane_offset(n, z + 2) + row_offset(n, z + 2, y0)) : rb00;
+  const int la00 = n - z - y0 + 1;
+  const int ll00 = hasL ? la00 + 1 : la00;
+  const int lb00 = hasB ? la00 - 1 : la00;
+  const int lu00 = hasU ? la00 - 2 : lb00;
+  // interior: x >= 1, y >= 1, z >= 1 and x + y + z <= n - 1
+  const bool zA = z >= 1;
+
+  for (int x0 = 0; x0 < la00; x0 += 32) {
+    const int px = x0 + lane;
+    const double* __restrict__ X = Xm + px;
+    double* __restrict__ Y = Ym + px;
+    if (TETMF_P1F_NEXTSEG && x0 + 32 < la00) {
+      // rows y0-1 .. y0+kChunk of this warp's planes A, B (and L / U at the
+      // CTA's plane-block edges; inner L / U planes are other warps' A / B)
+      const double* Xn = X + 32;
+      const int wid = static_cast<int>(threadIdx.x >> 5);
+      int a = ra00 - (la00 + 1), b = rb00 - (lb00 + 1), l = rl00, u = ru00 - (lu00 + 1);
+      int lna = la00 + 1, lnb = lb00 + 1, lnl = ll00, lnu = lu00 + 1;
+#pragma unroll 1
+      for (int r = 0; r < kChunk + 2; ++r) {
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(Xn + a));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(Xn + b));
+        if (wid == 0 && r < kChunk + 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(Xn + l));
+        if (wid == kWarps - 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(Xn + u));
+        a += lna; b += lnb; l += lnl; u += lnu;
+        --lna; --lnb; --lnl; --lnu;
+      }
+    }
+    // per-lane weights: the x = 0 column (lane 0 of segment 0) walks with the
+    // x = 0 face variant (type 1), every other column with the interior stencil
+    double w[15];
+    {
+      const double* __restrict__ wt = tab + (px == 0 ? 16 : 0);
+#pragma unroll
+      for (int k = 0; k < 15; ++k) w[k] = __ldg(wt + k);
+    }
+    int ra = ra00, rl = rl00, rb = rb00, ru = ru00;
+    int la = la00, ll = ll00, lb = lb00, lu = lu00;
+    const int ram = ra - (la + 1), rbm = rb - (lb + 1), rum = ru - (lu + 1);
+    double Am0 = __ldg(X + ram), Am1 = __ldg(X + ram + 1);
+    double A0m = __ldg(X + ra - 1), A00 = __ldg(X + ra), A01 = __ldg(X + ra + 1);
+    double L00 = __ldg(X + rl), L01 = __ldg(X + rl + 1);
+    double Bmm = __ldg(X + rbm - 1), Bm0 = __ldg(X + rbm), Bm1 = __ldg(X + rbm + 1);
+    double B0m = __ldg(X + rb - 1), B00 = __ldg(X + rb), B01 = __ldg(X + rb + 1);
+    double Umm = __ldg(X + rum - 1), Um0 = __ldg(X + rum);
+    // s = px + yy + z of plane A's point at row yy; the walk stores points of
+    // type 0 and 1: y >= 1, z >= 1, x + y + z <= n - 1
+    const int s0 = px + y0 + z;
+#pragma unroll
+    for (int r = 0; r < kChunk; ++r) {
+      const int yy = y0 + r;
+      const int rl1 = rl + ll, ra1 = ra + la, rb1 = rb + lb;
+      const double Lp0 = __ldg(X + rl1), Lp1 = __ldg(X + rl1 + 1);
+      const double Apm = __ldg(X + ra1 - 1), Ap0 = __ldg(X + ra1), Ap1 = __ldg(X + ra1 + 1);
+      const double Bpm = __ldg(X + rb1 - 1), Bp0 = __ldg(X + rb1), Bp1 = __ldg(X + rb1 + 1);
+      const double U0m = __ldg(X + ru - 1), U00 = __ldg(X + ru);
+      const double fa = sum15(w, A00, A01, A0m, Ap0, Am0, B00, L00, Am1, Apm, L01, B0m, Lp0, Bm0, Lp1, Bmm);
+      const double fb = sum15(w, B00, B01, B0m, Bp0, Bm0, U00, A00, Bm1, Bpm, A01, U0m, Ap0, Um0, Ap1, Umm);
+      if (yy >= 1 && zA && s0 + r <= n - 1) Y[ra] = fa;
+      if (yy >= 1 && s0 + r + 1 <= n - 1) Y[rb] = fb;
+      Am0 = A00; Am1 = A01;
+      A0m = Apm; A00 = Ap0; A01 = Ap1;
+      L00 = Lp0; L01 = Lp1;
+      Bmm = B0m; Bm0 = B00; Bm1 = B01;
+      B0m = Bpm; B00 = Bp0; B01 = Bp1;
+      Umm = U0m; Um0 = U00;
+      ru += lu;
+      rl = rl1; ra = ra1; rb = rb1;
+      --ll; --la; --lb; --lu;
+    }
+  }
+  // diagonal points (x + y + z = n) of the block's rows: lanes 0..kChunk-1
+  // plane A (z), lanes 16..16+kChunk-1 plane B (z+1); y = 0 and z = 0 belong
+  // to the face kernel
+  {
+    const int zz = z + (lane >> 4), yy = y0 + (lane & 15);
+    if ((lane & 15) < kChunk && zz >= 1 && yy >= 1 && yy <= n - zz) {
+      const int xx = n - zz - yy;
+      Ym[lattice_index(n, xx, yy, zz)] = gather_point(Xm, tab + 16 * (8 | (xx == 0 ? 1 : 0)), n, xx, yy, zz);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Variant 6: the same two-plane walk, fed from shared memory. A CTA owns the
+// box (macro, planes [z0, z0 + 2*kWarps6), rows [y0, y0 + kRows6), columns
+// [x0, x0 + kCols6)); at start one thread per (plane, row) of the box plus
+// halo (planes z0-1 .. z0+2*kWarps6, rows y0-1 .. y0+kRows6) issues ONE 1-D
+// TMA bulk copy (cp.async.bulk) of the row piece [x0-1, x0+kCols6+1) into its
+// own shared-memory row, all completing on one mbarrier. The whole read set
+// of the CTA is thus in flight at once (no registers held, no per-step
+// latency), and the walk reads shared memory only. Several CTAs per SM
+// overlap one CTA's copies with the others' walks.
+// Shared-memory row i holds global indices [base_i, base_i + kPitch6) with
+// base_i = (start_i + x0 - 2) & ~1 (16-byte aligned copies); column x of the
+// row that starts at global index g sits at (g + x0) & 1 ... see srow().
+// Copied pieces are real lattice data or finite neighbours (the previous /
+// next row, the guard regions): every read of a stored point is in-lattice,
+// and lanes that do not store may read anything finite or not.
+#ifndef TETMF_P1S_COLS
+#define TETMF_P1S_COLS 64
+#endif
+#ifndef TETMF_P1S_ROWS
+#define TETMF_P1S_ROWS 8   // measured best with 2 warps (cube6 L8 117.7 us; 4 rows x 4 warps 135 us)
+#endif
+#ifndef TETMF_P1S_WARPS
+#define TETMF_P1S_WARPS 2
+#endif
+#ifndef TETMF_P1S_MINB
+#define TETMF_P1S_MINB 0
+#endif
+constexpr int kCols6 = TETMF_P1S_COLS;
+constexpr int kRows6 = TETMF_P1S_ROWS;
+constexpr int kWarps6 = TETMF_P1S_WARPS;
+constexpr int kSegs6 = kCols6 / 32;
+constexpr int kPlanes6 = 2 * kWarps6 + 2;        // with the halo planes
+constexpr int kRowsH6 = kRows6 + 2;              // with the halo rows
+constexpr int kCopies6 = kPlanes6 * kRowsH6;
+constexpr int kPitch6 = kCols6 + 6;              // doubles per shared-memory row
+static_assert(kCols6 % 32 == 0 && kRows6 <= 16 && kCopies6 <= 32 * kWarps6, "p1 smem tiling");
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+#if TETMF_P1S_MINB > 0
+__global__ void __launch_bounds__(32 * kWarps6, TETMF_P1S_MINB)
+#else
+__global__ void __launch_bounds__(32 * kWarps6)
+#endif
+p1_smem_kernel(const double* __restrict__ xin, double* __restrict__ yout, const Task5* __restrict__ tasks, i64 stride,
+               int n, const P1DeviceTable* __restrict__ tabs, const MacroDesc* __restrict__ macros) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) unsigned long long bar;
+  const Task5 t = tasks[blockIdx.x];
+  const int y0 = t.y0, z0 = t.z0, x0 = t.pad;
+  const double* __restrict__ Xm = xin + static_cast<i64>(t.macro) * stride;
+  double* __restrict__ Ym = yout + static_cast<i64>(t.macro) * stride;
+  const int tid = static_cast<int>(threadIdx.x);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "r"(kCopies6));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid < kCopies6) {
+    const int pi = tid / kRowsH6, ri = tid - pi * kRowsH6;
+    const int p = min(max(z0 - 1 + pi, 0), n);  // missing planes alias the nearest (zero weights)
+    const int y = y0 - 1 + ri;                  // -1 for the halo of block 0: the formula's finite neighbours
+    const int m = n - p;
+    unsigned bytes = 0;
+    if (y <= m) {
+      const int rs = static_cast<int>(plane_offset(n, p)) + y * (m + 1) - y * (y - 1) / 2;
+      const int base = (rs + x0 - 2) & ~1;
+      const int g0 = (rs + x0 - 1) & ~1;
+      const int g1 = (rs + min(x0 + kCols6 + 1, m + 2 - y) + 1) & ~1;  // row end + 1 at most
+      if (g1 > g0) {
+        bytes = static_cast<unsigned>(g1 - g0) * 8u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(sm + tid * kPitch6 + (g0 - base))),
+            "l"(Xm + g0), "r"(bytes), "r"(smem_u32(&bar))
+            : "memory");
+      }
+    }
+    if (bytes == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar)) : "memory");
+  }
+  const int lane = tid & 31, wid = tid >> 5;
+  const int z = z0 + 2 * wid;
+  const bool work = z <= n - y0 && x0 <= n - y0 - z;  // the warp's planes hold points of the box
+  const double* __restrict__ tab = &tabs[macros[t.macro].group].stencil[0][0];
+  if (work) {
+    // wait for the box (all copies landed)
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "W6_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0, %1;\n"
+        "@!p bra W6_%=;\n"
+        "}\n" ::"r"(smem_u32(&bar)),
+        "r"(0x989680u)
+        : "memory");
+    // planes L = z-1, A = z, B = z+1, U = z+2 at box plane indices 2w .. 2w+3
+    // (clamped at the lattice ends like the copies); global row starts and
+    // lengths as in the direct walk
+    const int pl = max(z - 1, 0), pa = z, pb = min(z + 1, n), pu = min(z + 2, n);
+    auto rstart = [&](int p, int y) { return static_cast<int>(plane_offset(n, p)) + y * (n - p + 1) - y * (y - 1) / 2; };
+    const int PL = 2 * wid, PA = PL + 1, PB = PL + 2, PU = PL + 3;
+    const bool zA = z >= 1;
+#pragma unroll 1
+    for (int sg = 0; sg < kSegs6; ++sg) {
+      const int px = x0 + 32 * sg + lane;
+      if (x0 + 32 * sg > n - y0 - z) break;  // segment past the row ends of both planes
+      double w[15];
+      {
+        const double* __restrict__ wt = tab + (px == 0 ? 16 : 0);
+#pragma unroll
+        for (int k = 0; k < 15; ++k) w[k] = __ldg(wt + k);
+      }
+      // global row starts at row y0 (A, B, L) / y0-1 (U's trailing row) and
+      // the shared-memory element index of column px in each row:
+      //   idx(pi, ri, g) = (pi*kRowsH6 + ri)*kPitch6 + 2 + ((g + x0) & 1) - x0 + px
+      // (base = (g + x0 - 2) & ~1, so g + px - base = px - x0 + 2 + ((g + x0) & 1))
+      auto idx = [&](int pi, int ri, int g) {
+        return (pi * kRowsH6 + ri) * kPitch6 + 2 + ((g + x0) & 1) - x0 + px;
+      };
+      int ga = rstart(pa, y0), gl = rstart(pl, y0), gb = rstart(pb, y0), gu = rstart(pu, y0);
+      int la = n - pa - y0 + 1, ll = n - pl - y0 + 1, lb = n - pb - y0 + 1, lu = n - pu - y0 + 1;
+      const int gam = ga - (la + 1), gbm = gb - (lb + 1), gum = gu - (lu + 1);
+      const int iam = idx(PA, 0, gam), ia0 = idx(PA, 1, ga), il0 = idx(PL, 1, gl);
+      const int ibm = idx(PB, 0, gbm), ib0 = idx(PB, 1, gb), ium = idx(PU, 0, gum);
+      double Am0 = sm[iam], Am1 = sm[iam + 1];
+      double A0m = sm[ia0 - 1], A00 = sm[ia0], A01 = sm[ia0 + 1];
+      double L00 = sm[il0], L01 = sm[il0 + 1];
+      double Bmm = sm[ibm - 1], Bm0 = sm[ibm], Bm1 = sm[ibm + 1];
+      double B0m = sm[ib0 - 1], B00 = sm[ib0], B01 = sm[ib0 + 1];
+      double Umm = sm[ium - 1], Um0 = sm[ium];
+      int yA = static_cast<int>(plane_offset(n, z)) + y0 * (n - z + 1) - y0 * (y0 - 1) / 2 + px;  // global y index, A
+      int yB = static_cast<int>(plane_offset(n, z + 1)) + y0 * (n - z) - y0 * (y0 - 1) / 2 + px;
+      const int s0 = px + y0 + z;
+#pragma unroll
+      for (int r = 0; r < kRows6; ++r) {
+        const int yy = y0 + r;
+        const int gl1 = gl + ll, ga1 = ga + la, gb1 = gb + lb;
+        const int il = idx(PL, r + 2, gl1), ia = idx(PA, r + 2, ga1), ib = idx(PB, r + 2, gb1), iu = idx(PU, r + 1, gu);
+        const double Lp0 = sm[il], Lp1 = sm[il + 1];
+        const double Apm = sm[ia - 1], Ap0 = sm[ia], Ap1 = sm[ia + 1];
+        const double Bpm = sm[ib - 1], Bp0 = sm[ib], Bp1 = sm[ib + 1];
+        const double U0m = sm[iu - 1], U00 = sm[iu];
+        const double fa = sum15(w, A00, A01, A0m, Ap0, Am0, B00, L00, Am1, Apm, L01, B0m, Lp0, Bm0, Lp1, Bmm);
+        const double fb = sum15(w, B00, B01, B0m, Bp0, Bm0, U00, A00, Bm1, Bpm, A01, U0m, Ap0, Um0, Ap1, Umm);
+        if (yy >= 1 && zA && s0 + r <= n - 1) Ym[yA] = fa;
+        if (yy >= 1 && s0 + r + 1 <= n - 1) Ym[yB] = fb;
+        yA += n - z + 1 - yy;
+        yB += n - z - yy;
+        Am0 = A00; Am1 = A01;
+        A0m = Apm; A00 = Ap0; A01 = Ap1;
+        L00 = Lp0; L01 = Lp1;
+        Bmm = B0m; Bm0 = B00; Bm1 = B01;
+        B0m = Bpm; B00 = Bp0; B01 = Bp1;
+        Umm = U0m; Um0 = U00;
+        gu += lu;
+        gl = gl1; ga = ga1; gb = gb1;
+        --ll; --la; --lb; --lu;
+      }
+    }
+    // diagonal points of the box rows (as in the direct walk), by the CTA
+    // whose column range holds them
+    const int zz = z + (lane >> 4), yy = y0 + (lane & 15);
+    if ((lane & 15) < kRows6 && zz >= 1 && zz <= n && yy >= 1 && yy <= n - zz) {
+      const int xx = n - zz - yy;
+      if (xx >= x0 && xx < x0 + kCols6)
+        Ym[lattice_index(n, xx, yy, zz)] = gather_point(Xm, tab + 16 * (8 | (xx == 0 ? 1 : 0)), n, xx, yy, zz);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Variant 7: persistent, double-buffered version of variant 6. Each CTA loops
+// over boxes (macro, 2*kPairs7 planes, kRows7 rows, kCols7 columns); while
+// its warps walk box k out of one shared-memory stage, the per-row TMA bulk
+// copies of box k+1 land in the other stage (full / empty mbarrier pair per
+// stage), so copy latency is off the critical path. Warp w walks plane pair
+// w / kSegs7, 32-column segment w % kSegs7 of the box; the segment-0 warp of
+// each pair also computes the pair's diagonal points (gathers, L2).
+#ifndef TETMF_P1P_COLS
+#define TETMF_P1P_COLS 64
+#endif
+#ifndef TETMF_P1P_ROWS
+#define TETMF_P1P_ROWS 8
+#endif
+#ifndef TETMF_P1P_PAIRS
+#define TETMF_P1P_PAIRS 2
+#endif
+#ifndef TETMF_P1P_NULL
+#define TETMF_P1P_NULL 0
+#endif
+#ifndef TETMF_P1P_MINB
+#define TETMF_P1P_MINB 0
+#endif
+constexpr int kCols7 = TETMF_P1P_COLS;
+constexpr int kRows7 = TETMF_P1P_ROWS;
+constexpr int kPairs7 = TETMF_P1P_PAIRS;
+constexpr int kSegs7 = kCols7 / 32;
+constexpr int kWarps7 = kPairs7 * kSegs7;
+constexpr int kPlanes7 = 2 * kPairs7 + 2;
+constexpr int kRowsH7 = kRows7 + 2;
+constexpr int kCopies7 = kPlanes7 * kRowsH7;
+constexpr int kPitch7 = kCols7 + 6;
+constexpr int kStage7 = kCopies7 * kPitch7;  // doubles per stage
+static_assert(kCols7 % 32 == 0 && kRows7 <= 16 && kCopies7 <= 32 * kWarps7, "p1 pipe tiling");
+
+// 32-bit lattice offsets (a level's storage fits in int for n <= 1022)
+__device__ __forceinline__ int tet32(int k) {
+  return static_cast<int>(static_cast<unsigned>((k + 1) * (k + 2)) * static_cast<unsigned>(k + 3) / 6u);
+}
+__device__ __forceinline__ int rstart32(int n, int p, int y) {
+  return tet32(n) - tet32(n - p) + y * (n - p + 1) - y * (y - 1) / 2;
+}
+
+__device__ __forceinline__ void mbar_wait_parity(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "W7_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra W7_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+
+// kAsync = false: per-row TMA bulk copies on full / empty mbarriers (variant 7);
+// kAsync = true: the same box rows as coalesced 16-byte cp.async chunks (one
+// warp per row, lanes over the row), one commit group per box, block-wide
+// barriers around each box (variant 8) -- no TMA engine per-copy cost.
+template <bool kAsync>
+#if TETMF_P1P_MINB > 0
+__global__ void __launch_bounds__(32 * kWarps7, TETMF_P1P_MINB)
+#else
+__global__ void __launch_bounds__(32 * kWarps7)
+#endif
+p1_pipe_kernel(const double* __restrict__ xin, double* __restrict__ yout, const Task5* __restrict__ tasks, int ntasks,
+               i64 stride, int n, const P1DeviceTable* __restrict__ tabs, const MacroDesc* __restrict__ macros) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) unsigned long long full[2], empty[2];
+  const int tid = static_cast<int>(threadIdx.x), lane = tid & 31, wid = tid >> 5;
+  if (!kAsync && tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[i])), "r"(kCopies7));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[i])), "r"(kWarps7));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // copy thread tid: (box plane pi, box row ri) of box ti into stage st
+  auto issue = [&](int ti, int st) {
+    const Task5 u = tasks[ti];
+    const int pi = tid / kRowsH7, ri = tid - pi * kRowsH7;
+    const int p = min(max(u.z0 - 1 + pi, 0), n);  // missing planes alias the nearest (zero weights)
+    const int y = u.y0 - 1 + ri;                   // -1 for the halo of block 0: finite neighbours
+    const int m = n - p, x0 = u.pad;
+    unsigned bytes = 0;
+    unsigned long long* bar = &full[st];
+    if (y <= m) {
+      const int rs = rstart32(n, p, y);
+      const int base = (rs + x0 - 2) & ~1;
+      const int g0 = (rs + x0 - 1) & ~1;
+      const int g1 = (rs + min(x0 + kCols7 + 1, m + 2 - y) + 1) & ~1;  // row end + 1 at most
+      if (g1 > g0) {
+        bytes = static_cast<unsigned>(g1 - g0) * 8u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(sm + st * kStage7 + tid * kPitch7 + (g0 - base))),
+            "l"(xin + static_cast<i64>(u.macro) * stride + g0), "r"(bytes), "r"(smem_u32(bar))
+            : "memory");
+      }
+    }
+    if (bytes == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+  };
+  auto issue_async = [&](int ti, int st) {
+    const Task5 u = tasks[ti];
+    for (int j = wid; j < kCopies7; j += kWarps7) {
+      const int pi = j / kRowsH7, ri = j - pi * kRowsH7;
+      const int p = min(max(u.z0 - 1 + pi, 0), n);
+      const int y = u.y0 - 1 + ri;
+      const int m = n - p, x0 = u.pad;
+      if (y > m) continue;
+      const int rs = rstart32(n, p, y);
+      const int base = (rs + x0 - 2) & ~1;
+      const int g0 = (rs + x0 - 1) & ~1;
+      const int g1 = (rs + min(x0 + kCols7 + 1, m + 2 - y) + 1) & ~1;
+      const double* src = xin + static_cast<i64>(u.macro) * stride + g0;
+      const unsigned dst = smem_u32(sm + st * kStage7 + j * kPitch7 + (g0 - base));
+      for (int c = lane; 2 * c < g1 - g0; c += 32)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * c), "l"(src + 2 * c) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const int G = static_cast<int>(gridDim.x);
+  if (kAsync) {
+    if (static_cast<int>(blockIdx.x) < ntasks) issue_async(blockIdx.x, 0);
+  } else if (tid < kCopies7 && static_cast<int>(blockIdx.x) < ntasks) {
+    issue(blockIdx.x, 0);
+  }
+  const int pr = wid / kSegs7, sg = wid - pr * kSegs7;
+  int k = 0;
+  for (int ti = static_cast<int>(blockIdx.x); ti < ntasks; ti += G, ++k) {
+    const int st = k & 1;
+    if (kAsync) {
+      // the other stage was released by the barrier that ended box k-1
+      if (ti + G < ntasks) issue_async(ti + G, st ^ 1);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      __syncthreads();
+    } else if (tid < kCopies7 && ti + G < ntasks) {
+      // the other stage is free once every warp released box k-1
+      if (k >= 1) mbar_wait_parity(&empty[st ^ 1], static_cast<unsigned>((k - 1) >> 1) & 1u);
+      issue(ti + G, st ^ 1);
+    }
+    const Task5 t = tasks[ti];
+    const int y0 = t.y0, x0 = t.pad;
+    const int z = t.z0 + 2 * pr;
+    const double* __restrict__ Xm = xin + static_cast<i64>(t.macro) * stride;
+    double* __restrict__ Ym = yout + static_cast<i64>(t.macro) * stride;
+    const double* __restrict__ tab = &tabs[macros[t.macro].group].stencil[0][0];
+    const double* __restrict__ S = sm + st * kStage7;
+    if (!kAsync) mbar_wait_parity(&full[st], static_cast<unsigned>(k >> 1) & 1u);
+    const int xs = x0 + 32 * sg;
+    if (z <= n - y0 && xs <= n - y0 - z) {
+      const int px = xs + lane;
+      double w[15];
+      {
+        const double* __restrict__ wt = tab + (px == 0 ? 16 : 0);
+#pragma unroll
+        for (int q = 0; q < 15; ++q) w[q] = __ldg(wt + q);
+      }
+      const int pl = max(z - 1, 0), pb = min(z + 1, n), pu = min(z + 2, n);
+      constexpr int PL = 0, PA = 1, PB = 2, PU = 3;  // relative to the pair's first box plane 2*pr
+      const int pbase = 2 * pr * kRowsH7 * kPitch7 + 2 - x0 + px;
+      // shared-memory index of column px in box row ri of the row starting at g
+      auto idx = [&](int P, int ri, int g) { return pbase + (P * kRowsH7 + ri) * kPitch7 + ((g + x0) & 1); };
+      int ga = rstart32(n, z, y0), gl = rstart32(n, pl, y0), gb = rstart32(n, pb, y0), gu = rstart32(n, pu, y0);
+      int la = n - z - y0 + 1, ll = n - pl - y0 + 1, lb = n - pb - y0 + 1, lu = n - pu - y0 + 1;
+      const int iam = idx(PA, 0, ga - (la + 1)), ia0 = idx(PA, 1, ga), il0 = idx(PL, 1, gl);
+      const int ibm = idx(PB, 0, gb - (lb + 1)), ib0 = idx(PB, 1, gb), ium = idx(PU, 0, gu - (lu + 1));
+      double Am0 = S[iam], Am1 = S[iam + 1];
+      double A0m = S[ia0 - 1], A00 = S[ia0], A01 = S[ia0 + 1];
+      double L00 = S[il0], L01 = S[il0 + 1];
+      double Bmm = S[ibm - 1], Bm0 = S[ibm], Bm1 = S[ibm + 1];
+      double B0m = S[ib0 - 1], B00 = S[ib0], B01 = S[ib0 + 1];
+      double Umm = S[ium - 1], Um0 = S[ium];
+      int yA = ga + px, yB = rstart32(n, z + 1, y0) + px;  // z + 1 = n + 1: never stored
+      const int s0 = px + y0 + z;
+      const bool zA = z >= 1;
+#pragma unroll
+      for (int r = 0; r < kRows7; ++r) {
+        const int yy = y0 + r;
+        const int gl1 = gl + ll, ga1 = ga + la, gb1 = gb + lb;
+        const int il = idx(PL, r + 2, gl1), ia = idx(PA, r + 2, ga1), ib = idx(PB, r + 2, gb1), iu = idx(PU, r + 1, gu);
+        const double Lp0 = S[il], Lp1 = S[il + 1];
+        const double Apm = S[ia - 1], Ap0 = S[ia], Ap1 = S[ia + 1];
+        const double Bpm = S[ib - 1], Bp0 = S[ib], Bp1 = S[ib + 1];
+        const double U0m = S[iu - 1], U00 = S[iu];
+#if TETMF_P1P_NULL  // A/B floor: same loads and stores, no stencil arithmetic
+        const double fa = A00 + Ap0 + L00 + Lp1 + Am0, fb = B00 + Bp0 + U00 + U0m + Bpm + Bmm;
+#else
+        const double fa = sum15(w, A00, A01, A0m, Ap0, Am0, B00, L00, Am1, Apm, L01, B0m, Lp0, Bm0, Lp1, Bmm);
+        const double fb = sum15(w, B00, B01, B0m, Bp0, Bm0, U00, A00, Bm1, Bpm, A01, U0m, Ap0, Um0, Ap1, Umm);
+#endif
+        if (yy >= 1 && zA && s0 + r <= n - 1) Ym[yA] = fa;
+        if (yy >= 1 && s0 + r + 1 <= n - 1) Ym[yB] = fb;
+        yA += la;
+        yB += la - 1;
+        Am0 = A00; Am1 = A01;
+        A0m = Apm; A00 = Ap0; A01 = Ap1;
+        L00 = Lp0; L01 = Lp1;
+        Bmm = B0m; Bm0 = B00; Bm1 = B01;
+        B0m = Bpm; B00 = Bp0; B01 = Bp1;
+        Umm = U0m; Um0 = U00;
+        gu += lu;
+        gl = gl1; ga = ga1; gb = gb1;
+        --ll; --la; --lb; --lu;
+      }
+    }
+    if (sg == 0) {
+      // diagonal points (x + y + z = n) of the pair's box rows inside the box columns
+      const int zz = z + (lane >> 4), yy = y0 + (lane & 15);
+      if ((lane & 15) < kRows7 && zz >= 1 && zz <= n && yy >= 1 && yy <= n - zz) {
+        const int xx = n - zz - yy;
+        if (xx >= x0 && xx < x0 + kCols7)
+          Ym[lattice_index(n, xx, yy, zz)] = gather_point(Xm, tab + 16 * (8 | (xx == 0 ? 1 : 0)), n, xx, yy, zz);
+      }
+    }
+    if (kAsync) {
+      __syncthreads();
+    } else {
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
+    }
+  }
+}
+
+// Faces z = 0 and y = 0 (coalesced along x): thread per (macro, face f, point
+// of the face triangle); a point on both is computed by f = 0 (z = 0). Grid:
+// x = points of a face triangle, y = macro * 2 + f. The x = 0 face is walked
+// by the interior kernel's lane 0 with its variant weights, the diagonal
+// face by its per-block gathers.
+__global__ void __launch_bounds__(256) p1_face_kernel(const double* __restrict__ xin, double* __restrict__ yout,
+                                                      i64 stride, int n, const P1DeviceTable* __restrict__ tabs,
+                                                      const MacroDesc* __restrict__ macros) {
+  const int T = (n + 1) * (n + 2) / 2;
+  const int q = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x);
+  if (q >= T) return;
+  const int li = static_cast<int>(blockIdx.y >> 1), f = static_cast<int>(blockIdx.y & 1);
+  // (a, b) with a + b <= n, b-major: row b starts at S(b) = b(2n+3-b)/2
+  const float c = 2.0f * n + 3.0f;
+  int b = static_cast<int>((c - sqrtf(fmaxf(c * c - 8.0f * q, 0.0f))) * 0.5f);
+  b = min(max(b, 0), n);
+  while (b > 0 && b * (2 * n + 3 - b) / 2 > q) --b;
+  while (b < n && (b + 1) * (2 * n + 2 - b) / 2 <= q) ++b;
+  const int a = q - b * (2 * n + 3 - b) / 2;
+  const int x = a, y = f == 0 ? b : 0, z = f == 0 ? 0 : b;
+  if (f == 1 && z == 0) return;  // on the z = 0 face
+  const int type = (x == 0 ? 1 : 0) | (y == 0 ? 2 : 0) | (z == 0 ? 4 : 0) | (x + y + z == n ? 8 : 0);
+  const double* __restrict__ X = xin + static_cast<i64>(li) * stride;
+  const double* __restrict__ wt = &tabs[macros[li].group].stencil[type][0];
+  yout[static_cast<i64>(li) * stride + lattice_index(n, x, y, z)] = gather_point(X, wt, n, x, y, z);
+}
+
+} // namespace
+
+// CTA tasks (macro, z0, y0): row block [y0, y0+kChunk) x planes [z0, z0+2*kWarps)
+// with rows in the block (z0 <= n - y0); order macro, y0, z0.
+void build_stencil5_tasks(int nmacros, int n, std::vector<int>& out) {
+  out.clear();
+  for (int li = 0; li < nmacros; ++li)
+    for (int y0 = 0; y0 <= n; y0 += kChunk)
+      for (int z0 = 0; z0 <= n - y0; z0 += kPlanes) {
+        out.push_back(li);
+        out.push_back(z0);
+        out.push_back(y0);
+        out.push_back(0);
+      }
+}
+
+// CTA boxes of variant 6 (macro, z0, y0, x0): x0 < row length of (y0, z0)
+void build_stencil6_tasks(int nmacros, int n, std::vector<int>& out) {
+  out.clear();
+  for (int li = 0; li < nmacros; ++li)
+    for (int y0 = 0; y0 <= n; y0 += kRows6)
+      for (int z0 = 0; z0 <= n - y0; z0 += 2 * kWarps6)
+        for (int x0 = 0; x0 <= n - y0 - z0; x0 += kCols6) {
+          out.push_back(li);
+          out.push_back(z0);
+          out.push_back(y0);
+          out.push_back(x0);
+        }
+}
+
+void launch_p1_stencil6(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
+  if (ntasks == 0) return;
+  const std::size_t smem = static_cast<std::size_t>(kCopies6) * kPitch6 * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    TETMF_CUDA(cudaFuncSetAttribute(p1_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    configured = true;
+  }
+  p1_smem_kernel<<<static_cast<unsigned>(ntasks), 32 * kWarps6, smem, s>>>(
+      x, y, reinterpret_cast<const Task5*>(d_tasks), macro_stride, n, d_tables, d_macros);
+  check_launch("p1_smem");
+  const int T = (n + 1) * (n + 2) / 2;
+  p1_face_kernel<<<dim3(static_cast<unsigned>((T + 255) / 256), static_cast<unsigned>(2 * nmacros)), 256, 0, s>>>(
+      x, y, macro_stride, n, d_tables, d_macros);
+  check_launch("p1_face");
+}
+
+// CTA boxes of variant 7 (macro, z0, y0, x0)
+void build_stencil7_tasks(int nmacros, int n, std::vector<int>& out) {
+  out.clear();
+  for (int li = 0; li < nmacros; ++li)
+    for (int y0 = 0; y0 <= n; y0 += kRows7)
+      for (int z0 = 0; z0 <= n - y0; z0 += 2 * kPairs7)
+        for (int x0 = 0; x0 <= n - y0 - z0; x0 += kCols7) {
+          out.push_back(li);
+          out.push_back(z0);
+          out.push_back(y0);
+          out.push_back(x0);
+        }
+}
+
+template <bool kAsync>
+static void launch_p1_pipe(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                           int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
+  if (ntasks == 0) return;
+  if (n > 1022) fail_arg("p1 pipe kernel: level too large for 32-bit lattice offsets");
+  const std::size_t smem = 2 * static_cast<std::size_t>(kStage7) * sizeof(double);
+  static int grid_ctas = 0;
+  if (grid_ctas == 0) {
+    TETMF_CUDA(cudaFuncSetAttribute(p1_pipe_kernel<kAsync>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+    int dev = 0, sms = 0, per_sm = 0;
+    TETMF_CUDA(cudaGetDevice(&dev));
+    TETMF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    TETMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p1_pipe_kernel<kAsync>, 32 * kWarps7, smem));
+    grid_ctas = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const int grid = ntasks < grid_ctas ? ntasks : grid_ctas;
+  p1_pipe_kernel<kAsync><<<static_cast<unsigned>(grid), 32 * kWarps7, smem, s>>>(
+      x, y, reinterpret_cast<const Task5*>(d_tasks), ntasks, macro_stride, n, d_tables, d_macros);
+  check_launch("p1_pipe");
+  const int T = (n + 1) * (n + 2) / 2;
+  p1_face_kernel<<<dim3(static_cast<unsigned>((T + 255) / 256), static_cast<unsigned>(2 * nmacros)), 256, 0, s>>>(
+      x, y, macro_stride, n, d_tables, d_macros);
+  check_launch("p1_face");
+}
+
+void launch_p1_stencil7(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
+  launch_p1_pipe<false>(x, y, d_tasks, ntasks, macro_stride, n, nmacros, d_tables, d_macros, s);
+}
+
+void launch_p1_stencil8(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
+  launch_p1_pipe<true>(x, y, d_tasks, ntasks, macro_stride, n, nmacros, d_tables, d_macros, s);
+}
+
+void launch_p1_stencil5(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
+  if (ntasks == 0) return;
+  p1_interior_kernel<<<static_cast<unsigned>(ntasks), 32 * kWarps, 0, s>>>(
+      x, y, reinterpret_cast<const Task5*>(d_tasks), ntasks, macro_stride, n, d_tables, d_macros);
+  check_launch("p1_interior");
+  const int T = (n + 1) * (n + 2) / 2;
+  p1_face_kernel<<<dim3(static_cast<unsigned>((T + 255) / 256), static_cast<unsigned>(2 * nmacros)), 256, 0, s>>>(
+      x, y, macro_stride, n, d_tables, d_macros);
+  check_launch("p1_face");
+}
+
+} // namespace tetmf

@@ -142,6 +142,15 @@ Context::LevelData& Context::level(Space s, int level) {
     build_stencil_tma_tasks(static_cast<int>(macros_.size()), n, tasks);
     ld->ntasks3 = static_cast<int>(tasks.size() / 4);
     ld->tasks3.upload(tasks.data(), tasks.size(), stream_);
+    build_stencil7_tasks(static_cast<int>(macros_.size()), n, tasks);
+    ld->ntasks7 = static_cast<int>(tasks.size() / 4);
+    ld->tasks7.upload(tasks.data(), tasks.size(), stream_);
+    build_stencil6_tasks(static_cast<int>(macros_.size()), n, tasks);
+    ld->ntasks6 = static_cast<int>(tasks.size() / 4);
+    ld->tasks6.upload(tasks.data(), tasks.size(), stream_);
+    build_stencil5_tasks(static_cast<int>(macros_.size()), n, tasks);
+    ld->ntasks5 = static_cast<int>(tasks.size() / 4);
+    ld->tasks5.upload(tasks.data(), tasks.size(), stream_);
     build_stencil_tasks(static_cast<int>(macros_.size()), n, tasks);
     ld->ntasks2 = static_cast<int>(tasks.size() / 4);
     ld->tasks2.upload(tasks.data(), tasks.size(), stream_);
@@ -395,11 +404,26 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
       else if (kernel_variant_ == 3)
         launch_p1_stencil_tma(x, y, ld.tasks3.get(), ld.ntasks3, ld.lay.macro_stride, ld.lay.n, t.p1.get(),
                               ld.macros.get(), s);
+      else if (kernel_variant_ == 8)
+        launch_p1_stencil8(x, y, ld.tasks7.get(), ld.ntasks7, ld.lay.macro_stride, ld.lay.n, nm, t.p1.get(),
+                           ld.macros.get(), s);
+      else if (kernel_variant_ == 7)
+        launch_p1_stencil7(x, y, ld.tasks7.get(), ld.ntasks7, ld.lay.macro_stride, ld.lay.n, nm, t.p1.get(),
+                           ld.macros.get(), s);
+      else if (kernel_variant_ == 6)
+        launch_p1_stencil6(x, y, ld.tasks6.get(), ld.ntasks6, ld.lay.macro_stride, ld.lay.n, nm, t.p1.get(),
+                           ld.macros.get(), s);
+      else if (kernel_variant_ == 5)
+        launch_p1_stencil5(x, y, ld.tasks5.get(), ld.ntasks5, ld.lay.macro_stride, ld.lay.n, nm, t.p1.get(),
+                           ld.macros.get(), s);
       else if (kernel_variant_ == 4)
         launch_p1_stencil_tile(x, y, ld.tasks4.get(), ld.ntasks4, ld.lay.macro_stride, ld.lay.n, t.p1.get(),
                                ld.macros.get(), s);
-      else
+      else if (kernel_variant_ == 9)
         launch_p1_stencil2(x, y, ld.tasks.get(), ld.ntasks, ld.lay.macro_stride, ld.lay.n, t.p1.get(),
+                           ld.macros.get(), s);
+      else
+        launch_p1_stencil6(x, y, ld.tasks6.get(), ld.ntasks6, ld.lay.macro_stride, ld.lay.n, nm, t.p1.get(),
                            ld.macros.get(), s);
       break;
     case Form::P1KDiffusion:

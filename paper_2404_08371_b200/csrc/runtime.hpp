@@ -103,6 +103,12 @@ public:
     int ntasks2 = 0;
     DeviceBuffer<int> tasks3;           // P1: TMA plane-streaming tasks (variant 3)
     int ntasks3 = 0;
+    DeviceBuffer<int> tasks5;           // P1: interior row-walk CTA tasks (variant 5)
+    int ntasks5 = 0;
+    DeviceBuffer<int> tasks6;           // P1: shared-memory box tasks (variant 6)
+    int ntasks6 = 0;
+    DeviceBuffer<int> tasks7;           // P1: persistent double-buffered box tasks (variant 7)
+    int ntasks7 = 0;
     DeviceBuffer<int> tasks4;           // P1: register-tile tasks (variant 4)
     int ntasks4 = 0;
     DeviceBuffer<int> p1k_tasks;        // P1: row tasks of the P1K gather kernel (K2)
