@@ -259,10 +259,16 @@ p1_interior_kernel(const double* __restrict__ xin, double* __restrict__ yout, co
 #define TETMF_P1S_COLS 64
 #endif
 #ifndef TETMF_P1S_ROWS
-#define TETMF_P1S_ROWS 8   // measured best with 2 warps (cube6 L8 117.7 us; 4 rows x 4 warps 135 us)
+#define TETMF_P1S_ROWS 8   // cube6 L8: 8 rows x 4 warps 94 us, x 2 warps 118 us, 4 rows x 4 warps 108 us
 #endif
 #ifndef TETMF_P1S_WARPS
-#define TETMF_P1S_WARPS 2
+#define TETMF_P1S_WARPS 4
+#endif
+#ifndef TETMF_P1S_COPYONLY
+#define TETMF_P1S_COPYONLY 0
+#endif
+#ifndef TETMF_P1S_NOSTORE
+#define TETMF_P1S_NOSTORE 0
 #endif
 #ifndef TETMF_P1S_MINB
 #define TETMF_P1S_MINB 0
@@ -277,8 +283,23 @@ constexpr int kCopies6 = kPlanes6 * kRowsH6;
 constexpr int kPitch6 = kCols6 + 6;              // doubles per shared-memory row
 static_assert(kCols6 % 32 == 0 && kRows6 <= 16 && kCopies6 <= 32 * kWarps6, "p1 smem tiling");
 
+// 32-bit lattice offsets (a level's storage fits in int for n <= 1022)
+__device__ __forceinline__ int tet32(int k) {
+  return static_cast<int>(static_cast<unsigned>((k + 1) * (k + 2)) * static_cast<unsigned>(k + 3) / 6u);
+}
+__device__ __forceinline__ int rstart32(int n, int p, int y) {
+  return tet32(n) - tet32(n - p) + y * (n - p + 1) - y * (y - 1) / 2;
+}
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+// shared-memory load at byte address a + IMM (the immediate folds into the LDS)
+template <int IMM>
+__device__ __forceinline__ double lds_at(unsigned a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(IMM));
+  return v;
 }
 
 #if TETMF_P1S_MINB > 0
@@ -290,6 +311,10 @@ p1_smem_kernel(const double* __restrict__ xin, double* __restrict__ yout, const 
                int n, const P1DeviceTable* __restrict__ tabs, const MacroDesc* __restrict__ macros) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long bar;
+  // element index of column 0 in each box row: column x of box row j is
+  // sm[rowidx[j] + x] (row j holds global [base_j, base_j + kPitch6), base_j
+  // = (start_j + x0 - 2) & ~1, so x sits at j*kPitch6 + 2 + ((start_j + x0) & 1) + x - x0)
+  __shared__ unsigned rowaddr[kCopies6];
   const Task5 t = tasks[blockIdx.x];
   const int y0 = t.y0, z0 = t.z0, x0 = t.pad;
   const double* __restrict__ Xm = xin + static_cast<i64>(t.macro) * stride;
@@ -305,10 +330,11 @@ p1_smem_kernel(const double* __restrict__ xin, double* __restrict__ yout, const 
     const int p = min(max(z0 - 1 + pi, 0), n);  // missing planes alias the nearest (zero weights)
     const int y = y0 - 1 + ri;                  // -1 for the halo of block 0: the formula's finite neighbours
     const int m = n - p;
+    const int rs = rstart32(n, p, y);
+    const int base = (rs + x0 - 2) & ~1;
+    rowaddr[tid] = smem_u32(sm) + 8u * static_cast<unsigned>(tid * kPitch6 + 2 + ((rs + x0) & 1) - x0);
     unsigned bytes = 0;
     if (y <= m) {
-      const int rs = static_cast<int>(plane_offset(n, p)) + y * (m + 1) - y * (y - 1) / 2;
-      const int base = (rs + x0 - 2) & ~1;
       const int g0 = (rs + x0 - 1) & ~1;
       const int g1 = (rs + min(x0 + kCols6 + 1, m + 2 - y) + 1) & ~1;  // row end + 1 at most
       if (g1 > g0) {
@@ -324,93 +350,86 @@ p1_smem_kernel(const double* __restrict__ xin, double* __restrict__ yout, const 
     }
     if (bytes == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar)) : "memory");
   }
+  __syncthreads();  // rowaddr visible
   const int lane = tid & 31, wid = tid >> 5;
   const int z = z0 + 2 * wid;
   const bool work = z <= n - y0 && x0 <= n - y0 - z;  // the warp's planes hold points of the box
   const double* __restrict__ tab = &tabs[macros[t.macro].group].stencil[0][0];
-  if (work) {
-    // wait for the box (all copies landed)
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "W6_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0, %1;\n"
-        "@!p bra W6_%=;\n"
-        "}\n" ::"r"(smem_u32(&bar)),
-        "r"(0x989680u)
-        : "memory");
-    // planes L = z-1, A = z, B = z+1, U = z+2 at box plane indices 2w .. 2w+3
-    // (clamped at the lattice ends like the copies); global row starts and
-    // lengths as in the direct walk
-    const int pl = max(z - 1, 0), pa = z, pb = min(z + 1, n), pu = min(z + 2, n);
-    auto rstart = [&](int p, int y) { return static_cast<int>(plane_offset(n, p)) + y * (n - p + 1) - y * (y - 1) / 2; };
-    const int PL = 2 * wid, PA = PL + 1, PB = PL + 2, PU = PL + 3;
-    const bool zA = z >= 1;
+  if (!work) return;  // (warp 0 always works: it keeps the CTA alive until the copies land)
+  // wait for the box (all copies landed)
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "W6_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0, %1;\n"
+      "@!p bra W6_%=;\n"
+      "}\n" ::"r"(smem_u32(&bar)),
+      "r"(0x989680u)
+      : "memory");
+  if (TETMF_P1S_COPYONLY) return;  // A/B: the box copies alone
+  // planes L = z-1, A = z, B = z+1, U = z+2 = box planes 2w .. 2w+3
+  const unsigned* __restrict__ RL = rowaddr + (2 * wid) * kRowsH6;
+  const unsigned* __restrict__ RA = RL + kRowsH6;
+  const unsigned* __restrict__ RB = RA + kRowsH6;
+  const unsigned* __restrict__ RU = RB + kRowsH6;
+  const int la0 = n - z - y0 + 1;  // row y0 length, plane A
+  const int ystart = y0 == 0 ? 1 : 0;  // first stored row of the block (y = 0 is the face pass's)
 #pragma unroll 1
-    for (int sg = 0; sg < kSegs6; ++sg) {
-      const int px = x0 + 32 * sg + lane;
-      if (x0 + 32 * sg > n - y0 - z) break;  // segment past the row ends of both planes
-      double w[15];
-      {
-        const double* __restrict__ wt = tab + (px == 0 ? 16 : 0);
+  for (int sg = 0; sg < kSegs6; ++sg) {
+    const int px = x0 + 32 * sg + lane;
+    if (x0 + 32 * sg >= la0) break;  // segment past the row ends of both planes
+    double w[15];
+    {
+      const double* __restrict__ wt = tab + (px == 0 ? 16 : 0);
 #pragma unroll
-        for (int k = 0; k < 15; ++k) w[k] = __ldg(wt + k);
-      }
-      // global row starts at row y0 (A, B, L) / y0-1 (U's trailing row) and
-      // the shared-memory element index of column px in each row:
-      //   idx(pi, ri, g) = (pi*kRowsH6 + ri)*kPitch6 + 2 + ((g + x0) & 1) - x0 + px
-      // (base = (g + x0 - 2) & ~1, so g + px - base = px - x0 + 2 + ((g + x0) & 1))
-      auto idx = [&](int pi, int ri, int g) {
-        return (pi * kRowsH6 + ri) * kPitch6 + 2 + ((g + x0) & 1) - x0 + px;
-      };
-      int ga = rstart(pa, y0), gl = rstart(pl, y0), gb = rstart(pb, y0), gu = rstart(pu, y0);
-      int la = n - pa - y0 + 1, ll = n - pl - y0 + 1, lb = n - pb - y0 + 1, lu = n - pu - y0 + 1;
-      const int gam = ga - (la + 1), gbm = gb - (lb + 1), gum = gu - (lu + 1);
-      const int iam = idx(PA, 0, gam), ia0 = idx(PA, 1, ga), il0 = idx(PL, 1, gl);
-      const int ibm = idx(PB, 0, gbm), ib0 = idx(PB, 1, gb), ium = idx(PU, 0, gum);
-      double Am0 = sm[iam], Am1 = sm[iam + 1];
-      double A0m = sm[ia0 - 1], A00 = sm[ia0], A01 = sm[ia0 + 1];
-      double L00 = sm[il0], L01 = sm[il0 + 1];
-      double Bmm = sm[ibm - 1], Bm0 = sm[ibm], Bm1 = sm[ibm + 1];
-      double B0m = sm[ib0 - 1], B00 = sm[ib0], B01 = sm[ib0 + 1];
-      double Umm = sm[ium - 1], Um0 = sm[ium];
-      int yA = static_cast<int>(plane_offset(n, z)) + y0 * (n - z + 1) - y0 * (y0 - 1) / 2 + px;  // global y index, A
-      int yB = static_cast<int>(plane_offset(n, z + 1)) + y0 * (n - z) - y0 * (y0 - 1) / 2 + px;
-      const int s0 = px + y0 + z;
+      for (int k = 0; k < 15; ++k) w[k] = __ldg(wt + k);
+    }
+    // last stored row offsets: A stores rows r with s0 + r <= n-1 (z >= 1), B with s0 + r + 1 <= n-1
+    const int s0 = px + y0 + z;
+    const int rlastA = z >= 1 ? n - 1 - s0 : -1, rlastB = n - 2 - s0;
+    double* __restrict__ Ya = Ym + (rstart32(n, z, y0) + px);
+    double* __restrict__ Yb = Ym + (rstart32(n, min(z + 1, n), y0) + px);
+    int la = la0;
+    const unsigned bx = 8u * static_cast<unsigned>(px);  // byte offset of the lane's column
+    double Am0 = lds_at<0>(RA[0] + bx), Am1 = lds_at<8>(RA[0] + bx);
+    double A0m = lds_at<-8>(RA[1] + bx), A00 = lds_at<0>(RA[1] + bx), A01 = lds_at<8>(RA[1] + bx);
+    double L00 = lds_at<0>(RL[1] + bx), L01 = lds_at<8>(RL[1] + bx);
+    double Bmm = lds_at<-8>(RB[0] + bx), Bm0 = lds_at<0>(RB[0] + bx), Bm1 = lds_at<8>(RB[0] + bx);
+    double B0m = lds_at<-8>(RB[1] + bx), B00 = lds_at<0>(RB[1] + bx), B01 = lds_at<8>(RB[1] + bx);
+    double Umm = lds_at<-8>(RU[0] + bx), Um0 = lds_at<0>(RU[0] + bx);
 #pragma unroll
-      for (int r = 0; r < kRows6; ++r) {
-        const int yy = y0 + r;
-        const int gl1 = gl + ll, ga1 = ga + la, gb1 = gb + lb;
-        const int il = idx(PL, r + 2, gl1), ia = idx(PA, r + 2, ga1), ib = idx(PB, r + 2, gb1), iu = idx(PU, r + 1, gu);
-        const double Lp0 = sm[il], Lp1 = sm[il + 1];
-        const double Apm = sm[ia - 1], Ap0 = sm[ia], Ap1 = sm[ia + 1];
-        const double Bpm = sm[ib - 1], Bp0 = sm[ib], Bp1 = sm[ib + 1];
-        const double U0m = sm[iu - 1], U00 = sm[iu];
-        const double fa = sum15(w, A00, A01, A0m, Ap0, Am0, B00, L00, Am1, Apm, L01, B0m, Lp0, Bm0, Lp1, Bmm);
-        const double fb = sum15(w, B00, B01, B0m, Bp0, Bm0, U00, A00, Bm1, Bpm, A01, U0m, Ap0, Um0, Ap1, Umm);
-        if (yy >= 1 && zA && s0 + r <= n - 1) Ym[yA] = fa;
-        if (yy >= 1 && s0 + r + 1 <= n - 1) Ym[yB] = fb;
-        yA += n - z + 1 - yy;
-        yB += n - z - yy;
-        Am0 = A00; Am1 = A01;
-        A0m = Apm; A00 = Ap0; A01 = Ap1;
-        L00 = Lp0; L01 = Lp1;
-        Bmm = B0m; Bm0 = B00; Bm1 = B01;
-        B0m = Bpm; B00 = Bp0; B01 = Bp1;
-        Umm = U0m; Um0 = U00;
-        gu += lu;
-        gl = gl1; ga = ga1; gb = gb1;
-        --ll; --la; --lb; --lu;
-      }
+    for (int r = 0; r < kRows6; ++r) {
+      const unsigned il = RL[r + 2] + bx, ia = RA[r + 2] + bx, ib = RB[r + 2] + bx, iu = RU[r + 1] + bx;
+      const double Lp0 = lds_at<0>(il), Lp1 = lds_at<8>(il);
+      const double Apm = lds_at<-8>(ia), Ap0 = lds_at<0>(ia), Ap1 = lds_at<8>(ia);
+      const double Bpm = lds_at<-8>(ib), Bp0 = lds_at<0>(ib), Bp1 = lds_at<8>(ib);
+      const double U0m = lds_at<-8>(iu), U00 = lds_at<0>(iu);
+      const double fa = sum15(w, A00, A01, A0m, Ap0, Am0, B00, L00, Am1, Apm, L01, B0m, Lp0, Bm0, Lp1, Bmm);
+      const double fb = sum15(w, B00, B01, B0m, Bp0, Bm0, U00, A00, Bm1, Bpm, A01, U0m, Ap0, Um0, Ap1, Umm);
+#if TETMF_P1S_NOSTORE  // A/B: the loads and arithmetic without the stores
+      if (fa == 12345.678 && fb == 0.5) *Ya = fa;
+#else
+      if (r >= ystart && r <= rlastA) *Ya = fa;
+      if (r >= ystart && r <= rlastB) *Yb = fb;
+#endif
+      Ya += la;       // row y -> y+1: + row y length (plane A)
+      Yb += la - 1;   // plane B rows are one shorter
+      --la;
+      Am0 = A00; Am1 = A01;
+      A0m = Apm; A00 = Ap0; A01 = Ap1;
+      L00 = Lp0; L01 = Lp1;
+      Bmm = B0m; Bm0 = B00; Bm1 = B01;
+      B0m = Bpm; B00 = Bp0; B01 = Bp1;
+      Umm = U0m; Um0 = U00;
     }
-    // diagonal points of the box rows (as in the direct walk), by the CTA
-    // whose column range holds them
-    const int zz = z + (lane >> 4), yy = y0 + (lane & 15);
-    if ((lane & 15) < kRows6 && zz >= 1 && zz <= n && yy >= 1 && yy <= n - zz) {
-      const int xx = n - zz - yy;
-      if (xx >= x0 && xx < x0 + kCols6)
-        Ym[lattice_index(n, xx, yy, zz)] = gather_point(Xm, tab + 16 * (8 | (xx == 0 ? 1 : 0)), n, xx, yy, zz);
-    }
+  }
+  // diagonal points of the box rows (as in the direct walk), by the CTA
+  // whose column range holds them
+  const int zz = z + (lane >> 4), yy = y0 + (lane & 15);
+  if ((lane & 15) < kRows6 && zz >= 1 && zz <= n && yy >= 1 && yy <= n - zz) {
+    const int xx = n - zz - yy;
+    if (xx >= x0 && xx < x0 + kCols6)
+      Ym[lattice_index(n, xx, yy, zz)] = gather_point(Xm, tab + 16 * (8 | (xx == 0 ? 1 : 0)), n, xx, yy, zz);
   }
 }
 
@@ -449,13 +468,6 @@ constexpr int kPitch7 = kCols7 + 6;
 constexpr int kStage7 = kCopies7 * kPitch7;  // doubles per stage
 static_assert(kCols7 % 32 == 0 && kRows7 <= 16 && kCopies7 <= 32 * kWarps7, "p1 pipe tiling");
 
-// 32-bit lattice offsets (a level's storage fits in int for n <= 1022)
-__device__ __forceinline__ int tet32(int k) {
-  return static_cast<int>(static_cast<unsigned>((k + 1) * (k + 2)) * static_cast<unsigned>(k + 3) / 6u);
-}
-__device__ __forceinline__ int rstart32(int n, int p, int y) {
-  return tet32(n) - tet32(n - p) + y * (n - p + 1) - y * (y - 1) / 2;
-}
 
 __device__ __forceinline__ void mbar_wait_parity(unsigned long long* bar, unsigned parity) {
   asm volatile(
@@ -702,6 +714,7 @@ void build_stencil6_tasks(int nmacros, int n, std::vector<int>& out) {
 void launch_p1_stencil6(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
                         int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
   if (ntasks == 0) return;
+  if (n > 1022) fail_arg("p1 box kernel: level too large for 32-bit lattice offsets");
   const std::size_t smem = static_cast<std::size_t>(kCopies6) * kPitch6 * sizeof(double);
   static bool configured = false;
   if (!configured) {
