@@ -80,7 +80,7 @@ void gradient_transpose(const Function& nd1, Function& p1, int level) {
   double* y = p1.data(level);
   launch_gradient_t(nd1.data(level), y, static_cast<int>(le.lay.macros.size()), le.lay.macro_stride,
                     le.lay.class_stride, lp.lay.macro_stride, le.lay.n, le.slot_table.get(), ctx.stream());
-  launch_interface_sum(y, lp.group_offsets.get(), lp.group_copies.get(), lp.groups.num_groups(), ctx.stream());
+  lp.interface_sum(y, ctx.stream());
   if (lp.exchange) lp.exchange->run(y, ctx.stream());
 }
 

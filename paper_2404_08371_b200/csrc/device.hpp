@@ -43,6 +43,10 @@ void launch_import_ref(double* lat, const i64* map, i64 total, const double* ref
 void launch_export_ref(const double* lat, const i64* map, i64 total, double* ref, cudaStream_t s);
 void launch_interface_sum(double* y, const i64* offsets, const i64* copies, i64 ngroups, cudaStream_t s,
                           bool signed_values = true);
+// K4 with two-copy groups packed as 32-bit pairs (one thread per pair) and
+// the remaining groups in CSR form, one launch; same sums as interface_sum
+void launch_interface_sum_packed(double* y, const unsigned* pairs, i64 npairs, const i64* offsets, const i64* copies,
+                                 i64 nrest, cudaStream_t s, bool signed_values = true);
 void launch_axpy(double* y, const double* x, double a, i64 count, cudaStream_t s);
 
 void launch_p1_stencil(const double* x, double* y, const MacroDesc* d_macros, int nmacros, i64 macro_stride,

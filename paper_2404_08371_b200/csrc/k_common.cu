@@ -213,6 +213,37 @@ __global__ void interface_sum_kernel(double* y, const i64* offsets, const i64* c
   }
 }
 
+template <bool SIGNED>
+__global__ void interface_sum_packed_kernel(double* y, const uint2* __restrict__ pairs, i64 npairs,
+                                            const i64* __restrict__ offsets, const i64* __restrict__ copies,
+                                            i64 nrest) {
+  const i64 g = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (g < npairs) {
+    // the CSR kernel's order: s = 0; s += copy 0; s += copy 1
+    const uint2 p = pairs[g];
+    const double va = y[p.x >> 1], vb = y[p.y >> 1];
+    double s = 0.0;
+    s += (SIGNED && (p.x & 1u)) ? -va : va;
+    s += (SIGNED && (p.y & 1u)) ? -vb : vb;
+    y[p.x >> 1] = (SIGNED && (p.x & 1u)) ? -s : s;
+    y[p.y >> 1] = (SIGNED && (p.y & 1u)) ? -s : s;
+    return;
+  }
+  const i64 r = g - npairs;
+  if (r >= nrest) return;
+  const i64 b = offsets[r], e = offsets[r + 1];
+  double s = 0.0;
+  for (i64 k = b; k < e; ++k) {
+    const i64 c = copies[k];
+    const double v = y[c >> 1];
+    s += (SIGNED && (c & 1)) ? -v : v;
+  }
+  for (i64 k = b; k < e; ++k) {
+    const i64 c = copies[k];
+    y[c >> 1] = (SIGNED && (c & 1)) ? -s : s;
+  }
+}
+
 __global__ void axpy_kernel(double* y, const double* x, double a, i64 count) {
   const i64 tid = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
   if (tid < count) y[tid] += a * x[tid];
@@ -286,6 +317,18 @@ void launch_interface_sum(double* y, const i64* offsets, const i64* copies, i64 
   else
     interface_sum_kernel<false><<<grid_for(ngroups), kThreads, 0, s>>>(y, offsets, copies, ngroups);
   check_launch("interface_sum");
+}
+
+void launch_interface_sum_packed(double* y, const unsigned* pairs, i64 npairs, const i64* offsets, const i64* copies,
+                                 i64 nrest, cudaStream_t s, bool signed_values) {
+  const i64 total = npairs + nrest;
+  if (total <= 0) return;
+  const uint2* p = reinterpret_cast<const uint2*>(pairs);
+  if (signed_values)
+    interface_sum_packed_kernel<true><<<grid_for(total), kThreads, 0, s>>>(y, p, npairs, offsets, copies, nrest);
+  else
+    interface_sum_packed_kernel<false><<<grid_for(total), kThreads, 0, s>>>(y, p, npairs, offsets, copies, nrest);
+  check_launch("interface_sum_packed");
 }
 
 void launch_axpy(double* y, const double* x, double a, i64 count, cudaStream_t s) {

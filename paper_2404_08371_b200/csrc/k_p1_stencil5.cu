@@ -116,6 +116,26 @@ __device__ __forceinline__ double gather_point(const double* __restrict__ X, con
   return sum15(w, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9], v[10], v[11], v[12], v[13], v[14]);
 }
 
+// Point q of face f (0: z = 0, 1: y = 0, the z = 0 edge excluded) of macro
+// li: the triangle a + b <= n enumerated b-major (row b starts at
+// S(b) = b(2n+3-b)/2); x = a, and y (f = 0) or z (f = 1) = b.
+__device__ __forceinline__ void face_point(const double* __restrict__ xin, double* __restrict__ yout, i64 stride,
+                                           int n, const P1DeviceTable* __restrict__ tabs,
+                                           const MacroDesc* __restrict__ macros, int li, int f, int q) {
+  const float c = 2.0f * n + 3.0f;
+  int b = static_cast<int>((c - sqrtf(fmaxf(c * c - 8.0f * q, 0.0f))) * 0.5f);
+  b = min(max(b, 0), n);
+  while (b > 0 && b * (2 * n + 3 - b) / 2 > q) --b;
+  while (b < n && (b + 1) * (2 * n + 2 - b) / 2 <= q) ++b;
+  const int a = q - b * (2 * n + 3 - b) / 2;
+  const int x = a, y = f == 0 ? b : 0, z = f == 0 ? 0 : b;
+  if (f == 1 && z == 0) return;  // on the z = 0 face
+  const int type = (x == 0 ? 1 : 0) | (y == 0 ? 2 : 0) | (z == 0 ? 4 : 0) | (x + y + z == n ? 8 : 0);
+  const double* __restrict__ X = xin + static_cast<i64>(li) * stride;
+  const double* __restrict__ wt = &tabs[macros[li].group].stencil[type][0];
+  yout[static_cast<i64>(li) * stride + lattice_index(n, x, y, z)] = gather_point(X, wt, n, x, y, z);
+}
+
 #if TETMF_P1F_MINB > 0
 __global__ void __launch_bounds__(32 * kWarps, TETMF_P1F_MINB)
 #else
@@ -307,8 +327,19 @@ __global__ void __launch_bounds__(32 * kWarps6, TETMF_P1S_MINB)
 #else
 __global__ void __launch_bounds__(32 * kWarps6)
 #endif
-p1_smem_kernel(const double* __restrict__ xin, double* __restrict__ yout, const Task5* __restrict__ tasks, i64 stride,
-               int n, const P1DeviceTable* __restrict__ tabs, const MacroDesc* __restrict__ macros) {
+p1_smem_kernel(const double* __restrict__ xin, double* __restrict__ yout, const Task5* __restrict__ tasks, int ntasks,
+               int nmacros, i64 stride, int n, const P1DeviceTable* __restrict__ tabs,
+               const MacroDesc* __restrict__ macros) {
+  if (static_cast<int>(blockIdx.x) >= ntasks) {
+    // face CTAs after the boxes (same launch, they fill the tail): faces z = 0
+    // and y = 0 of every macro, one point per thread
+    const int T = (n + 1) * (n + 2) / 2;
+    const int gid = (static_cast<int>(blockIdx.x) - ntasks) * static_cast<int>(blockDim.x) + static_cast<int>(threadIdx.x);
+    const int li = gid / (2 * T), rem = gid - li * 2 * T;
+    if (li < nmacros)
+      face_point(xin, yout, stride, n, tabs, macros, li, rem >= T ? 1 : 0, rem >= T ? rem - T : rem);
+    return;
+  }
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long bar;
   // element index of column 0 in each box row: column x of box row j is
@@ -331,21 +362,45 @@ p1_smem_kernel(const double* __restrict__ xin, double* __restrict__ yout, const 
     const int y = y0 - 1 + ri;                  // -1 for the halo of block 0: the formula's finite neighbours
     const int m = n - p;
     const int rs = rstart32(n, p, y);
-    const int base = (rs + x0 - 2) & ~1;
-    rowaddr[tid] = smem_u32(sm) + 8u * static_cast<unsigned>(tid * kPitch6 + 2 + ((rs + x0) & 1) - x0);
+    // Slab mode: when the box starts at x0 = 0 and the plane's box rows
+    // (y0-1 .. yb) are short, their whole contiguous stretch [start(y0-1) - 1,
+    // start(yb+1) + 1) fits the plane's shared-memory region and is ONE copy
+    // (issued by the plane's row-0 thread); rows then sit at their natural
+    // offsets inside the stretch. Otherwise one copy per row, as below.
+    const int yb = min(y0 + kRows6, m);
+    const int rsa = rstart32(n, p, y0 - 1), rse = rstart32(n, p, yb + 1);
+    const int sbase = (rsa - 1) & ~1;
+    const int send = (rse + 2) & ~1;
+    const bool slab = x0 == 0 && y0 - 1 <= m && send - sbase <= kRowsH6 * kPitch6;
     unsigned bytes = 0;
-    if (y <= m) {
-      const int g0 = (rs + x0 - 1) & ~1;
-      const int g1 = (rs + min(x0 + kCols6 + 1, m + 2 - y) + 1) & ~1;  // row end + 1 at most
-      if (g1 > g0) {
-        bytes = static_cast<unsigned>(g1 - g0) * 8u;
+    if (slab) {
+      const unsigned reg = smem_u32(sm + pi * kRowsH6 * kPitch6);
+      rowaddr[tid] = reg + 8u * static_cast<unsigned>(y <= yb + 1 ? rs - sbase : 0);
+      if (ri == 0) {
+        bytes = static_cast<unsigned>(send - sbase) * 8u;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(bytes)
                      : "memory");
         asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(sm + tid * kPitch6 + (g0 - base))),
-            "l"(Xm + g0), "r"(bytes), "r"(smem_u32(&bar))
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(reg),
+            "l"(Xm + sbase), "r"(bytes), "r"(smem_u32(&bar))
             : "memory");
+      }
+    } else {
+      const int base = (rs + x0 - 2) & ~1;
+      rowaddr[tid] = smem_u32(sm) + 8u * static_cast<unsigned>(tid * kPitch6 + 2 + ((rs + x0) & 1) - x0);
+      if (y <= m) {
+        const int g0 = (rs + x0 - 1) & ~1;
+        const int g1 = (rs + min(x0 + kCols6 + 1, m + 2 - y) + 1) & ~1;  // row end + 1 at most
+        if (g1 > g0) {
+          bytes = static_cast<unsigned>(g1 - g0) * 8u;
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(bytes)
+                       : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(sm + tid * kPitch6 + (g0 - base))),
+              "l"(Xm + g0), "r"(bytes), "r"(smem_u32(&bar))
+              : "memory");
+        }
       }
     }
     if (bytes == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar)) : "memory");
@@ -356,6 +411,10 @@ p1_smem_kernel(const double* __restrict__ xin, double* __restrict__ yout, const 
   const bool work = z <= n - y0 && x0 <= n - y0 - z;  // the warp's planes hold points of the box
   const double* __restrict__ tab = &tabs[macros[t.macro].group].stencil[0][0];
   if (!work) return;  // (warp 0 always works: it keeps the CTA alive until the copies land)
+  // interior weights, loaded while the copies land
+  double w[15];
+#pragma unroll
+  for (int k = 0; k < 15; ++k) w[k] = __ldg(tab + k);
   // wait for the box (all copies landed)
   asm volatile(
       "{\n"
@@ -378,8 +437,9 @@ p1_smem_kernel(const double* __restrict__ xin, double* __restrict__ yout, const 
   for (int sg = 0; sg < kSegs6; ++sg) {
     const int px = x0 + 32 * sg + lane;
     if (x0 + 32 * sg >= la0) break;  // segment past the row ends of both planes
-    double w[15];
-    {
+    if (x0 + 32 * sg <= 32) {
+      // the lane at x = 0 (segment 0 of an x0 = 0 box) walks with the x = 0
+      // face variant (type 1); the next segment's lane 0 is interior again
       const double* __restrict__ wt = tab + (px == 0 ? 16 : 0);
 #pragma unroll
       for (int k = 0; k < 15; ++k) w[k] = __ldg(wt + k);
@@ -665,20 +725,7 @@ __global__ void __launch_bounds__(256) p1_face_kernel(const double* __restrict__
   const int T = (n + 1) * (n + 2) / 2;
   const int q = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x);
   if (q >= T) return;
-  const int li = static_cast<int>(blockIdx.y >> 1), f = static_cast<int>(blockIdx.y & 1);
-  // (a, b) with a + b <= n, b-major: row b starts at S(b) = b(2n+3-b)/2
-  const float c = 2.0f * n + 3.0f;
-  int b = static_cast<int>((c - sqrtf(fmaxf(c * c - 8.0f * q, 0.0f))) * 0.5f);
-  b = min(max(b, 0), n);
-  while (b > 0 && b * (2 * n + 3 - b) / 2 > q) --b;
-  while (b < n && (b + 1) * (2 * n + 2 - b) / 2 <= q) ++b;
-  const int a = q - b * (2 * n + 3 - b) / 2;
-  const int x = a, y = f == 0 ? b : 0, z = f == 0 ? 0 : b;
-  if (f == 1 && z == 0) return;  // on the z = 0 face
-  const int type = (x == 0 ? 1 : 0) | (y == 0 ? 2 : 0) | (z == 0 ? 4 : 0) | (x + y + z == n ? 8 : 0);
-  const double* __restrict__ X = xin + static_cast<i64>(li) * stride;
-  const double* __restrict__ wt = &tabs[macros[li].group].stencil[type][0];
-  yout[static_cast<i64>(li) * stride + lattice_index(n, x, y, z)] = gather_point(X, wt, n, x, y, z);
+  face_point(xin, yout, stride, n, tabs, macros, static_cast<int>(blockIdx.y >> 1), static_cast<int>(blockIdx.y & 1), q);
 }
 
 } // namespace
@@ -715,19 +762,20 @@ void launch_p1_stencil6(const double* x, double* y, const int* d_tasks, int ntas
                         int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
   if (ntasks == 0) return;
   if (n > 1022) fail_arg("p1 box kernel: level too large for 32-bit lattice offsets");
-  const std::size_t smem = static_cast<std::size_t>(kCopies6) * kPitch6 * sizeof(double);
+  // + a margin: in slab mode lanes past the short rows read up to a segment
+  // beyond the last plane's stretch (never stored)
+  const std::size_t smem = (static_cast<std::size_t>(kCopies6) * kPitch6 + 96) * sizeof(double);
   static bool configured = false;
   if (!configured) {
     TETMF_CUDA(cudaFuncSetAttribute(p1_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     configured = true;
   }
-  p1_smem_kernel<<<static_cast<unsigned>(ntasks), 32 * kWarps6, smem, s>>>(
-      x, y, reinterpret_cast<const Task5*>(d_tasks), macro_stride, n, d_tables, d_macros);
-  check_launch("p1_smem");
+  // boxes, then the face CTAs (faces z = 0 and y = 0) in the same launch
   const int T = (n + 1) * (n + 2) / 2;
-  p1_face_kernel<<<dim3(static_cast<unsigned>((T + 255) / 256), static_cast<unsigned>(2 * nmacros)), 256, 0, s>>>(
-      x, y, macro_stride, n, d_tables, d_macros);
-  check_launch("p1_face");
+  const int face_ctas = (2 * T * nmacros + 32 * kWarps6 - 1) / (32 * kWarps6);
+  p1_smem_kernel<<<static_cast<unsigned>(ntasks + face_ctas), 32 * kWarps6, smem, s>>>(
+      x, y, reinterpret_cast<const Task5*>(d_tasks), ntasks, nmacros, macro_stride, n, d_tables, d_macros);
+  check_launch("p1_smem");
 }
 
 // CTA boxes of variant 7 (macro, z0, y0, x0)

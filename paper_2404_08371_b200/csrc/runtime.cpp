@@ -42,6 +42,7 @@ void DeviceBuffer<T>::upload(const T* host, std::size_t count, cudaStream_t s) {
 }
 template class DeviceBuffer<double>;
 template class DeviceBuffer<i64>;
+template class DeviceBuffer<unsigned>;
 template class DeviceBuffer<MacroDesc>;
 template class DeviceBuffer<P1DeviceTable>;
 template class DeviceBuffer<N1DeviceTable>;
@@ -209,6 +210,27 @@ Context::LevelData& Context::level(Space s, int level) {
   ld->groups = local_groups_only(mesh_, topo_, ld->lay, rank_of, rank_);
   ld->group_offsets.upload(ld->groups.offsets.data(), ld->groups.offsets.size(), stream_);
   ld->group_copies.upload(ld->groups.copies.data(), ld->groups.copies.size(), stream_);
+  if (ld->lay.total() < (i64(1) << 31)) {
+    std::vector<unsigned> pairs;
+    std::vector<i64> ro{0}, rc;
+    const auto& G = ld->groups;
+    for (i64 g = 0; g < G.num_groups(); ++g) {
+      const i64 b = G.offsets[g], e = G.offsets[g + 1];
+      if (e - b == 2) {
+        pairs.push_back(static_cast<unsigned>(G.copies[b]));
+        pairs.push_back(static_cast<unsigned>(G.copies[b + 1]));
+      } else {
+        rc.insert(rc.end(), G.copies.begin() + b, G.copies.begin() + e);
+        ro.push_back(static_cast<i64>(rc.size()));
+      }
+    }
+    ld->npairs = static_cast<i64>(pairs.size() / 2);
+    ld->nrest = static_cast<i64>(ro.size()) - 1;
+    ld->group_pairs.upload(pairs.data(), pairs.size(), stream_);
+    ld->rest_offsets.upload(ro.data(), ro.size(), stream_);
+    ld->rest_copies.upload(rc.data(), rc.size(), stream_);
+    ld->packed = true;
+  }
   if (nranks_ > 1)
     ld->exchange = std::make_unique<Exchange>(build_exchange_plan(mesh_, topo_, ld->lay, rank_of, rank_),
                                               comm_backend_.get());
@@ -232,6 +254,14 @@ Context::LevelData& Context::ref_level(Space s, int level) {
 // their register windows without bounds predicates (out-of-lattice values
 // only ever meet zero weights), so the windows may touch up to one row plus
 // one warp width outside the storage.
+void Context::LevelData::interface_sum(double* y, cudaStream_t s, bool signed_values) const {
+  if (packed)
+    launch_interface_sum_packed(y, group_pairs.get(), npairs, rest_offsets.get(), rest_copies.get(), nrest, s,
+                                signed_values);
+  else
+    launch_interface_sum(y, group_offsets.get(), group_copies.get(), groups.num_groups(), s, signed_values);
+}
+
 i64 storage_guard(int n) { return round_up(static_cast<i64>(n) + 96, 32); }
 
 double* Function::data(int level) {
@@ -468,7 +498,7 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
       fail_internal("kernel_apply: unsupported form");
   }
   if (ev_stop) TETMF_CUDA(cudaEventRecord(ev_stop, s));
-  launch_interface_sum(y, ld.group_offsets.get(), ld.group_copies.get(), ld.groups.num_groups(), s);
+  ld.interface_sum(y, s);
   if (ld.exchange) ld.exchange->run(y, s);
 }
 
@@ -519,7 +549,7 @@ void Operator::diagonal(Function& d, int level) {
         fail_arg("diagonal: not available for this form");
     }
   }
-  launch_interface_sum(y, ld.group_offsets.get(), ld.group_copies.get(), ld.groups.num_groups(), s, false);
+  ld.interface_sum(y, s, false);
   if (ld.exchange) ld.exchange->run(y, s, false);
 }
 

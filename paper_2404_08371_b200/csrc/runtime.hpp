@@ -94,6 +94,14 @@ public:
     DeviceBuffer<MacroDesc> macros;
     InterfaceGroups groups;
     DeviceBuffer<i64> group_offsets, group_copies;
+    // K4 fast path: two-copy groups as packed 32-bit (index << 1 | sign)
+    // pairs; the groups with more copies keep the CSR form (rest_*). Used
+    // when the level's storage has < 2^31 entries, else the full CSR.
+    DeviceBuffer<unsigned> group_pairs;
+    DeviceBuffer<i64> rest_offsets, rest_copies;
+    i64 npairs = 0, nrest = 0;
+    bool packed = false;
+    void interface_sum(double* y, cudaStream_t s, bool signed_values = true) const;
     std::unique_ptr<RefNumbering> ref;  // lazily, import/export only
     DeviceBuffer<i64> ref_map;
     std::unique_ptr<Exchange> exchange; // nranks > 1
