@@ -392,7 +392,7 @@ int tetmf_op_profile(tetmf_op* op, int enable) {
 int tetmf_op_set_variant(tetmf_op* op, int variant) {
   return guard([&] {
     need(op, "op");
-    if (variant < 0 || variant > 9) fail_arg("unknown kernel variant");
+    if (variant < 0 || variant > 10) fail_arg("unknown kernel variant");
     op->impl->set_kernel_variant(variant);
   });
 }

@@ -322,41 +322,25 @@ __device__ __forceinline__ double lds_at(unsigned a) {
   return v;
 }
 
-#if TETMF_P1S_MINB > 0
-__global__ void __launch_bounds__(32 * kWarps6, TETMF_P1S_MINB)
-#else
-__global__ void __launch_bounds__(32 * kWarps6)
-#endif
-p1_smem_kernel(const double* __restrict__ xin, double* __restrict__ yout, const Task5* __restrict__ tasks, int ntasks,
-               int nmacros, i64 stride, int n, const P1DeviceTable* __restrict__ tabs,
-               const MacroDesc* __restrict__ macros) {
-  if (static_cast<int>(blockIdx.x) >= ntasks) {
-    // face CTAs after the boxes (same launch, they fill the tail): faces z = 0
-    // and y = 0 of every macro, one point per thread
-    const int T = (n + 1) * (n + 2) / 2;
-    const int gid = (static_cast<int>(blockIdx.x) - ntasks) * static_cast<int>(blockDim.x) + static_cast<int>(threadIdx.x);
-    const int li = gid / (2 * T), rem = gid - li * 2 * T;
-    if (li < nmacros)
-      face_point(xin, yout, stride, n, tabs, macros, li, rem >= T ? 1 : 0, rem >= T ? rem - T : rem);
-    return;
-  }
-  extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) unsigned long long bar;
-  // element index of column 0 in each box row: column x of box row j is
-  // sm[rowidx[j] + x] (row j holds global [base_j, base_j + kPitch6), base_j
-  // = (start_j + x0 - 2) & ~1, so x sits at j*kPitch6 + 2 + ((start_j + x0) & 1) + x - x0)
-  __shared__ unsigned rowaddr[kCopies6];
-  const Task5 t = tasks[blockIdx.x];
-  const int y0 = t.y0, z0 = t.z0, x0 = t.pad;
-  const double* __restrict__ Xm = xin + static_cast<i64>(t.macro) * stride;
-  double* __restrict__ Ym = yout + static_cast<i64>(t.macro) * stride;
-  const int tid = static_cast<int>(threadIdx.x);
-  if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "r"(kCopies6));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid < kCopies6) {
+__device__ __forceinline__ void mbar_wait_parity(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "W7_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra W7_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+
+// Box copies (thread tid < kCopies6 of the CTA): box u into stage S (row
+// address table rowtab), completing on barp.
+__device__ __forceinline__ void box_issue6(const Task5& u, int tid, double* S, unsigned* rowtab,
+                                           unsigned long long* barp, const double* __restrict__ xin, i64 stride,
+                                           int n) {
+  const int y0 = u.y0, z0 = u.z0, x0 = u.pad;
+  const double* __restrict__ Xm = xin + static_cast<i64>(u.macro) * stride;
     const int pi = tid / kRowsH6, ri = tid - pi * kRowsH6;
     const int p = min(max(z0 - 1 + pi, 0), n);  // missing planes alias the nearest (zero weights)
     const int y = y0 - 1 + ri;                  // -1 for the halo of block 0: the formula's finite neighbours
@@ -374,60 +358,50 @@ p1_smem_kernel(const double* __restrict__ xin, double* __restrict__ yout, const 
     const bool slab = x0 == 0 && y0 - 1 <= m && send - sbase <= kRowsH6 * kPitch6;
     unsigned bytes = 0;
     if (slab) {
-      const unsigned reg = smem_u32(sm + pi * kRowsH6 * kPitch6);
-      rowaddr[tid] = reg + 8u * static_cast<unsigned>(y <= yb + 1 ? rs - sbase : 0);
+      const unsigned reg = smem_u32(S + pi * kRowsH6 * kPitch6);
+      rowtab[tid] = reg + 8u * static_cast<unsigned>(y <= yb + 1 ? rs - sbase : 0);
       if (ri == 0) {
         bytes = static_cast<unsigned>(send - sbase) * 8u;
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(bytes)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(barp)), "r"(bytes)
                      : "memory");
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(reg),
-            "l"(Xm + sbase), "r"(bytes), "r"(smem_u32(&bar))
+            "l"(Xm + sbase), "r"(bytes), "r"(smem_u32(barp))
             : "memory");
       }
     } else {
       const int base = (rs + x0 - 2) & ~1;
-      rowaddr[tid] = smem_u32(sm) + 8u * static_cast<unsigned>(tid * kPitch6 + 2 + ((rs + x0) & 1) - x0);
+      rowtab[tid] = smem_u32(S) + 8u * static_cast<unsigned>(tid * kPitch6 + 2 + ((rs + x0) & 1) - x0);
       if (y <= m) {
         const int g0 = (rs + x0 - 1) & ~1;
         const int g1 = (rs + min(x0 + kCols6 + 1, m + 2 - y) + 1) & ~1;  // row end + 1 at most
         if (g1 > g0) {
           bytes = static_cast<unsigned>(g1 - g0) * 8u;
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(bytes)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(barp)), "r"(bytes)
                        : "memory");
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  smem_u32(sm + tid * kPitch6 + (g0 - base))),
-              "l"(Xm + g0), "r"(bytes), "r"(smem_u32(&bar))
+                  smem_u32(S + tid * kPitch6 + (g0 - base))),
+              "l"(Xm + g0), "r"(bytes), "r"(smem_u32(barp))
               : "memory");
         }
       }
     }
-    if (bytes == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar)) : "memory");
-  }
-  __syncthreads();  // rowaddr visible
-  const int lane = tid & 31, wid = tid >> 5;
-  const int z = z0 + 2 * wid;
-  const bool work = z <= n - y0 && x0 <= n - y0 - z;  // the warp's planes hold points of the box
-  const double* __restrict__ tab = &tabs[macros[t.macro].group].stencil[0][0];
-  if (!work) return;  // (warp 0 always works: it keeps the CTA alive until the copies land)
-  // interior weights, loaded while the copies land
-  double w[15];
-#pragma unroll
-  for (int k = 0; k < 15; ++k) w[k] = __ldg(tab + k);
-  // wait for the box (all copies landed)
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "W6_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0, %1;\n"
-      "@!p bra W6_%=;\n"
-      "}\n" ::"r"(smem_u32(&bar)),
-      "r"(0x989680u)
-      : "memory");
-  if (TETMF_P1S_COPYONLY) return;  // A/B: the box copies alone
+    if (bytes == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(barp)) : "memory");
+}
+
+// The warp's walk of box t (plane pair z = z0 + 2*wid) out of the stage whose
+// row address table is rowtab; w holds the interior weights on entry.
+__device__ __forceinline__ void box_walk6(const Task5& t, const unsigned* __restrict__ rowtab, double (&w)[15],
+                                          int wid, int lane, const double* __restrict__ xin,
+                                          double* __restrict__ yout, i64 stride, int n,
+                                          const double* __restrict__ tab) {
+  const int y0 = t.y0, x0 = t.pad;
+  const int z = t.z0 + 2 * wid;
+  const double* __restrict__ Xm = xin + static_cast<i64>(t.macro) * stride;
+  double* __restrict__ Ym = yout + static_cast<i64>(t.macro) * stride;
   // planes L = z-1, A = z, B = z+1, U = z+2 = box planes 2w .. 2w+3
-  const unsigned* __restrict__ RL = rowaddr + (2 * wid) * kRowsH6;
+  const unsigned* __restrict__ RL = rowtab + (2 * wid) * kRowsH6;
   const unsigned* __restrict__ RA = RL + kRowsH6;
   const unsigned* __restrict__ RB = RA + kRowsH6;
   const unsigned* __restrict__ RU = RB + kRowsH6;
@@ -493,6 +467,88 @@ p1_smem_kernel(const double* __restrict__ xin, double* __restrict__ yout, const 
   }
 }
 
+// kPersistent = false (variant 6, the default): one box per CTA, copy -> wait
+// -> walk; several CTAs per SM overlap. kPersistent = true (variant 10): a
+// persistent CTA double-buffers two boxes (full / empty mbarrier per stage):
+// the copies of box k+1 land while the warps walk box k. Face CTAs (faces
+// z = 0, y = 0) follow the boxes in the same launch.
+template <bool kPersistent>
+#if TETMF_P1S_MINB > 0
+__global__ void __launch_bounds__(32 * kWarps6, TETMF_P1S_MINB)
+#else
+__global__ void __launch_bounds__(32 * kWarps6)
+#endif
+p1_box_kernel(const double* __restrict__ xin, double* __restrict__ yout, const Task5* __restrict__ tasks, int ntasks,
+              int nboxctas, int nmacros, i64 stride, int n, const P1DeviceTable* __restrict__ tabs,
+              const MacroDesc* __restrict__ macros) {
+  if (static_cast<int>(blockIdx.x) >= nboxctas) {
+    // face CTAs after the boxes (same launch, they fill the tail): faces z = 0
+    // and y = 0 of every macro, one point per thread
+    const int T = (n + 1) * (n + 2) / 2;
+    const int gid = (static_cast<int>(blockIdx.x) - nboxctas) * static_cast<int>(blockDim.x) + static_cast<int>(threadIdx.x);
+    const int li = gid / (2 * T), rem = gid - li * 2 * T;
+    if (li < nmacros)
+      face_point(xin, yout, stride, n, tabs, macros, li, rem >= T ? 1 : 0, rem >= T ? rem - T : rem);
+    return;
+  }
+  extern __shared__ __align__(128) double sm[];
+  // row address tables: column x of box row j is at shared byte address
+  // rowaddr[stage][j] + 8x (per-row copies: row j holds global [base_j,
+  // base_j + kPitch6), base_j = (start_j + x0 - 2) & ~1; slab mode: the
+  // plane's rows at their natural offsets in one stretch)
+  __shared__ unsigned rowaddr[kPersistent ? 2 : 1][kCopies6];
+  __shared__ __align__(8) unsigned long long full[2], empty[2];
+  const int tid = static_cast<int>(threadIdx.x), lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) {
+    for (int i = 0; i < (kPersistent ? 2 : 1); ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[i])), "r"(kCopies6));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[i])), "r"(kWarps6));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  constexpr int kStage6 = kCopies6 * kPitch6 + 96;  // doubles per stage (+ slab-mode overread margin)
+  if (!kPersistent) {
+    const Task5 t = tasks[blockIdx.x];
+    if (tid < kCopies6) box_issue6(t, tid, sm, rowaddr[0], &full[0], xin, stride, n);
+    __syncthreads();  // rowaddr visible
+    const int z = t.z0 + 2 * wid;
+    if (!(z <= n - t.y0 && t.pad <= n - t.y0 - z)) return;  // (warp 0 always works: it keeps the CTA alive)
+    const double* __restrict__ tab = &tabs[macros[t.macro].group].stencil[0][0];
+    double w[15];  // interior weights, loaded while the copies land
+#pragma unroll
+    for (int k = 0; k < 15; ++k) w[k] = __ldg(tab + k);
+    mbar_wait_parity(&full[0], 0u);
+    if (TETMF_P1S_COPYONLY) return;  // A/B: the box copies alone
+    box_walk6(t, rowaddr[0], w, wid, lane, xin, yout, stride, n, tab);
+    return;
+  }
+  const int G = nboxctas;
+  if (tid < kCopies6 && static_cast<int>(blockIdx.x) < ntasks)
+    box_issue6(tasks[blockIdx.x], tid, sm, rowaddr[0], &full[0], xin, stride, n);
+  int k = 0;
+  for (int ti = static_cast<int>(blockIdx.x); ti < ntasks; ti += G, ++k) {
+    const int st = k & 1;
+    if (tid < kCopies6 && ti + G < ntasks) {
+      // the other stage is free once every warp released box k-1
+      if (k >= 1) mbar_wait_parity(&empty[st ^ 1], static_cast<unsigned>((k - 1) >> 1) & 1u);
+      box_issue6(tasks[ti + G], tid, sm + (st ^ 1) * kStage6, rowaddr[st ^ 1], &full[st ^ 1], xin, stride, n);
+    }
+    const Task5 t = tasks[ti];
+    const double* __restrict__ tab = &tabs[macros[t.macro].group].stencil[0][0];
+    double w[15];
+#pragma unroll
+    for (int q = 0; q < 15; ++q) w[q] = __ldg(tab + q);
+    // every warp observes the box before releasing it (a released,
+    // unobserved phase would alias the stage's next phase)
+    mbar_wait_parity(&full[st], static_cast<unsigned>(k >> 1) & 1u);
+    const int z = t.z0 + 2 * wid;
+    if (z <= n - t.y0 && t.pad <= n - t.y0 - z) box_walk6(t, rowaddr[st], w, wid, lane, xin, yout, stride, n, tab);
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Variant 7: persistent, double-buffered version of variant 6. Each CTA loops
 // over boxes (macro, 2*kPairs7 planes, kRows7 rows, kCols7 columns); while
@@ -529,17 +585,6 @@ constexpr int kStage7 = kCopies7 * kPitch7;  // doubles per stage
 static_assert(kCols7 % 32 == 0 && kRows7 <= 16 && kCopies7 <= 32 * kWarps7, "p1 pipe tiling");
 
 
-__device__ __forceinline__ void mbar_wait_parity(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "W7_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra W7_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x989680u)
-      : "memory");
-}
 
 // kAsync = false: per-row TMA bulk copies on full / empty mbarriers (variant 7);
 // kAsync = true: the same box rows as coalesced 16-byte cp.async chunks (one
@@ -758,24 +803,41 @@ void build_stencil6_tasks(int nmacros, int n, std::vector<int>& out) {
         }
 }
 
-void launch_p1_stencil6(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
-                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
+template <bool kPersistent>
+static void launch_p1_box(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                          int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
   if (ntasks == 0) return;
   if (n > 1022) fail_arg("p1 box kernel: level too large for 32-bit lattice offsets");
-  // + a margin: in slab mode lanes past the short rows read up to a segment
-  // beyond the last plane's stretch (never stored)
-  const std::size_t smem = (static_cast<std::size_t>(kCopies6) * kPitch6 + 96) * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    TETMF_CUDA(cudaFuncSetAttribute(p1_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    configured = true;
+  // per stage: the box rows + a margin (in slab mode lanes past the short rows
+  // read up to a segment beyond the last plane's stretch; never stored)
+  const std::size_t smem = (kPersistent ? 2 : 1) * (static_cast<std::size_t>(kCopies6) * kPitch6 + 96) * sizeof(double);
+  static int box_ctas = 0;
+  if (box_ctas == 0) {
+    TETMF_CUDA(cudaFuncSetAttribute(p1_box_kernel<kPersistent>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+    int dev = 0, sms = 0, per_sm = 0;
+    TETMF_CUDA(cudaGetDevice(&dev));
+    TETMF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    TETMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p1_box_kernel<kPersistent>, 32 * kWarps6, smem));
+    box_ctas = sms * (per_sm > 0 ? per_sm : 1);
   }
+  const int nbox = kPersistent ? (ntasks < box_ctas ? ntasks : box_ctas) : ntasks;
   // boxes, then the face CTAs (faces z = 0 and y = 0) in the same launch
   const int T = (n + 1) * (n + 2) / 2;
   const int face_ctas = (2 * T * nmacros + 32 * kWarps6 - 1) / (32 * kWarps6);
-  p1_smem_kernel<<<static_cast<unsigned>(ntasks + face_ctas), 32 * kWarps6, smem, s>>>(
-      x, y, reinterpret_cast<const Task5*>(d_tasks), ntasks, nmacros, macro_stride, n, d_tables, d_macros);
-  check_launch("p1_smem");
+  p1_box_kernel<kPersistent><<<static_cast<unsigned>(nbox + face_ctas), 32 * kWarps6, smem, s>>>(
+      x, y, reinterpret_cast<const Task5*>(d_tasks), ntasks, nbox, nmacros, macro_stride, n, d_tables, d_macros);
+  check_launch("p1_box");
+}
+
+void launch_p1_stencil6(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
+  launch_p1_box<false>(x, y, d_tasks, ntasks, macro_stride, n, nmacros, d_tables, d_macros, s);
+}
+
+void launch_p1_stencil10(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
+                         int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
+  launch_p1_box<true>(x, y, d_tasks, ntasks, macro_stride, n, nmacros, d_tables, d_macros, s);
 }
 
 // CTA boxes of variant 7 (macro, z0, y0, x0)

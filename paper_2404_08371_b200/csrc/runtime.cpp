@@ -449,6 +449,9 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
       else if (kernel_variant_ == 4)
         launch_p1_stencil_tile(x, y, ld.tasks4.get(), ld.ntasks4, ld.lay.macro_stride, ld.lay.n, t.p1.get(),
                                ld.macros.get(), s);
+      else if (kernel_variant_ == 10)
+        launch_p1_stencil10(x, y, ld.tasks6.get(), ld.ntasks6, ld.lay.macro_stride, ld.lay.n, nm, t.p1.get(),
+                            ld.macros.get(), s);
       else if (kernel_variant_ == 9)
         launch_p1_stencil2(x, y, ld.tasks.get(), ld.ntasks, ld.lay.macro_stride, ld.lay.n, t.p1.get(),
                            ld.macros.get(), s);

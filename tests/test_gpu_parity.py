@@ -129,7 +129,7 @@ def test_optimized_vs_first_version(tm, mesh, form, level):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("variant", [2, 3, 4, 5, 7, 8, 9])
+@pytest.mark.parametrize("variant", [2, 3, 4, 5, 7, 8, 9, 10])
 @pytest.mark.parametrize("mesh,level", [("cube6", 8), ("single-tet", 7), ("cubes2", 6), ("cubes1x1x2", 5),
                                         ("single-tet", 2)])
 def test_p1_kernel_variants_bitwise(tm, variant, mesh, level):
@@ -150,7 +150,7 @@ def test_p1_kernel_variants_bitwise(tm, variant, mesh, level):
     for _ in range(4):
         op.apply(x, y1, level)
         got = y1.download(level)
-        if variant in (3, 5, 7, 8, 9):
+        if variant in (3, 5, 7, 8, 9, 10):
             assert np.array_equal(got, ref)
         else:
             assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()

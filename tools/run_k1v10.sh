@@ -1,0 +1,6 @@
+export PYTHONPATH=$PWD
+# K1: default box kernel (0) vs persistent double-buffered boxes (10), default and tuning builds
+timeout 120 python tools/k1_ab.py cube6 8 0 10 2>&1 | grep variant
+for v in "$@"; do TETMF_LIB=paper_2404_08371_b200/_lib/variants/libtetmf_$v.so timeout 120 python tools/k1_ab.py cube6 8 0 10 2>&1 | grep variant | sed "s/^/$v /"; done
+timeout 120 python tools/k1_ab.py cubes2 7 0 10 2>&1 | grep variant
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "variants_bitwise" 2>&1 | tail -2
