@@ -110,6 +110,14 @@ int tetmf_apply(tetmf_op* op, const tetmf_fn* src, tetmf_fn* dst, int level, int
  * overwritten); synchronizes before returning. */
 int tetmf_apply_ref_host(tetmf_op* op, tetmf_fn* src, tetmf_fn* dst, int level, const double* host_v,
                          double* host_w);
+/* The same for a batch of nvec independent host vectors (FormSystem::apply
+ * called nvec times): w_k = A v_k, all in reference numbering, pinned host
+ * memory recommended. Pipelined over three streams: the host->device copy
+ * of v_{k+1} and the device->host copy of w_{k-1} overlap the permute /
+ * apply / permute of v_k (two device staging buffers each way). Every w_k is
+ * complete when the call returns (synchronizes). */
+int tetmf_apply_ref_host_batch(tetmf_op* op, tetmf_fn* src, tetmf_fn* dst, int level, int nvec,
+                               const double* const* host_v, double* const* host_w);
 
 /* Dirichlet-masked matrix-free CG (the reference's
  * cg_solve, which its sources do not contain). Homogeneous

@@ -77,6 +77,8 @@ _SIGS = {
     "tetmf_op_destroy": (ctypes.c_int, [_c_vp]),
     "tetmf_apply": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, ctypes.c_int, ctypes.c_int]),
     "tetmf_apply_ref_host": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, ctypes.c_int, _c_dp, _c_dp]),
+    "tetmf_apply_ref_host_batch": (ctypes.c_int, [_c_vp, _c_vp, _c_vp, ctypes.c_int, ctypes.c_int,
+                                                  ctypes.POINTER(_c_dp), ctypes.POINTER(_c_dp)]),
     "tetmf_host_alloc": (ctypes.c_int, [ctypes.POINTER(_c_vp), ctypes.c_int64]),
     "tetmf_host_free": (ctypes.c_int, [_c_vp]),
     "tetmf_plan_ref_map": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, _c_i64p, ctypes.c_int64, _c_i64p]),
@@ -380,6 +382,18 @@ class Operator:
         pv = _dptr(v) if isinstance(v, np.ndarray) else ctypes.cast(_c_vp(v), _c_dp)
         pw = _dptr(w) if isinstance(w, np.ndarray) else ctypes.cast(_c_vp(w), _c_dp)
         _check(lib().tetmf_apply_ref_host(self._h, src.handle, dst.handle, level, pv, pw))
+
+    def apply_ref_host_batch(self, src: Function, dst: Function, level: int, vs, ws):
+        """w_k = A v_k for lists of float64 numpy arrays or raw (pinned) host
+        pointers (int), pipelined (tetmf_apply_ref_host_batch)."""
+        if len(vs) != len(ws):
+            raise ValueError("apply_ref_host_batch: len(vs) != len(ws)")
+
+        def ptr(a):
+            return _dptr(a) if isinstance(a, np.ndarray) else ctypes.cast(_c_vp(a), _c_dp)
+        pv = (_c_dp * len(vs))(*[ptr(a) for a in vs])
+        pw = (_c_dp * len(ws))(*[ptr(a) for a in ws])
+        _check(lib().tetmf_apply_ref_host_batch(self._h, src.handle, dst.handle, level, len(vs), pv, pw))
 
     def cg_solve(self, b: Function, x: Function, level: int, rtol: float = 1e-10, max_iter: int = 1000,
                  diag: Function | None = None):

@@ -295,6 +295,78 @@ int tetmf_apply_ref_host(tetmf_op* op, tetmf_fn* src, tetmf_fn* dst, int level, 
   });
 }
 
+int tetmf_apply_ref_host_batch(tetmf_op* op, tetmf_fn* src, tetmf_fn* dst, int level, int nvec,
+                               const double* const* host_v, double* const* host_w) {
+  return guard([&] {
+    need(op, "op");
+    need(src, "src");
+    need(dst, "dst");
+    if (nvec < 0) fail_arg("apply_ref_host_batch: nvec < 0");
+    if (nvec == 0) return;
+    need(host_v, "host_v");
+    need(host_w, "host_w");
+    for (int k = 0; k < nvec; ++k) {
+      need(host_v[k], "host_v[k]");
+      need(host_w[k], "host_w[k]");
+    }
+    Function& s = *src->impl;
+    Function& d = *dst->impl;
+    Context& c = s.ctx();
+    if (c.nranks() > 1) fail_arg("apply_ref_host_batch: single-rank contexts only");
+    const i64 nd = s.num_ref_dofs(level);
+    if (d.num_ref_dofs(level) != nd) fail_arg("apply_ref_host_batch: src/dst space mismatch");
+    // staging: in[0..1], out[0..1] (reference numbering, device)
+    double* stage = op->impl->ref_scratch(4 * nd);
+    double* in[2] = {stage, stage + nd};
+    double* out[2] = {stage + 2 * nd, stage + 3 * nd};
+    const cudaStream_t cs = c.stream();
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    TETMF_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+    TETMF_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+    std::vector<cudaEvent_t> ev_in(nvec), ev_imported(nvec), ev_exported(nvec), ev_out(nvec);
+    for (int k = 0; k < nvec; ++k) {
+      TETMF_CUDA(cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming));
+      TETMF_CUDA(cudaEventCreateWithFlags(&ev_imported[k], cudaEventDisableTiming));
+      TETMF_CUDA(cudaEventCreateWithFlags(&ev_exported[k], cudaEventDisableTiming));
+      TETMF_CUDA(cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming));
+    }
+    const std::size_t bytes = static_cast<std::size_t>(nd) * sizeof(double);
+    auto issue_h2d = [&](int k) {
+      if (k >= 2) TETMF_CUDA(cudaStreamWaitEvent(h2d, ev_imported[k - 2], 0));  // in[k % 2] consumed
+      TETMF_CUDA(cudaMemcpyAsync(in[k & 1], host_v[k], bytes, cudaMemcpyHostToDevice, h2d));
+      TETMF_CUDA(cudaEventRecord(ev_in[k], h2d));
+    };
+    issue_h2d(0);
+    if (nvec > 1) issue_h2d(1);
+    for (int k = 0; k < nvec; ++k) {
+      // compute stream: import v_k, apply, export w_k
+      TETMF_CUDA(cudaStreamWaitEvent(cs, ev_in[k], 0));
+      s.import_ref_device(level, in[k & 1]);
+      TETMF_CUDA(cudaEventRecord(ev_imported[k], cs));
+      if (k + 2 < nvec) issue_h2d(k + 2);
+      op->impl->apply(s, d, level, Update::Replace);
+      if (k >= 2) TETMF_CUDA(cudaStreamWaitEvent(cs, ev_out[k - 2], 0));  // out[k % 2] drained
+      d.export_ref_device(level, out[k & 1]);
+      TETMF_CUDA(cudaEventRecord(ev_exported[k], cs));
+      // copy-out stream: w_k
+      TETMF_CUDA(cudaStreamWaitEvent(d2h, ev_exported[k], 0));
+      TETMF_CUDA(cudaMemcpyAsync(host_w[k], out[k & 1], bytes, cudaMemcpyDeviceToHost, d2h));
+      TETMF_CUDA(cudaEventRecord(ev_out[k], d2h));
+    }
+    TETMF_CUDA(cudaStreamSynchronize(d2h));
+    TETMF_CUDA(cudaStreamSynchronize(h2d));
+    c.synchronize();
+    for (int k = 0; k < nvec; ++k) {
+      cudaEventDestroy(ev_in[k]);
+      cudaEventDestroy(ev_imported[k]);
+      cudaEventDestroy(ev_exported[k]);
+      cudaEventDestroy(ev_out[k]);
+    }
+    cudaStreamDestroy(h2d);
+    cudaStreamDestroy(d2h);
+  });
+}
+
 int tetmf_fn_dot(const tetmf_fn* a, const tetmf_fn* b, int level, double* out) {
   return guard([&] {
     need(a, "a");

@@ -154,3 +154,36 @@ def test_p1_kernel_variants_bitwise(tm, variant, mesh, level):
             assert np.array_equal(got, ref)
         else:
             assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mesh,form,level", [("cube6", "N1", 3), ("cube6", "P1", 4)])
+def test_apply_ref_host_batch(tm, mesh, form, level):
+    """tetmf_apply_ref_host_batch (pipelined H2D / apply / D2H over three
+    streams, two staging buffers each way) gives every w_k bitwise equal to a
+    synchronous tetmf_apply_ref_host of v_k, for more vectors than staging
+    buffers; and the first one matches the reference's apply."""
+    fid, sid = FORMS[form]
+    ctx = tm.Context(mesh, device=0)
+    src, dst = tm.Function(ctx, sid), tm.Function(ctx, sid)
+    cf = []
+    if form == "N1":
+        a, b = tm.Function(ctx, tm.SPACE_P1), tm.Function(ctx, tm.SPACE_P1)
+        a.fill_coefficient(level, tm.COEFF_ALPHA)
+        b.fill_coefficient(level, tm.COEFF_BETA)
+        cf = [a, b]
+    op = tm.Operator(ctx, fid, cf)
+    src.fill_seeded(level, 3)
+    nd = src.export_ref(level).size
+    rng = np.random.default_rng(5)
+    vs = [rng.uniform(-1.0, 1.0, nd) for _ in range(5)]
+    ws = [np.zeros(nd) for _ in range(5)]
+    op.apply_ref_host_batch(src, dst, level, vs, ws)
+    for v, w in zip(vs, ws):
+        one = np.zeros(nd)
+        op.apply_ref_host(src, dst, level, v, one)
+        assert np.array_equal(w, one)
+    r = RefSystem(mesh, form, level)
+    c0, c1 = r.coefficients()
+    wr, _ = r.apply(vs[0], c0, c1, degree=0)
+    assert relerr(ws[0], wr) <= RTOL
