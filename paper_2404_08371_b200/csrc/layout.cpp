@@ -15,7 +15,7 @@ namespace tetmf {
 
 LevelLayout LevelLayout::make(Space s, int level, int num_macros_global, const std::vector<int>& macros) {
   if (level < 0 || level > 14) fail_arg("level out of range (0..14)");
-  if ((s == Space::ND1 || s == Space::P2) && level < 1) fail_arg("ND1 / P2 storage requires level >= 1");
+  // level 0 (n = 1): the edge lattices have extent 0, one anchor per class
   LevelLayout l;
   l.space = s;
   l.level = level;

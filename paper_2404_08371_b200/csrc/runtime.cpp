@@ -401,7 +401,7 @@ void Operator::check(const Function& src, const Function& dst, int level) const 
   if (src.space() != fi.trial || dst.space() != fi.trial || !src.has_level(level))
     fail_arg("apply: field shape mismatch");
   if (&src == &dst) fail_arg("apply: src and dst must be different functions");
-  if ((form_ == Form::N1CurlCurlMass) && level < 1) fail_arg("apply: N1 requires level >= 1");
+
   for (const Function* c : coeffs_)
     if (!c->has_level(level)) fail_arg("coefficient field has wrong space or level");
 }

@@ -281,7 +281,8 @@ def test_error_model(tm):
     with pytest.raises(tm.InvalidArgument):
         tm.Operator(ctx, tm.FORM_N1, [x, e])        # coefficients live in P1
     with pytest.raises(tm.InvalidArgument):
-        ctx.layout(tm.SPACE_ND1, 0)                # ND1 needs level >= 1
+        ctx.layout(tm.SPACE_ND1, 15)               # levels 0..14
+    assert ctx.layout(tm.SPACE_ND1, 0) is not None  # level 0: one anchor per edge class
     with pytest.raises(tm.InvalidArgument):
         x.size(3)                                  # planning-only context owns no device memory
 

@@ -21,7 +21,7 @@ def _setup(tm, mesh, level, seed):
     return ctx, k, x, tm.Operator(ctx, tm.FORM_P2V, [k])
 
 
-@pytest.mark.parametrize("mesh,level", [("single-tet", 1), ("single-tet", 2), ("single-tet", 3), ("cube6", 1),
+@pytest.mark.parametrize("mesh,level", [("single-tet", 0), ("cube6", 0), ("single-tet", 1), ("single-tet", 2), ("single-tet", 3), ("cube6", 1),
                                         ("cube6", 2), ("cubes2", 1), ("cubes2", 2)])
 def test_p2v_parity_with_reference(tm, tmp_path, mesh, level):
     port_mesh = mesh

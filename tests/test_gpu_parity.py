@@ -60,6 +60,8 @@ def relerr(a, b):
 
 
 CASES = [
+    ("single-tet", "P1", 0), ("cube6", "P1", 0), ("single-tet", "P1K", 0), ("cube6", "P1K", 0),
+    ("single-tet", "N1", 0), ("cube6", "N1", 0),
     ("single-tet", "P1", 1), ("single-tet", "P1", 2), ("single-tet", "P1", 3), ("single-tet", "P1", 5),
     ("single-tet", "P1", 6),
     ("cube6", "P1", 1), ("cube6", "P1", 2), ("cube6", "P1", 4),
