@@ -95,7 +95,8 @@ void build_n1_fold_tasks(const std::vector<int>& local_macros, int n, int parity
 void pad_n1_fold_tasks(std::vector<int>& tasks);
 void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, const double* x, const double* alpha,
                     const double* beta, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
-                    i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s);
+                    i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s,
+                    const N1GramTable* ptab = nullptr);
 int n1_kernel_mode();
 // K2 default: per-point gather over the 24 incident elements (k_p1k_gather.cu)
 void build_p1k_tasks(int nmacros, int n, std::vector<int>& out);

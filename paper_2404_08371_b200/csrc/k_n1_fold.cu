@@ -108,9 +108,27 @@ struct FoldIn {
   }
 };
 
-template <int PASS, int RULE>
+// Gram table of one geometry group as a kernel parameter (the launch's
+// constant bank): every table read has a compile-time offset, so it is a
+// c[0x0][imm] operand of the DFMA -- no shared-memory loads, no registers.
+struct ParamTab {
+  const double* p;
+  template <int I>
+  __device__ __forceinline__ double get() const { return p[I]; }
+};
+struct ParamTabs {
+  const N1GramTable& t;
+  template <int O>
+  __device__ __forceinline__ ParamTab tab() const { return ParamTab{t.o[O]}; }
+};
+
+// PTAB = false: the group's table is staged in shared memory (one launch per
+// pass covers all groups); PTAB = true: it is the parameter `ptab` (one
+// launch per pass and group).
+template <int PASS, int RULE, bool PTAB>
 __global__ void __launch_bounds__(32 * kWarps, TETMF_N1F_MIN_BLOCKS)
-n1_fold_kernel(const N1GramTable* __restrict__ gram, const MacroDesc* __restrict__ macros,
+n1_fold_kernel(const __grid_constant__ N1GramTable ptab, const N1GramTable* __restrict__ gram,
+               const MacroDesc* __restrict__ macros,
                const double* __restrict__ xin, const double* __restrict__ alpha, const double* __restrict__ beta,
                double* __restrict__ yout, const FoldTask* __restrict__ tasks, int ntasks, i64 stride, i64 cstride,
                i64 cf_stride, int n) {
@@ -119,8 +137,10 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram, const MacroDesc* __restrict
   // one launch covers every geometry group of a pass; task lists are padded
   // per group to whole CTAs, so the CTA's first task (always real) names
   // the group of all its warps
-  const N1GramTable* gt = gram + macros[tasks[blockIdx.x * kWarps].macro].group;
-  for (int i = threadIdx.x; i < 6 * kGramRow; i += blockDim.x) (&sg.o[0][0])[i] = __ldg(&gt->o[0][0] + i);
+  if (!PTAB) {
+    const N1GramTable* gt = gram + macros[tasks[blockIdx.x * kWarps].macro].group;
+    for (int i = threadIdx.x; i < 6 * kGramRow; i += blockDim.x) (&sg.o[0][0])[i] = __ldg(&gt->o[0][0] + i);
+  }
   const int lane = threadIdx.x & 31;
   double* ring = dsm + sizeof(N1GramTable) / sizeof(double) + (threadIdx.x >> 5) * kWarpSmem;
   for (int i = lane; i < kRing; i += 32) ring[i] = 0.0;  // unfilled positions must read finite
@@ -273,8 +293,12 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram, const MacroDesc* __restrict
 #pragma unroll
     for (int k = 0; k < 19; ++k) Y[k] = 0.0;
     const int s = X + y + z;
-    cube_elements<RULE>(SmemTabs{sg}, FoldIn{r0, r1, r0 + dq, r1 + dq}, Y, cube && s <= n - 1, cube && s <= n - 2,
-                        cube && s <= n - 3);
+    if (PTAB)
+      cube_elements<RULE>(ParamTabs{ptab}, FoldIn{r0, r1, r0 + dq, r1 + dq}, Y, cube && s <= n - 1,
+                          cube && s <= n - 2, cube && s <= n - 3);
+    else
+      cube_elements<RULE>(SmemTabs{sg}, FoldIn{r0, r1, r0 + dq, r1 + dq}, Y, cube && s <= n - 1, cube && s <= n - 2,
+                          cube && s <= n - 3);
     __syncwarp();  // ring slot tt mod 3 is refilled by the next step's copies
 
     // contributions of the x-1 neighbour cube (same row)
@@ -389,20 +413,26 @@ void pad_n1_fold_tasks(std::vector<int>& tasks) {
   }
 }
 
-// gram: tables of all geometry groups; macros: local macro descriptors
+// gram: tables of all geometry groups; macros: local macro descriptors;
+// ptab (optional): the host copy of ONE group's table -> the parameter-bank
+// kernel for a task range of that group only
 void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, const double* x, const double* alpha,
                     const double* beta, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
-                    i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s) {
+                    i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s, const N1GramTable* ptab) {
   if (ntasks == 0) return;
   if (rule < 0 || rule > 2) fail_internal("n1_fold: rule index out of range");
   constexpr int smem = static_cast<int>(sizeof(N1GramTable) + sizeof(double) * kWarpSmem * kWarps);
+  using K = decltype(&n1_fold_kernel<0, 0, false>);
+  static const K kerns[2][2][3] = {
+      {{n1_fold_kernel<0, 0, false>, n1_fold_kernel<0, 1, false>, n1_fold_kernel<0, 2, false>},
+       {n1_fold_kernel<1, 0, false>, n1_fold_kernel<1, 1, false>, n1_fold_kernel<1, 2, false>}},
+      {{n1_fold_kernel<0, 0, true>, n1_fold_kernel<0, 1, true>, n1_fold_kernel<0, 2, true>},
+       {n1_fold_kernel<1, 0, true>, n1_fold_kernel<1, 1, true>, n1_fold_kernel<1, 2, true>}}};
   static const bool attr = [] {
-    cudaFuncSetAttribute(n1_fold_kernel<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(n1_fold_kernel<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(n1_fold_kernel<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(n1_fold_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(n1_fold_kernel<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(n1_fold_kernel<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int t = 0; t < 2; ++t)
+      for (int p = 0; p < 2; ++p)
+        for (int r = 0; r < 3; ++r)
+          cudaFuncSetAttribute(kerns[t][p][r], cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     double R[2][4][10];
     n1_rule_moments(1, R[0]);
     n1_rule_moments(2, R[1]);
@@ -411,12 +441,10 @@ void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, 
   }();
   (void)attr;
   const unsigned grid = static_cast<unsigned>((ntasks + kWarps - 1) / kWarps);
-  using K = decltype(&n1_fold_kernel<0, 0>);
-  static const K kerns[2][3] = {{n1_fold_kernel<0, 0>, n1_fold_kernel<0, 1>, n1_fold_kernel<0, 2>},
-                                {n1_fold_kernel<1, 0>, n1_fold_kernel<1, 1>, n1_fold_kernel<1, 2>}};
-  kerns[pass][rule]<<<grid, 32 * kWarps, smem, s>>>(gram, macros, x, alpha, beta, y,
-                                                    reinterpret_cast<const FoldTask*>(d_tasks), ntasks, macro_stride,
-                                                    class_stride, coeff_stride, n);
+  static const N1GramTable zero{};
+  kerns[ptab ? 1 : 0][pass][rule]<<<grid, 32 * kWarps, smem, s>>>(
+      ptab ? *ptab : zero, gram, macros, x, alpha, beta, y, reinterpret_cast<const FoldTask*>(d_tasks), ntasks,
+      macro_stride, class_stride, coeff_stride, n);
   check_launch("n1_fold");
 }
 

@@ -178,12 +178,16 @@ Context::LevelData& Context::level(Space s, int level) {
       std::vector<int> merged;
       for (int pass = 0; pass < 2; ++pass) {
         ld->fold_range[2 * pass] = static_cast<int>(merged.size() / 4);
+        ld->fold_group_range.resize(ngroups_, {0, 0, 0, 0});
         for (int g = 0; g < ngroups_; ++g) {
           const auto& gt = ld->group_tasks[g];
           std::vector<int> part(all.begin() + 4 * gt[2 * pass], all.begin() + 4 * (gt[2 * pass] + gt[2 * pass + 1]));
+          ld->fold_group_range[g][2 * pass] = static_cast<int>(merged.size() / 4);
+          ld->fold_group_range[g][2 * pass + 1] = 0;
           if (part.empty()) continue;
           pad_n1_fold_tasks(part);
           merged.insert(merged.end(), part.begin(), part.end());
+          ld->fold_group_range[g][2 * pass + 1] = static_cast<int>(part.size() / 4);
         }
         ld->fold_range[2 * pass + 1] = static_cast<int>(merged.size() / 4) - ld->fold_range[2 * pass];
       }
@@ -380,6 +384,7 @@ Operator::LevelTables& Operator::tables(int level) {
         done[grp[li]] = true;
       }
     lt->n1g.upload(gt.data(), gt.size(), ctx_->stream());
+    lt->n1g_host = gt;
   } else {
     std::vector<P1DeviceTable> t(ng);
     std::vector<bool> done(ng, false);
@@ -472,6 +477,16 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
       if (kernel_variant_ == 1) {
         launch_n1_cubes(x, coeffs_[0]->data(level), coeffs_[1]->data(level), y, ld.macros.get(), nm,
                         ld.lay.macro_stride, ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, t.n1.get(), s);
+      } else if (n1_kernel_mode() == 3 && kernel_variant_ == 2) {
+        // parameter-bank tables: one launch per pass and geometry group
+        const int rule = rule_index();
+        for (int pass = 0; pass < 2; ++pass)
+          for (std::size_t g = 0; g < ld.fold_group_range.size(); ++g) {
+            const auto& r = ld.fold_group_range[g];
+            launch_n1_fold(t.n1g.get(), ld.macros.get(), pass, x, coeffs_[0]->data(level), coeffs_[1]->data(level), y,
+                           ld.fold_tasks.get() + 4 * r[2 * pass], r[2 * pass + 1], ld.lay.macro_stride,
+                           ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, rule, s, &t.n1g_host[g]);
+          }
       } else if (n1_kernel_mode() == 3) {
         const int rule = rule_index();
         for (int pass = 0; pass < 2; ++pass)

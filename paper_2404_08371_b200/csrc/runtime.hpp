@@ -130,6 +130,7 @@ public:
     // ND1, folded kernel: per pass, all groups' tasks padded to whole CTAs
     DeviceBuffer<int> fold_tasks;
     std::array<int, 4> fold_range{0, 0, 0, 0};    // {offset0, count0, offset1, count1}
+    std::vector<std::array<int, 4>> fold_group_range;  // per geometry group, same layout
   };
   LevelData& level(Space s, int level);
   LevelData& ref_level(Space s, int level);  // level() + reference numbering
@@ -207,6 +208,7 @@ private:
     DeviceBuffer<P1DeviceTable> p1;
     DeviceBuffer<N1DeviceTable> n1;
     DeviceBuffer<N1GramTable> n1g;       // Gram form per geometry group (K3 v2)
+    std::vector<N1GramTable> n1g_host;   // host copies (parameter-bank K3 launches)
     DeviceBuffer<P2VTable> p2v;          // P2V coefficient-basis tables per geometry group
   };
   LevelTables& tables(int level);
