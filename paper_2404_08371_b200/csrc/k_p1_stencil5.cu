@@ -297,7 +297,12 @@ constexpr int kCols6 = TETMF_P1S_COLS;
 constexpr int kRows6 = TETMF_P1S_ROWS;
 constexpr int kWarps6 = TETMF_P1S_WARPS;
 constexpr int kSegs6 = kCols6 / 32;
-constexpr int kPlanes6 = 2 * kWarps6 + 2;        // with the halo planes
+#ifndef TETMF_P1S_SINGLE
+#define TETMF_P1S_SINGLE 0  // 1: one plane per warp (7 shared loads per point, fewer registers)
+#endif
+constexpr bool kSingle6 = TETMF_P1S_SINGLE;
+constexpr int kBoxPlanes6 = kSingle6 ? kWarps6 : 2 * kWarps6;  // planes computed per box
+constexpr int kPlanes6 = kBoxPlanes6 + 2;        // with the halo planes
 constexpr int kRowsH6 = kRows6 + 2;              // with the halo rows
 constexpr int kCopies6 = kPlanes6 * kRowsH6;
 constexpr int kPitch6 = kCols6 + 6;              // doubles per shared-memory row
@@ -467,6 +472,66 @@ __device__ __forceinline__ void box_walk6(const Task5& t, const unsigned* __rest
   }
 }
 
+
+// Single-plane walk (TETMF_P1S_SINGLE): warp wid walks plane z = z0 + wid
+// (box planes wid .. wid+2 = z-1, z, z+1) over the box's segments; 7 shared
+// loads per point, the same sums in the same order as the pair walk.
+__device__ __forceinline__ void box_walk6_single(const Task5& t, const unsigned* __restrict__ rowtab,
+                                                 double (&w)[15], int wid, int lane, const double* __restrict__ xin,
+                                                 double* __restrict__ yout, i64 stride, int n,
+                                                 const double* __restrict__ tab) {
+  const int y0 = t.y0, x0 = t.pad;
+  const int z = t.z0 + wid;
+  const double* __restrict__ Xm = xin + static_cast<i64>(t.macro) * stride;
+  double* __restrict__ Ym = yout + static_cast<i64>(t.macro) * stride;
+  const unsigned* __restrict__ RL = rowtab + wid * kRowsH6;
+  const unsigned* __restrict__ RZ = RL + kRowsH6;
+  const unsigned* __restrict__ RU = RZ + kRowsH6;
+  const int la0 = n - z - y0 + 1;
+  const int ystart = y0 == 0 ? 1 : 0;
+#pragma unroll 1
+  for (int sg = 0; sg < kSegs6; ++sg) {
+    const int px = x0 + 32 * sg + lane;
+    if (x0 + 32 * sg >= la0) break;
+    if (x0 + 32 * sg <= 32) {
+      const double* __restrict__ wt = tab + (px == 0 ? 16 : 0);
+#pragma unroll
+      for (int k = 0; k < 15; ++k) w[k] = __ldg(wt + k);
+    }
+    const int s0 = px + y0 + z;
+    const int rlast = z >= 1 ? n - 1 - s0 : -1;
+    double* __restrict__ Yz = Ym + (rstart32(n, z, y0) + px);
+    int la = la0;
+    const unsigned bx = 8u * static_cast<unsigned>(px);
+    double Zm0 = lds_at<0>(RZ[0] + bx), Zm1 = lds_at<8>(RZ[0] + bx);
+    double Z0m = lds_at<-8>(RZ[1] + bx), Z00 = lds_at<0>(RZ[1] + bx);
+    double L00 = lds_at<0>(RL[1] + bx), L01 = lds_at<8>(RL[1] + bx);
+    double Umm = lds_at<-8>(RU[0] + bx), Um0 = lds_at<0>(RU[0] + bx);
+#pragma unroll
+    for (int r = 0; r < kRows6; ++r) {
+      const unsigned iz0 = RZ[r + 1] + bx, iz = RZ[r + 2] + bx, il = RL[r + 2] + bx, iu = RU[r + 1] + bx;
+      const double Z01 = lds_at<8>(iz0);
+      const double Zpm = lds_at<-8>(iz), Zp0 = lds_at<0>(iz);
+      const double Lp0 = lds_at<0>(il), Lp1 = lds_at<8>(il);
+      const double U0m = lds_at<-8>(iu), U00 = lds_at<0>(iu);
+      const double f = sum15(w, Z00, Z01, Z0m, Zp0, Zm0, U00, L00, Zm1, Zpm, L01, U0m, Lp0, Um0, Lp1, Umm);
+      if (r >= ystart && r <= rlast) *Yz = f;
+      Yz += la;
+      --la;
+      Zm0 = Z00; Zm1 = Z01;
+      Z0m = Zpm; Z00 = Zp0;
+      L00 = Lp0; L01 = Lp1;
+      Umm = U0m; Um0 = U00;
+    }
+  }
+  const int yy = y0 + lane;
+  if (lane < kRows6 && z >= 1 && yy >= 1 && yy <= n - z) {
+    const int xx = n - z - yy;
+    if (xx >= x0 && xx < x0 + kCols6)
+      Ym[lattice_index(n, xx, yy, z)] = gather_point(Xm, tab + 16 * (8 | (xx == 0 ? 1 : 0)), n, xx, yy, z);
+  }
+}
+
 // kPersistent = false (variant 6, the default): one box per CTA, copy -> wait
 // -> walk; several CTAs per SM overlap. kPersistent = true (variant 10): a
 // persistent CTA double-buffers two boxes (full / empty mbarrier per stage):
@@ -512,7 +577,7 @@ p1_box_kernel(const double* __restrict__ xin, double* __restrict__ yout, const T
     const Task5 t = tasks[blockIdx.x];
     if (tid < kCopies6) box_issue6(t, tid, sm, rowaddr[0], &full[0], xin, stride, n);
     __syncthreads();  // rowaddr visible
-    const int z = t.z0 + 2 * wid;
+    const int z = t.z0 + (kSingle6 ? wid : 2 * wid);
     if (!(z <= n - t.y0 && t.pad <= n - t.y0 - z)) return;  // (warp 0 always works: it keeps the CTA alive)
     const double* __restrict__ tab = &tabs[macros[t.macro].group].stencil[0][0];
     double w[15];  // interior weights, loaded while the copies land
@@ -520,7 +585,10 @@ p1_box_kernel(const double* __restrict__ xin, double* __restrict__ yout, const T
     for (int k = 0; k < 15; ++k) w[k] = __ldg(tab + k);
     mbar_wait_parity(&full[0], 0u);
     if (TETMF_P1S_COPYONLY) return;  // A/B: the box copies alone
-    box_walk6(t, rowaddr[0], w, wid, lane, xin, yout, stride, n, tab);
+    if (kSingle6)
+      box_walk6_single(t, rowaddr[0], w, wid, lane, xin, yout, stride, n, tab);
+    else
+      box_walk6(t, rowaddr[0], w, wid, lane, xin, yout, stride, n, tab);
     return;
   }
   const int G = nboxctas;
@@ -542,8 +610,13 @@ p1_box_kernel(const double* __restrict__ xin, double* __restrict__ yout, const T
     // every warp observes the box before releasing it (a released,
     // unobserved phase would alias the stage's next phase)
     mbar_wait_parity(&full[st], static_cast<unsigned>(k >> 1) & 1u);
-    const int z = t.z0 + 2 * wid;
-    if (z <= n - t.y0 && t.pad <= n - t.y0 - z) box_walk6(t, rowaddr[st], w, wid, lane, xin, yout, stride, n, tab);
+    const int z = t.z0 + (kSingle6 ? wid : 2 * wid);
+    if (z <= n - t.y0 && t.pad <= n - t.y0 - z) {
+      if (kSingle6)
+        box_walk6_single(t, rowaddr[st], w, wid, lane, xin, yout, stride, n, tab);
+      else
+        box_walk6(t, rowaddr[st], w, wid, lane, xin, yout, stride, n, tab);
+    }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
   }
@@ -794,7 +867,7 @@ void build_stencil6_tasks(int nmacros, int n, std::vector<int>& out) {
   out.clear();
   for (int li = 0; li < nmacros; ++li)
     for (int y0 = 0; y0 <= n; y0 += kRows6)
-      for (int z0 = 0; z0 <= n - y0; z0 += 2 * kWarps6)
+      for (int z0 = 0; z0 <= n - y0; z0 += kBoxPlanes6)
         for (int x0 = 0; x0 <= n - y0 - z0; x0 += kCols6) {
           out.push_back(li);
           out.push_back(z0);
