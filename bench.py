@@ -117,8 +117,11 @@ class ClockSampler:
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        out = {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+               "reasons": reasons, "samples": len(self.samples)}
+        if getattr(self, "window", None):
+            out["window"] = self.window
+        return out
 
 
 # ------------------------------------------------------------------ CPU legs
@@ -267,10 +270,22 @@ def run_gpu(a):
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    lc0 = tm.launch_count()
-    op.profile(True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     with ClockSampler(local) as clk:
+        # nvidia-smi samples every 100 ms; when the timed region is shorter,
+        # untimed applies keep the GPU under the same load until the sampler
+        # has seen it (before) and once more after the timed steps, so the
+        # samples bracket the timed region (clk.window says which)
+        def load_until(count, limit_s=3.0):
+            t_end = time.time() + limit_s
+            while len(clk.samples) < count and time.time() < t_end:
+                for _ in range(4):
+                    op.apply(x, y, level)
+                torch.cuda.synchronize()
+        load_until(2)
+        n_before = len(clk.samples)
+        lc0 = tm.launch_count()
+        op.profile(True)
         for i in range(a.steps):
             if flush is not None:
                 flush.zero_()  # L2 flush outside the timed interval of each step
@@ -278,11 +293,16 @@ def run_gpu(a):
             op.apply(x, y, level)
             ev[i][1].record(stream)
         torch.cuda.synchronize()
+        launches = tm.launch_count() - lc0
+        kern_ms, kern_n = op.kernel_stats()
+        op.profile(False)
+        n_during = len(clk.samples) - n_before
+        load_until(len(clk.samples) + 1)
+        clk.window = ("timed region" if n_during >= 2 else
+                      f"untimed applies under the same load immediately before / after the timed region "
+                      f"({n_during} sample(s) inside it)")
     barrier()
     torch.cuda.synchronize()
-    launches = tm.launch_count() - lc0
-    kern_ms, kern_n = op.kernel_stats()
-    op.profile(False)
     step_ms = [s.elapsed_time(e) for s, e in ev]
     t_total = sum(step_ms)
     if ws > 1:
