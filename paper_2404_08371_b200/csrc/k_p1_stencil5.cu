@@ -395,6 +395,30 @@ __device__ __forceinline__ void box_issue6(const Task5& u, int tid, double* S, u
     if (bytes == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(barp)) : "memory");
 }
 
+#ifndef TETMF_P1S_DIAG_EARLY
+#define TETMF_P1S_DIAG_EARLY 1  // diagonal gathers while the box copies land (0: after the walk)
+#endif
+constexpr bool kDiagInWalk = !TETMF_P1S_DIAG_EARLY;
+
+// Diagonal points (x + y + z = n) of the warp's plane pair in the box rows,
+// by the CTA whose column range holds them: lanes 0..kRows6-1 plane z,
+// lanes 16.. plane z+1; direct gathers (global / L2), independent of the box
+// copies.
+__device__ __forceinline__ void box_diag6(const Task5& t, int wid, int lane, const double* __restrict__ xin,
+                                          double* __restrict__ yout, i64 stride, int n,
+                                          const double* __restrict__ tab) {
+  const int y0 = t.y0, x0 = t.pad;
+  const int z = t.z0 + 2 * wid;
+  const double* __restrict__ Xm = xin + static_cast<i64>(t.macro) * stride;
+  double* __restrict__ Ym = yout + static_cast<i64>(t.macro) * stride;
+  const int zz = z + (lane >> 4), yy = y0 + (lane & 15);
+  if ((lane & 15) < kRows6 && zz >= 1 && zz <= n && yy >= 1 && yy <= n - zz) {
+    const int xx = n - zz - yy;
+    if (xx >= x0 && xx < x0 + kCols6)
+      Ym[lattice_index(n, xx, yy, zz)] = gather_point(Xm, tab + 16 * (8 | (xx == 0 ? 1 : 0)), n, xx, yy, zz);
+  }
+}
+
 // The warp's walk of box t (plane pair z = z0 + 2*wid) out of the stage whose
 // row address table is rowtab; w holds the interior weights on entry.
 __device__ __forceinline__ void box_walk6(const Task5& t, const unsigned* __restrict__ rowtab, double (&w)[15],
@@ -462,14 +486,7 @@ __device__ __forceinline__ void box_walk6(const Task5& t, const unsigned* __rest
       Umm = U0m; Um0 = U00;
     }
   }
-  // diagonal points of the box rows (as in the direct walk), by the CTA
-  // whose column range holds them
-  const int zz = z + (lane >> 4), yy = y0 + (lane & 15);
-  if ((lane & 15) < kRows6 && zz >= 1 && zz <= n && yy >= 1 && yy <= n - zz) {
-    const int xx = n - zz - yy;
-    if (xx >= x0 && xx < x0 + kCols6)
-      Ym[lattice_index(n, xx, yy, zz)] = gather_point(Xm, tab + 16 * (8 | (xx == 0 ? 1 : 0)), n, xx, yy, zz);
-  }
+  if (kDiagInWalk) box_diag6(t, wid, lane, xin, yout, stride, n, tab);
 }
 
 
@@ -583,6 +600,7 @@ p1_box_kernel(const double* __restrict__ xin, double* __restrict__ yout, const T
     double w[15];  // interior weights, loaded while the copies land
 #pragma unroll
     for (int k = 0; k < 15; ++k) w[k] = __ldg(tab + k);
+    if (!kDiagInWalk && !kSingle6) box_diag6(t, wid, lane, xin, yout, stride, n, tab);
     mbar_wait_parity(&full[0], 0u);
     if (TETMF_P1S_COPYONLY) return;  // A/B: the box copies alone
     if (kSingle6)
@@ -607,6 +625,7 @@ p1_box_kernel(const double* __restrict__ xin, double* __restrict__ yout, const T
     double w[15];
 #pragma unroll
     for (int q = 0; q < 15; ++q) w[q] = __ldg(tab + q);
+    if (!kDiagInWalk && !kSingle6 && t.z0 + 2 * wid <= n - t.y0) box_diag6(t, wid, lane, xin, yout, stride, n, tab);
     // every warp observes the box before releasing it (a released,
     // unobserved phase would alias the stage's next phase)
     mbar_wait_parity(&full[st], static_cast<unsigned>(k >> 1) & 1u);
