@@ -200,14 +200,33 @@ __constant__ OrientConsts kOc = make_orient_consts();
 #ifndef TETMF_P2V_MINB
 #define TETMF_P2V_MINB 1
 #endif
+#ifndef TETMF_P2V_STAGE
+#define TETMF_P2V_STAGE 0  // 1: the cube's 27 x and 27 k values staged in shared memory once per cube
+#endif
+constexpr bool kStage2 = TETMF_P2V_STAGE;
+constexpr int kThreads2 = kStage2 ? 64 : kThreads;  // cubes per CTA (static shared memory <= 48 KB)
+
+// cube slots (0..7 vertices, 8..26 edges) touched by the elements valid at
+// anchor-sum class c (0: WU only, 1: + BU BD GU GD, 2: + WD), as bit masks
+constexpr unsigned slot_mask(int cls) {
+  unsigned m = 0;
+  for (int o = 0; o < 6; ++o) {
+    const int need = o == WU ? 0 : o == WD ? 2 : 1;
+    if (need > cls) continue;
+    for (int i = 0; i < 4; ++i) m |= 1u << n1::cube_vertex(o, i);
+    for (int e = 0; e < 6; ++e) m |= 1u << (8 + cube_edge_of(o, e));
+  }
+  return m;
+}
+
 template <int RULE>
-__global__ void __launch_bounds__(kThreads, TETMF_P2V_MINB)
+__global__ void __launch_bounds__(kThreads2, TETMF_P2V_MINB)
 p2v_cubes2_kernel(const double* __restrict__ x, const double* __restrict__ kc, double* __restrict__ y,
                   const MacroDesc* __restrict__ macros, int nmacros, i64 stride, i64 cstride, int n,
                   const P2VTable* __restrict__ tabs) {
-  __shared__ double acc[27][kThreads];  // the cube's accumulators, [slot][thread]
+  __shared__ double acc[27][kThreads2];  // the cube's accumulators, [slot][thread]
   const i64 anchors = tet_count(n - 1);
-  const i64 tid = blockIdx.x * static_cast<i64>(kThreads) + threadIdx.x;
+  const i64 tid = blockIdx.x * static_cast<i64>(kThreads2) + threadIdx.x;
   if (tid >= anchors * nmacros) return;
   const int li = static_cast<int>(tid / anchors);
   int ax, ay, az;
@@ -222,25 +241,57 @@ p2v_cubes2_kernel(const double* __restrict__ x, const double* __restrict__ kc, d
   const CubeRows cr = cube_rows(n, ay, az);
   double* Y = &acc[0][threadIdx.x];
 #pragma unroll
-  for (int i = 0; i < 27; ++i) Y[i * kThreads] = 0.0;
+  for (int i = 0; i < 27; ++i) Y[i * kThreads2] = 0.0;
+#if TETMF_P2V_STAGE
+  // the cube's DoFs touched by a valid element, all loads issued at once
+  __shared__ double xs[27][kThreads2], ks[27][kThreads2];
+  {
+    const unsigned need = s <= n - 3 ? slot_mask(2) : s <= n - 2 ? slot_mask(1) : slot_mask(0);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int gi = cr.Rv[v >> 2][(v >> 1) & 1] + ax + (v & 1);
+      const bool on = (need >> v) & 1u;
+      xs[v][threadIdx.x] = on ? __ldg(xm + gi) : 0.0;
+      ks[v][threadIdx.x] = on ? __ldg(km + gi) : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < 19; ++e) {
+      const CubeEdgeRef r = cube_edge_ref(e);
+      const int gi = vstride + r.c * cs + cr.Re[r.oz][r.oy] + ax + r.ox;
+      const bool on = (need >> (8 + e)) & 1u;
+      xs[8 + e][threadIdx.x] = on ? __ldg(xm + gi) : 0.0;
+      ks[8 + e][threadIdx.x] = on ? __ldg(km + gi) : 0.0;
+    }
+  }
+#endif
   // orientations valid by anchor sum (orient_sum_limit): WU s <= n-1
   // (always), BU BD GU GD s <= n-2, WD s <= n-3
 #pragma unroll 1
   for (int o = 0; o < 6; ++o) {
     if (s > (o == WU ? n - 1 : o == WD ? n - 3 : n - 2)) continue;
+    double xv[10], kv[10], g[10];
+#if TETMF_P2V_STAGE
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+      const int sl = i < 4 ? kOc.vslot[o][i] : kOc.eslot[o][i - 4];
+      xv[i] = xs[sl][threadIdx.x];
+      kv[i] = ks[sl][threadIdx.x];
+      g[i] = __ldg(T->G[o] + i);
+    }
+#else
     int idx[10];
 #pragma unroll
     for (int i = 0; i < 4; ++i) idx[i] = cr.Rv[kOc.vz[o][i]][kOc.vy[o][i]] + ax + kOc.vx[o][i];
 #pragma unroll
     for (int e = 0; e < 6; ++e)
       idx[4 + e] = vstride + kOc.ecls[o][e] * cs + cr.Re[kOc.ez[o][e]][kOc.ey[o][e]] + ax + kOc.ex[o][e];
-    double xv[10], kv[10], g[10];
 #pragma unroll
     for (int i = 0; i < 10; ++i) {
       xv[i] = __ldg(xm + idx[i]);
       kv[i] = __ldg(km + idx[i]);
       g[i] = __ldg(T->G[o] + i);
     }
+#endif
     // K_rs = sum_m k_m C[m][rs]
     double K[10];
 #pragma unroll
@@ -278,24 +329,24 @@ p2v_cubes2_kernel(const double* __restrict__ x, const double* __restrict__ kc, d
           v = fma(3.0, z, v);
         } else {
           v -= z;
-          double& ye = Y[kOc.eslot[o][local_edge_of(q, s2)] * kThreads];
+          double& ye = Y[kOc.eslot[o][local_edge_of(q, s2)] * kThreads2];
           ye = fma(4.0, z, ye);
         }
       }
-      Y[kOc.vslot[o][q] * kThreads] += v;
+      Y[kOc.vslot[o][q] * kThreads2] += v;
     }
   }
   // scatter: DoFs no valid element touched hold exact zeros (skipped; their
   // indices may lie outside the lattice)
 #pragma unroll
   for (int v = 0; v < 8; ++v) {
-    const double val = Y[v * kThreads];
+    const double val = Y[v * kThreads2];
     if (val != 0.0) atomicAdd(ym + cr.Rv[v >> 2][(v >> 1) & 1] + ax + (v & 1), val);
   }
 #pragma unroll
   for (int e = 0; e < 19; ++e) {
     const CubeEdgeRef r = cube_edge_ref(e);
-    const double val = Y[(8 + e) * kThreads];
+    const double val = Y[(8 + e) * kThreads2];
     if (val != 0.0) atomicAdd(ym + vstride + r.c * cs + cr.Re[r.oz][r.oy] + ax + r.ox, val);
   }
 }
@@ -407,19 +458,19 @@ void launch_p2v_cubes2(const double* x, const double* k, double* y, const MacroD
   TETMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * macro_stride * nmacros, s));
   const i64 total = tet_count(n - 1) * nmacros;
   if (total == 0) return;
-  const unsigned grid = static_cast<unsigned>((total + kThreads - 1) / kThreads);
+  const unsigned grid = static_cast<unsigned>((total + kThreads2 - 1) / kThreads2);
   switch (rule) {
     case 0:
-      p2v_cubes2_kernel<0><<<grid, kThreads, 0, s>>>(x, k, y, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
+      p2v_cubes2_kernel<0><<<grid, kThreads2, 0, s>>>(x, k, y, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
       break;
     case 1:
-      p2v_cubes2_kernel<1><<<grid, kThreads, 0, s>>>(x, k, y, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
+      p2v_cubes2_kernel<1><<<grid, kThreads2, 0, s>>>(x, k, y, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
       break;
     case 2:
-      p2v_cubes2_kernel<2><<<grid, kThreads, 0, s>>>(x, k, y, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
+      p2v_cubes2_kernel<2><<<grid, kThreads2, 0, s>>>(x, k, y, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
       break;
     default:
-      p2v_cubes2_kernel<3><<<grid, kThreads, 0, s>>>(x, k, y, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
+      p2v_cubes2_kernel<3><<<grid, kThreads2, 0, s>>>(x, k, y, d_macros, nmacros, macro_stride, class_stride, n, d_tables);
   }
   check_launch("p2v_cubes2");
 }
