@@ -308,9 +308,10 @@ constexpr int kCopies6 = kPlanes6 * kRowsH6;
 constexpr int kPitch6 = kCols6 + 6;              // doubles per shared-memory row
 static_assert(kCols6 % 32 == 0 && kRows6 <= 16 && kCopies6 <= 32 * kWarps6, "p1 smem tiling");
 
-// 32-bit lattice offsets (a level's storage fits in int for n <= 1022)
+// 32-bit lattice offsets: a macro's storage (tet_count(n) points) fits in
+// int up to level 11 (the launchers check); the product is formed in 64 bits
 __device__ __forceinline__ int tet32(int k) {
-  return static_cast<int>(static_cast<unsigned>((k + 1) * (k + 2)) * static_cast<unsigned>(k + 3) / 6u);
+  return static_cast<int>(static_cast<long long>((k + 1) * (k + 2)) * (k + 3) / 6);
 }
 __device__ __forceinline__ int rstart32(int n, int p, int y) {
   return tet32(n) - tet32(n - p) + y * (n - p + 1) - y * (y - 1) / 2;
@@ -899,7 +900,7 @@ template <bool kPersistent>
 static void launch_p1_box(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
                           int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
   if (ntasks == 0) return;
-  if (n > 1022) fail_arg("p1 box kernel: level too large for 32-bit lattice offsets");
+  if (tet_count(n) + n + 96 >= (i64(1) << 31)) fail_arg("p1 box kernel: level too large for 32-bit lattice offsets");
   // per stage: the box rows + a margin (in slab mode lanes past the short rows
   // read up to a segment beyond the last plane's stretch; never stored)
   const std::size_t smem = (kPersistent ? 2 : 1) * (static_cast<std::size_t>(kCopies6) * kPitch6 + 96) * sizeof(double);
@@ -950,7 +951,7 @@ template <bool kAsync>
 static void launch_p1_pipe(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
                            int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
   if (ntasks == 0) return;
-  if (n > 1022) fail_arg("p1 pipe kernel: level too large for 32-bit lattice offsets");
+  if (tet_count(n) + n + 96 >= (i64(1) << 31)) fail_arg("p1 pipe kernel: level too large for 32-bit lattice offsets");
   const std::size_t smem = 2 * static_cast<std::size_t>(kStage7) * sizeof(double);
   static int grid_ctas = 0;
   if (grid_ctas == 0) {

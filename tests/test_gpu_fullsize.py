@@ -87,3 +87,21 @@ def test_fullsize_optimized_vs_first_version(tm, mesh, form, level):
     a, b = _view(y0, level), _view(y1, level)
     assert (a - b).abs().max().item() <= 1e-12 * b.abs().max().item()
     torch.cuda.synchronize()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("level", [10])
+def test_p1_large_level_matches_round1_walk(tm, level):
+    """Levels past BASELINE's L8 (single-tet L10: 180 M points per vector):
+    the default K1 box kernel (32-bit lattice offsets formed in 64 bits)
+    equals the round-1 row walk (variant 9) bitwise."""
+    ctx = tm.Context("single-tet", device=0)
+    x, y0, y1 = tm.Function(ctx, tm.SPACE_P1), tm.Function(ctx, tm.SPACE_P1), tm.Function(ctx, tm.SPACE_P1)
+    op = tm.Operator(ctx, tm.FORM_P1)
+    x.fill_seeded(level, 23)
+    op.apply(x, y0, level)
+    op.set_variant(9)
+    op.apply(x, y1, level)
+    a, b = y0.download(level), y1.download(level)
+    assert np.array_equal(a, b)
+    assert np.abs(a).max() > 0.0
