@@ -9,6 +9,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <vector>
 
 #include "common.hpp"
 #include "exchange.hpp"
@@ -320,16 +321,27 @@ int tetmf_apply_ref_host_batch(tetmf_op* op, tetmf_fn* src, tetmf_fn* dst, int l
     double* in[2] = {stage, stage + nd};
     double* out[2] = {stage + 2 * nd, stage + 3 * nd};
     const cudaStream_t cs = c.stream();
-    cudaStream_t h2d = nullptr, d2h = nullptr;
-    TETMF_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
-    TETMF_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
-    std::vector<cudaEvent_t> ev_in(nvec), ev_imported(nvec), ev_exported(nvec), ev_out(nvec);
-    for (int k = 0; k < nvec; ++k) {
-      TETMF_CUDA(cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming));
-      TETMF_CUDA(cudaEventCreateWithFlags(&ev_imported[k], cudaEventDisableTiming));
-      TETMF_CUDA(cudaEventCreateWithFlags(&ev_exported[k], cudaEventDisableTiming));
-      TETMF_CUDA(cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming));
-    }
+    // streams / events released on every exit path (errors throw)
+    struct Res {
+      cudaStream_t h2d = nullptr, d2h = nullptr;
+      std::vector<cudaEvent_t> ev;
+      ~Res() {
+        if (h2d) cudaStreamSynchronize(h2d);
+        if (d2h) cudaStreamSynchronize(d2h);
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+        if (h2d) cudaStreamDestroy(h2d);
+        if (d2h) cudaStreamDestroy(d2h);
+      }
+    } res;
+    TETMF_CUDA(cudaStreamCreateWithFlags(&res.h2d, cudaStreamNonBlocking));
+    TETMF_CUDA(cudaStreamCreateWithFlags(&res.d2h, cudaStreamNonBlocking));
+    const cudaStream_t h2d = res.h2d, d2h = res.d2h;
+    res.ev.assign(4 * static_cast<std::size_t>(nvec), nullptr);
+    for (auto& e : res.ev) TETMF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEvent_t* ev_in = res.ev.data();
+    cudaEvent_t* ev_imported = ev_in + nvec;
+    cudaEvent_t* ev_exported = ev_imported + nvec;
+    cudaEvent_t* ev_out = ev_exported + nvec;
     const std::size_t bytes = static_cast<std::size_t>(nd) * sizeof(double);
     auto issue_h2d = [&](int k) {
       if (k >= 2) TETMF_CUDA(cudaStreamWaitEvent(h2d, ev_imported[k - 2], 0));  // in[k % 2] consumed
@@ -356,14 +368,6 @@ int tetmf_apply_ref_host_batch(tetmf_op* op, tetmf_fn* src, tetmf_fn* dst, int l
     TETMF_CUDA(cudaStreamSynchronize(d2h));
     TETMF_CUDA(cudaStreamSynchronize(h2d));
     c.synchronize();
-    for (int k = 0; k < nvec; ++k) {
-      cudaEventDestroy(ev_in[k]);
-      cudaEventDestroy(ev_imported[k]);
-      cudaEventDestroy(ev_exported[k]);
-      cudaEventDestroy(ev_out[k]);
-    }
-    cudaStreamDestroy(h2d);
-    cudaStreamDestroy(d2h);
   });
 }
 
