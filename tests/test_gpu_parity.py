@@ -208,3 +208,21 @@ def test_k1_repeated_applies_bitwise(tm, mesh, level, reps):
         y.fill_seeded(level, 1000 + i)
         op.apply(x, y, level)
         assert np.array_equal(y.download(level), ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("form,level", [("N1", 2), ("N1", 4), ("N1", 6), ("P1", 4), ("P1", 7), ("P1K", 5)])
+def test_parity_config5_mesh(tm, tmp_path, form, level):
+    """Config 5's mesh (2x2x2 Kuhn cubes = 48 macros, many interface
+    carriers shared by up to 24 macros) against the reference's own apply on
+    the same mesh file: x and the coefficient fields are the reference's,
+    imported through the reference numbering."""
+    from oracle.refapi import write_kuhn_mesh
+    path = str(tmp_path / "kuhn.mesh")
+    write_kuhn_mesh(path, 2)
+    r = RefSystem(path, form, level)
+    c0, c1 = r.coefficients()
+    x = np.random.default_rng(level).uniform(-1.0, 1.0, r.num_dofs)
+    w, _ = r.apply(x, c0, c1, degree=0)
+    got, _ = gpu_apply(tm, "cubes2", form, level, 0, via_import=x, coeffs_ref=(c0, c1))
+    assert relerr(got, w) <= RTOL
