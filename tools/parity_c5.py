@@ -1,7 +1,7 @@
-"""Parity of the GPU N1 apply on config 5's mesh (2x2x2 Kuhn cubes, 48
-macros) against the reference's own FormSystem::apply (oracle/_ref) at one
-level, x random in the reference numbering, coefficients the reference's.
-usage: python tools/parity_c5.py LEVEL [FORM]"""
+"""Parity of the GPU apply against the reference's own FormSystem::apply
+(oracle/_ref) at one level, x random in the reference numbering,
+coefficients the reference's. Default mesh: config 5's (2x2x2 Kuhn cubes,
+48 macros). usage: python tools/parity_c5.py LEVEL [FORM] [MESH]"""
 import sys
 import tempfile
 import time
@@ -13,16 +13,19 @@ from oracle.refapi import RefSystem, write_kuhn_mesh
 
 level = int(sys.argv[1]) if len(sys.argv) > 1 else 7
 form = sys.argv[2] if len(sys.argv) > 2 else "N1"
+mesh = sys.argv[3] if len(sys.argv) > 3 else "cubes2"
 fid, sid = {"P1": (tm.FORM_P1, tm.SPACE_P1), "N1": (tm.FORM_N1, tm.SPACE_ND1), "P1K": (tm.FORM_P1K, tm.SPACE_P1)}[form]
-path = tempfile.mktemp(suffix=".mesh")
-write_kuhn_mesh(path, 2)
+path = mesh
+if mesh.startswith("cubes"):
+    path = tempfile.mktemp(suffix=".mesh")
+    write_kuhn_mesh(path, int(mesh[5:]))
 t0 = time.time()
 r = RefSystem(path, form, level)
 c0, c1 = r.coefficients()
 x = np.random.default_rng(level).uniform(-1.0, 1.0, r.num_dofs)
 w, _ = r.apply(x, c0, c1, degree=0)
 t_ref = time.time() - t0
-ctx = tm.Context("cubes2", device=0)
+ctx = tm.Context(mesh, device=0)
 xs, ys = tm.Function(ctx, sid), tm.Function(ctx, sid)
 cf = []
 if form == "N1":
@@ -39,5 +42,5 @@ xs.import_ref(level, x)
 op.apply(xs, ys, level)
 got = ys.export_ref(level)
 err = np.abs(got - w).max() / np.abs(w).max()
-print(f"{form} cubes2x2x2 (48 macros) L{level}: {r.num_dofs} DoFs, reference apply {t_ref:.1f} s, "
+print(f"{form} {mesh} L{level}: {r.num_dofs} DoFs, reference apply {t_ref:.1f} s, "
       f"max|y_gpu - y_ref| / max|y_ref| = {err:.3e} ({'PASS' if err <= 1e-12 else 'FAIL'} at 1e-12)")
