@@ -14,7 +14,8 @@ from oracle.refapi import RefSystem, write_kuhn_mesh
 level = int(sys.argv[1]) if len(sys.argv) > 1 else 7
 form = sys.argv[2] if len(sys.argv) > 2 else "N1"
 mesh = sys.argv[3] if len(sys.argv) > 3 else "cubes2"
-fid, sid = {"P1": (tm.FORM_P1, tm.SPACE_P1), "N1": (tm.FORM_N1, tm.SPACE_ND1), "P1K": (tm.FORM_P1K, tm.SPACE_P1)}[form]
+fid, sid = {"P1": (tm.FORM_P1, tm.SPACE_P1), "N1": (tm.FORM_N1, tm.SPACE_ND1), "P1K": (tm.FORM_P1K, tm.SPACE_P1),
+            "P2V": (tm.FORM_P2V, tm.SPACE_P2)}[form]
 path = mesh
 if mesh.startswith("cubes"):
     path = tempfile.mktemp(suffix=".mesh")
@@ -33,8 +34,8 @@ if form == "N1":
     a.import_ref(level, c0)
     b.import_ref(level, c1)
     cf = [a, b]
-elif form == "P1K":
-    k = tm.Function(ctx, tm.SPACE_P1)
+elif form in ("P1K", "P2V"):
+    k = tm.Function(ctx, tm.SPACE_P1 if form == "P1K" else tm.SPACE_P2)
     k.import_ref(level, c0)
     cf = [k]
 op = tm.Operator(ctx, fid, cf)
