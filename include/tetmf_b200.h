@@ -49,6 +49,7 @@ extern "C" {
 typedef struct tetmf_ctx tetmf_ctx;
 typedef struct tetmf_fn tetmf_fn;
 typedef struct tetmf_op tetmf_op;
+typedef struct tetmf_loopback tetmf_loopback;
 
 enum {
   TETMF_OK = 0,
@@ -78,6 +79,21 @@ int tetmf_ctx_create(const char* mesh_desc, int device, tetmf_ctx** out);
  * nranks == 1 or planning-only contexts. */
 int tetmf_ctx_create_dist(const char* mesh_desc, int device, int rank, int nranks,
                           const void* nccl_unique_id, tetmf_ctx** out);
+/* Loopback group: nranks "virtual ranks" of ONE process on ONE device, each
+ * driven by its own host thread (collective calls -- apply, dot, solvers --
+ * must be made by every rank of the group). The interface exchange and the
+ * solver all-gather run as device-to-device copies between the virtual
+ * ranks' buffers, ordered by CUDA events and host barriers; the pack /
+ * combine / interface-sum kernels are the multi-GPU path's own. No kernel
+ * waits on another, so this is safe on a single GPU. Replaces nothing in the
+ * reference (its parallel layer is HyTeG MPI); it is the
+ * single-device test mode of the multi-rank apply. */
+int tetmf_loopback_create(int nranks, tetmf_loopback** out);
+int tetmf_loopback_destroy(tetmf_loopback* group);
+int tetmf_ctx_create_loopback(const char* mesh_desc, int device, tetmf_loopback* group, int rank, tetmf_ctx** out);
+/* one line describing the context's transport ("nccl rank r of N ...",
+ * "loopback virtual rank r of N ...", "single rank") */
+int tetmf_ctx_transport_info(const tetmf_ctx* ctx, char* buf, int buflen);
 int tetmf_ctx_destroy(tetmf_ctx* ctx);
 int tetmf_ctx_set_stream(tetmf_ctx* ctx, void* cuda_stream); /* NULL -> own stream */
 int tetmf_ctx_synchronize(tetmf_ctx* ctx);

@@ -56,6 +56,11 @@ _SIGS = {
     "tetmf_ctx_create_dist": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_vp,
                                              ctypes.POINTER(_c_vp)]),
     "tetmf_ctx_destroy": (ctypes.c_int, [_c_vp]),
+    "tetmf_loopback_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_c_vp)]),
+    "tetmf_loopback_destroy": (ctypes.c_int, [_c_vp]),
+    "tetmf_ctx_create_loopback": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _c_vp, ctypes.c_int,
+                                                 ctypes.POINTER(_c_vp)]),
+    "tetmf_ctx_transport_info": (ctypes.c_int, [_c_vp, ctypes.c_char_p, ctypes.c_int]),
     "tetmf_ctx_set_stream": (ctypes.c_int, [_c_vp, _c_vp]),
     "tetmf_ctx_synchronize": (ctypes.c_int, [_c_vp]),
     "tetmf_ctx_num_macros": (ctypes.c_int, [_c_vp, _c_ip, _c_ip]),
@@ -149,14 +154,77 @@ def _check(rc: int):
         raise TetmfError(rc, msg)
 
 
-def _dptr(a: np.ndarray):
-    assert a.dtype == np.float64 and a.flags.c_contiguous
+def _dptr(a: np.ndarray, size: Optional[int] = None):
+    """float64 C-contiguous array -> double*; size: required element count.
+    Explicit checks (not asserts, which python -O strips): the C side copies
+    exactly the count it expects, so a short array would overflow."""
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous:
+        raise InvalidArgument(EINVAL, "expected a C-contiguous float64 numpy array")
+    if size is not None and a.size != size:
+        raise InvalidArgument(EINVAL, f"array has {a.size} entries, expected {size}")
     return a.ctypes.data_as(_c_dp)
 
 
-def _iptr(a: np.ndarray):
-    assert a.dtype == np.int64 and a.flags.c_contiguous
+def _iptr(a: np.ndarray, size: Optional[int] = None):
+    if not isinstance(a, np.ndarray) or a.dtype != np.int64 or not a.flags.c_contiguous:
+        raise InvalidArgument(EINVAL, "expected a C-contiguous int64 numpy array")
+    if size is not None and a.size != size:
+        raise InvalidArgument(EINVAL, f"array has {a.size} entries, expected {size}")
     return a.ctypes.data_as(_c_i64p)
+
+
+class LoopbackGroup:
+    """nranks virtual ranks of this process on one device (tetmf_loopback_*):
+    the multi-rank apply's exchange and all-gather as device-to-device copies.
+    Drive each rank's collective calls from its own thread (run_ranks)."""
+
+    def __init__(self, nranks: int):
+        h = _c_vp()
+        _check(lib().tetmf_loopback_create(nranks, ctypes.byref(h)))
+        self._h = h
+        self.nranks = nranks
+
+    @property
+    def handle(self):
+        return self._h
+
+    def contexts(self, mesh: str, device: int = 0) -> list["Context"]:
+        return [Context.loopback(self, mesh, r, device) for r in range(self.nranks)]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tetmf_loopback_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_ranks(fn, nranks: int):
+    """Runs fn(rank) for every rank in its own thread (ctypes releases the
+    GIL during library calls, so the ranks meet at the collective steps);
+    returns the results in rank order and re-raises the first failure."""
+    import threading
+    out, err = [None] * nranks, [None] * nranks
+
+    def body(r):
+        try:
+            out[r] = fn(r)
+        except BaseException as e:  # noqa: BLE001 -- re-raised below
+            err[r] = e
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    return out
 
 
 class Context:
@@ -174,6 +242,22 @@ class Context:
         self.device = device
         self.rank = rank
         self.nranks = nranks
+
+    @classmethod
+    def loopback(cls, group: "LoopbackGroup", mesh: str, rank: int, device: int = 0) -> "Context":
+        """Virtual rank `rank` of a loopback group (tetmf_ctx_create_loopback)."""
+        self = cls.__new__(cls)
+        h = _c_vp()
+        _check(lib().tetmf_ctx_create_loopback(mesh.encode(), device, group.handle, rank, ctypes.byref(h)))
+        self._h = h
+        self.mesh, self.device, self.rank, self.nranks = mesh, device, rank, group.nranks
+        self._group = group  # keeps the group alive as long as its contexts
+        return self
+
+    def transport_info(self) -> str:
+        buf = ctypes.create_string_buffer(256)
+        _check(lib().tetmf_ctx_transport_info(self._h, buf, 256))
+        return buf.value.decode()
 
     @property
     def handle(self):
@@ -378,19 +462,22 @@ class Operator:
         _check(lib().tetmf_apply(self._h, src.handle, dst.handle, level, update))
 
     def apply_ref_host(self, src: Function, dst: Function, level: int, v, w):
-        """v, w: float64 numpy arrays or raw (pinned) host pointers (int)."""
-        pv = _dptr(v) if isinstance(v, np.ndarray) else ctypes.cast(_c_vp(v), _c_dp)
-        pw = _dptr(w) if isinstance(w, np.ndarray) else ctypes.cast(_c_vp(w), _c_dp)
+        """v, w: float64 numpy arrays of num_ref_dofs(level) entries (checked)
+        or raw (pinned) host pointers (int) of that many doubles."""
+        nd = src.num_ref_dofs(level)
+        pv = _dptr(v, nd) if isinstance(v, np.ndarray) else ctypes.cast(_c_vp(v), _c_dp)
+        pw = _dptr(w, nd) if isinstance(w, np.ndarray) else ctypes.cast(_c_vp(w), _c_dp)
         _check(lib().tetmf_apply_ref_host(self._h, src.handle, dst.handle, level, pv, pw))
 
     def apply_ref_host_batch(self, src: Function, dst: Function, level: int, vs, ws):
         """w_k = A v_k for lists of float64 numpy arrays or raw (pinned) host
         pointers (int), pipelined (tetmf_apply_ref_host_batch)."""
         if len(vs) != len(ws):
-            raise ValueError("apply_ref_host_batch: len(vs) != len(ws)")
+            raise InvalidArgument(EINVAL, "apply_ref_host_batch: len(vs) != len(ws)")
+        nd = src.num_ref_dofs(level)
 
         def ptr(a):
-            return _dptr(a) if isinstance(a, np.ndarray) else ctypes.cast(_c_vp(a), _c_dp)
+            return _dptr(a, nd) if isinstance(a, np.ndarray) else ctypes.cast(_c_vp(a), _c_dp)
         pv = (_c_dp * len(vs))(*[ptr(a) for a in vs])
         pw = (_c_dp * len(ws))(*[ptr(a) for a in ws])
         _check(lib().tetmf_apply_ref_host_batch(self._h, src.handle, dst.handle, level, len(vs), pv, pw))

@@ -6,6 +6,7 @@
 #include "../../include/tetmf_b200.h"
 
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -17,11 +18,7 @@
 #include "runtime_check.hpp"
 #include "solver.hpp"
 
-namespace tetmf {
-void nccl_get_unique_id(void* out);
-void* nccl_comm_create(int nranks, const void* unique_id, int rank);
-void nccl_comm_destroy(void* comm);
-} // namespace tetmf
+#include "transport.hpp"
 
 using namespace tetmf;
 
@@ -33,6 +30,9 @@ struct tetmf_fn {
 };
 struct tetmf_op {
   std::unique_ptr<Operator> impl;
+};
+struct tetmf_loopback {
+  std::shared_ptr<LoopbackHub> hub;
 };
 
 namespace {
@@ -100,10 +100,49 @@ int tetmf_ctx_create_dist(const char* mesh_desc, int device, int rank, int nrank
     c->impl = std::make_unique<Context>(mesh_desc, device, rank, nranks, partition_macros(nm, rank, nranks));
     if (nranks > 1 && device >= 0) {
       need(nccl_unique_id, "nccl_unique_id");
-      void* comm = nccl_comm_create(nranks, nccl_unique_id, rank);
-      c->impl->attach_exchange_backend(std::shared_ptr<void>(comm, nccl_comm_destroy));
+      c->impl->attach_transport(make_nccl_transport(nranks, nccl_unique_id, rank));
     }
     *out = c.release();
+  });
+}
+
+int tetmf_loopback_create(int nranks, tetmf_loopback** out) {
+  return guard([&] {
+    need(out, "out");
+    if (nranks < 1) fail_arg("loopback: nranks must be >= 1");
+    auto g = std::make_unique<tetmf_loopback>();
+    g->hub = std::make_shared<LoopbackHub>(nranks);
+    *out = g.release();
+  });
+}
+
+int tetmf_loopback_destroy(tetmf_loopback* g) {
+  return guard([&] { delete g; });
+}
+
+int tetmf_ctx_create_loopback(const char* mesh_desc, int device, tetmf_loopback* group, int rank, tetmf_ctx** out) {
+  return guard([&] {
+    need(mesh_desc, "mesh_desc");
+    need(group, "group");
+    need(out, "out");
+    if (device < 0) fail_arg("loopback: virtual ranks need a device");
+    const int nranks = group->hub->nranks();
+    if (rank < 0 || rank >= nranks) fail_arg("bad rank / world size");
+    auto c = std::make_unique<tetmf_ctx>();
+    const int nm = mesh_by_name(mesh_desc).num_tets();
+    c->impl = std::make_unique<Context>(mesh_desc, device, rank, nranks, partition_macros(nm, rank, nranks));
+    if (nranks > 1) c->impl->attach_transport(make_loopback_transport(group->hub, rank));
+    *out = c.release();
+  });
+}
+
+int tetmf_ctx_transport_info(const tetmf_ctx* ctx, char* buf, int buflen) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(buf, "buf");
+    if (buflen <= 0) fail_arg("buflen must be positive");
+    const std::string d = ctx->impl->transport() ? ctx->impl->transport()->describe() : std::string("single rank");
+    std::snprintf(buf, static_cast<size_t>(buflen), "%s", d.c_str());
   });
 }
 

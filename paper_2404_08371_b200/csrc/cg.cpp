@@ -16,8 +16,6 @@
 
 namespace tetmf {
 
-void nccl_allgather_doubles(void* comm, const double* d_in, double* d_out, int count, cudaStream_t stream);
-
 namespace {
 
 SlotSpace slot_space(const Context::LevelData& ld) {
@@ -45,7 +43,8 @@ double masked_dot(const Function& a, const Function& b, int level) {
   }
   double out = 0.0;
   if (ctx.nranks() > 1) {
-    nccl_allgather_doubles(ctx.comm_backend().get(), local, gathered, 1, s);
+    if (!ctx.transport()) throw CommError("dot: no transport attached to the multi-rank context");
+    ctx.transport()->allgather(local, gathered, 1, s);
     launch_sum_ordered(gathered, ctx.nranks(), total, s);
     TETMF_CUDA(cudaMemcpyAsync(&out, total, sizeof(double), cudaMemcpyDeviceToHost, s));
   } else {

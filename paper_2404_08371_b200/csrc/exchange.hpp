@@ -24,6 +24,7 @@
 #include "lattice.hpp"
 #include "layout.hpp"
 #include "mesh.hpp"
+#include "transport.hpp"
 
 namespace tetmf {
 
@@ -91,19 +92,21 @@ TM_HD void interface_sum_one(double* y, const i64* offsets, const i64* copies, i
   }
 }
 
-// Device side of one level's plan + the NCCL transport.
+// Device side of one level's plan; the bytes move through a Transport
+// (NCCL send/recv, or device-to-device copies between loopback virtual ranks).
 class Exchange {
 public:
-  Exchange(ExchangePlan plan, void* nccl_comm);
+  Exchange(ExchangePlan plan, Transport* transport);
   ~Exchange();
   // pack -> send/recv -> combine on `stream` (signed_values = false: ND1
-  // orientation signs ignored, for operator diagonals)
+  // orientation signs ignored, for operator diagonals). Collective: every
+  // rank calls it, also ranks without cross-rank carriers.
   void run(double* y, cudaStream_t stream, bool signed_values = true);
   const ExchangePlan& plan() const { return plan_; }
 
 private:
   ExchangePlan plan_;
-  void* comm_;
+  Transport* transport_;
   i64* d_send_index_ = nullptr;
   i64* d_group_offsets_ = nullptr;
   i64* d_group_entries_ = nullptr;

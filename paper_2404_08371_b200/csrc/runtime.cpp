@@ -237,7 +237,7 @@ Context::LevelData& Context::level(Space s, int level) {
   }
   if (nranks_ > 1)
     ld->exchange = std::make_unique<Exchange>(build_exchange_plan(mesh_, topo_, ld->lay, rank_of, rank_),
-                                              comm_backend_.get());
+                                              transport_.get());
   auto& ref = *ld;
   levels_.emplace(key, std::move(ld));
   return ref;
@@ -414,9 +414,12 @@ void Operator::check(const Function& src, const Function& dst, int level) const 
 void Operator::kernel_apply(const double* x, double* y, int level) {
   auto& ld = ctx_->level(info().trial, level);
   const int nm = static_cast<int>(ld.lay.macros.size());
-  if (nm == 0) return;
-  auto& t = tables(level);
   const cudaStream_t s = ctx_->stream();
+  if (nm == 0) {  // a rank without macros still takes part in the exchange
+    if (ld.exchange) ld.exchange->run(y, s);
+    return;
+  }
+  auto& t = tables(level);
   cudaEvent_t ev_stop = nullptr;
   if (profiling_) {
     if (events_used_ == events_.size()) {

@@ -31,6 +31,7 @@
 #include "layout.hpp"
 #include "mesh.hpp"
 #include "tables.hpp"
+#include "transport.hpp"
 
 namespace tetmf {
 
@@ -135,8 +136,9 @@ public:
   LevelData& level(Space s, int level);
   LevelData& ref_level(Space s, int level);  // level() + reference numbering
 
-  void attach_exchange_backend(std::shared_ptr<void> backend) { comm_backend_ = std::move(backend); }
-  const std::shared_ptr<void>& comm_backend() const { return comm_backend_; }
+  // NCCL (one process per GPU) or loopback (virtual ranks on one GPU)
+  void attach_transport(std::shared_ptr<Transport> t) { transport_ = std::move(t); }
+  Transport* transport() const { return transport_.get(); }
 
 private:
   MacroMesh mesh_;
@@ -148,7 +150,7 @@ private:
   cudaStream_t stream_ = nullptr;
   cudaStream_t own_stream_ = nullptr;
   std::map<std::pair<int, int>, std::unique_ptr<LevelData>> levels_;
-  std::shared_ptr<void> comm_backend_;
+  std::shared_ptr<Transport> transport_;
 };
 
 class Function {

@@ -1,0 +1,150 @@
+"""Multi-rank apply on ONE B200 through the loopback transport.
+
+P virtual ranks (tetmf_ctx_create_loopback), one host thread each, run the
+product's multi-rank path end to end: element kernels on the rank's macros,
+K4 for rank-local interface groups, the exchange pack kernel, the transfer
+(device-to-device copies between the ranks' buffers instead of NCCL
+send/recv), the combine kernel, and the solver's scalar all-gather. The
+results must be bitwise equal to the single-rank apply (every interface sum
+runs in ascending global macro order, exchange.hpp), and within 1e-12 of the
+reference's FormSystem::apply (oracle/_ref) after reassembly.
+
+Partitions: contiguous macro ranges (runtime.cpp partition_macros); cube6
+over 8 ranks leaves two ranks without macros (they still take part in every
+collective step).
+"""
+import numpy as np
+import pytest
+
+from oracle.refapi import RefSystem, write_kuhn_mesh
+
+pytestmark = pytest.mark.gpu
+
+FORMS = {"P1": (0, 0), "P1K": (3, 0), "N1": (2, 2), "P2V": (1, 1)}
+
+
+def _setup(tm, ctx, form, level, seed=42):
+    fid, sid = FORMS[form]
+    x, y = tm.Function(ctx, sid), tm.Function(ctx, sid)
+    cf = []
+    if form == "N1":
+        a, b = tm.Function(ctx, tm.SPACE_P1), tm.Function(ctx, tm.SPACE_P1)
+        a.fill_coefficient(level, tm.COEFF_ALPHA)
+        b.fill_coefficient(level, tm.COEFF_BETA)
+        cf = [a, b]
+    elif form in ("P1K", "P2V"):
+        k = tm.Function(ctx, tm.SPACE_P1 if form == "P1K" else tm.SPACE_P2)
+        k.fill_coefficient(level, tm.COEFF_K)
+        cf = [k]
+    op = tm.Operator(ctx, fid, cf)
+    x.fill_seeded(level, seed)
+    y.size(level)
+    return x, y, op, cf
+
+
+def _single(tm, mesh, form, level):
+    ctx = tm.Context(mesh, device=0)
+    x, y, op, cf = _setup(tm, ctx, form, level)
+    op.apply(x, y, level)
+    d = tm.Function(ctx, FORMS[form][1])
+    op.diagonal(d, level)
+    ms, _ = ctx.layout(FORMS[form][1], level)
+    return ctx, y.download(level).reshape(-1, ms), d.download(level).reshape(-1, ms), ms
+
+
+def _virtual(tm, mesh, form, level, nranks):
+    group = tm.LoopbackGroup(nranks)
+    ctxs = group.contexts(mesh, device=0)
+    objs = [_setup(tm, c, form, level) for c in ctxs]
+
+    def rank_body(r):
+        x, y, op, _ = objs[r]
+        op.apply(x, y, level)
+        d = tm.Function(ctxs[r], FORMS[form][1])
+        op.diagonal(d, level)
+        ctxs[r].synchronize()
+        return y.download(level), d.download(level)
+
+    res = tm.run_ranks(rank_body, nranks)
+    return ctxs, res
+
+
+CASES = [("cubes2", "N1", 4, 2), ("cubes2", "N1", 5, 4), ("cubes2", "N1", 4, 8), ("cube6", "P1", 6, 2),
+         ("cube6", "P1", 6, 4), ("cube6", "P1", 5, 8), ("cubes2", "P1K", 4, 8), ("cube6", "N1", 3, 8),
+         ("cube6", "P2V", 3, 4), ("cubes1x1x2", "P1", 5, 3)]
+
+
+@pytest.mark.parametrize("mesh,form,level,nranks", CASES)
+def test_virtual_ranks_bitwise_equal_single_rank(tm, mesh, form, level, nranks):
+    ctx1, y1, d1, ms = _single(tm, mesh, form, level)
+    ctxs, res = _virtual(tm, mesh, form, level, nranks)
+    seen = []
+    for c, (y, d) in zip(ctxs, res):
+        macros = c.local_macros()
+        seen += macros
+        assert "loopback virtual rank" in c.transport_info()
+        if not macros:
+            continue
+        assert np.array_equal(y.reshape(-1, ms), y1[macros]), f"rank {c.rank}: apply differs"
+        assert np.array_equal(d.reshape(-1, ms), d1[macros]), f"rank {c.rank}: diagonal differs"
+    assert sorted(seen) == list(range(ctx1.num_macros()[0]))
+
+
+@pytest.mark.parametrize("mesh,form,level,nranks", [("cubes2", "N1", 4, 4), ("cube6", "P1", 4, 8),
+                                                    ("cubes2", "P1K", 3, 2)])
+def test_virtual_ranks_match_reference(tm, tmp_path, mesh, form, level, nranks):
+    """Reassemble the ranks' storage into one single-rank function, export it
+    in reference numbering and compare with the reference's apply."""
+    ctxs, res = _virtual(tm, mesh, form, level, nranks)
+    ctx = tm.Context(mesh, device=0)
+    x, y, _, _ = _setup(tm, ctx, form, level)
+    ms, _ = ctx.layout(FORMS[form][1], level)
+    full = np.zeros((ctx.num_macros()[0], ms))
+    for c, (yr, _) in zip(ctxs, res):
+        if c.local_macros():
+            full[c.local_macros()] = yr.reshape(-1, ms)
+    y.upload(level, full.ravel())
+    got = y.export_ref(level)
+    rmesh = write_kuhn_mesh(str(tmp_path / "k.mesh"), int(mesh[5:])) if mesh.startswith("cubes") else mesh
+    ref = RefSystem(rmesh, form, level)
+    c0, c1 = ref.coefficients()
+    want, _ = ref.apply(x.export_ref(level), c0, c1)
+    assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+
+
+def test_virtual_ranks_cg_and_dot(tm):
+    """The solver's all-gather through the loopback transport: inner products
+    equal the single-rank ones to rounding, CG converges in the same number of
+    iterations to the same solution."""
+    mesh, form, level, nranks = "cubes2", "P1", 3, 4
+    ctx = tm.Context(mesh, device=0)
+    xs, b, op, _ = _setup(tm, ctx, form, level, seed=5)
+    xs.fill_seeded(level, 5, True)
+    op.apply(xs, b, level)
+    b.mask_dirichlet(level)
+    dot1 = b.dot(b, level)
+    x1 = tm.Function(ctx, 0)
+    it1, _, ok1 = op.cg_solve(b, x1, level, rtol=1e-10, max_iter=500)
+    assert ok1
+    ms, _ = ctx.layout(0, level)
+    sol1 = x1.download(level).reshape(-1, ms)
+
+    group = tm.LoopbackGroup(nranks)
+    ctxs = group.contexts(mesh, device=0)
+
+    def body(r):
+        xr, br, opr, _ = _setup(tm, ctxs[r], form, level, seed=5)
+        xr.fill_seeded(level, 5, True)
+        opr.apply(xr, br, level)
+        br.mask_dirichlet(level)
+        dot = br.dot(br, level)
+        sol = tm.Function(ctxs[r], 0)
+        it, _, ok = opr.cg_solve(br, sol, level, rtol=1e-10, max_iter=500)
+        return dot, it, ok, sol.download(level)
+
+    out = tm.run_ranks(body, nranks)
+    for c, (dot, it, ok, sol) in zip(ctxs, out):
+        assert ok and abs(dot - dot1) <= 1e-13 * abs(dot1)
+        assert abs(it - it1) <= 1
+        assert np.abs(sol.reshape(-1, ms) - sol1[c.local_macros()]).max() <= 1e-8 * np.abs(sol1).max()
+    assert len({o[0] for o in out}) == 1  # every rank sees the same scalar
