@@ -48,6 +48,9 @@ CONFIGS = {
     "c4": dict(name="P1 -Laplace cube6 L8 (config 4, strong scaling)", mesh="cube6", form="P1", level=8),
     "c5": dict(name="N1 alpha curl curl + beta, 48 macros/GPU L8 (config 5, weak scaling)", mesh=None,
                form="N1", level=8),
+    # config 2's form (P1 -div(k grad)) at config 4's bandwidth-bound size
+    "c2l": dict(name="P1 -div(k grad) cube6 L8 (config 2's form at config 4's size)", mesh="cube6", form="P1K",
+                level=8),
     # SURVEY.md 8(f) #2 (not a BASELINE config): the paper's P2V form
     "p2v": dict(name="P2V -div(k grad), u and k in P2, cube6 L8 (SURVEY 8(f) #2)", mesh="cube6", form="P2V",
                 level=8),
@@ -55,7 +58,7 @@ CONFIGS = {
 WEAK_MESH = {1: "cubes2x2x2", 2: "cubes2x2x4", 4: "cubes2x4x4", 8: "cubes4x4x4"}
 CPU_SAMPLE = {  # bounded sample of each workload for the CPU reference leg
     "c1": ("single-tet", 6), "c2": ("single-tet", 6), "c3": ("single-tet", 5),
-    "c4": ("cube6", 6), "c5": ("cubes2x2x2", 4), "p2v": ("cube6", 4),
+    "c4": ("cube6", 6), "c5": ("cubes2x2x2", 4), "p2v": ("cube6", 4), "c2l": ("cube6", 6),
 }
 # P2V: the factored algorithm's count (k_p2v.cu: K 190, U 28, W 112, Z 112,
 # contractions 28, accumulation 10 flop); the table form needs 1300
@@ -200,6 +203,110 @@ def run_reference_arm(a):
 
 
 # ------------------------------------------------------------------ GPU leg
+def roofline(cfg_key, form, local_counts, kern_avg_ms, ms_per_step, fp64_peak):
+    """Roofline of the dominant (element) kernel: algorithmic flops (N1, P2V:
+    FLOP_PER_ELEM x elements) or compulsory bytes (P1: x + y, P1K: x + k + y
+    per point) per launch / its CUDA-event duration, against the measured
+    peak; traffic = ncu DRAM bytes per launch from the committed capture."""
+    traffic = None
+    for name in ("r2_traffic.json", "r1_traffic.json"):
+        try:
+            traffic = json.load(open(os.path.join(ROOT, "profiles", name))).get(cfg_key)
+        except Exception:
+            traffic = None
+        if traffic:
+            break
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    sec = kern_avg_ms * 1e-3
+    if form in ("N1", "P2V"):
+        nd1_local, p1_local = local_counts["nd1_edges"], local_counts["p1_points"]
+        flops = FLOP_PER_ELEM[form] * local_counts["elements"]
+        # N1: x, y (edges) + alpha, beta (points); P2V: x, k, y (points + edges)
+        bytes_alg = 8.0 * ((2 * nd1_local + 2 * p1_local) if form == "N1" else 3 * (nd1_local + p1_local))
+        roof = {"bound": "fp64", "achieved": flops / sec / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": (flops / sec / 1e12) / fp64_peak if fp64_peak else None,
+                "flop_per_launch": flops, "flop_per_element": FLOP_PER_ELEM[form],
+                "peak_source": "measured FP64 DFMA-chain probe (tetmf_measure_fp64_peak) on this GPU",
+                "hbm": {"achieved": bytes_alg / sec / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                        "bytes_per_launch": bytes_alg}}
+    else:
+        nbytes = 8.0 * local_counts["p1_points"] * (3 if form == "P1K" else 2)
+        roof = {"bound": "hbm", "achieved": nbytes / sec / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                "frac": nbytes / sec / 1e9 / hbm_peak, "bytes_per_launch": nbytes,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+    roof["traffic"] = traffic["bytes_per_launch"] if traffic else None
+    roof["traffic_source"] = traffic["source"] if traffic else None
+    roof["kernel_ms"] = kern_avg_ms
+    roof["kernel_share_of_step"] = kern_avg_ms / ms_per_step
+    return roof
+
+
+def make_operator(tm, ctx, form, level, dirichlet=False, seed=42):
+    fid = {"P1": tm.FORM_P1, "P1K": tm.FORM_P1K, "N1": tm.FORM_N1, "P2V": tm.FORM_P2V}[form]
+    sid = tm.FORM_SPACE[fid]
+    x, y = tm.Function(ctx, sid), tm.Function(ctx, sid)
+    coeffs = []
+    if form == "N1":
+        al, be = tm.Function(ctx, tm.SPACE_P1), tm.Function(ctx, tm.SPACE_P1)
+        al.fill_coefficient(level, tm.COEFF_ALPHA)
+        be.fill_coefficient(level, tm.COEFF_BETA)
+        coeffs = [al, be]
+    elif form in ("P1K", "P2V"):
+        k = tm.Function(ctx, tm.SPACE_P1 if form == "P1K" else tm.SPACE_P2)
+        k.fill_coefficient(level, tm.COEFF_K)
+        coeffs = [k]
+    op = tm.Operator(ctx, fid, coeffs)
+    x.fill_seeded(level, seed, dirichlet)
+    y.size(level)
+    return op, x, y, coeffs
+
+
+def sub_record(tm, torch, key, steps, warmup, device, fp64_peak):
+    """One single-GPU config timed like the headline (events on the context
+    stream, kernel events, L2 flushed between steps when the inputs fit in
+    it), returned as a sub-record of the default bench line so that the
+    driver's record carries every operator's roofline, not only config 5's."""
+    cfg = CONFIGS[key]
+    level, form = cfg["level"], cfg["form"]
+    ctx = tm.Context(cfg["mesh"], device=device)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    op, x, y, _ = make_operator(tm, ctx, form, level, cfg.get("dirichlet", False))
+    nmac = ctx.num_macros()[0]
+    counts = lattice_counts(nmac, level, form)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda") \
+        if counts["elements"] < 50_000_000 else None
+    for _ in range(warmup):
+        op.apply(x, y, level)
+    torch.cuda.synchronize()
+    op.profile(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        if flush is not None:
+            flush.zero_()
+        ev[i][0].record(stream)
+        op.apply(x, y, level)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    kern_ms, kern_n = op.kernel_stats()
+    op.profile(False)
+    ms = sum(s.elapsed_time(e) for s, e in ev) / steps
+    n_unique = unique_dofs(cfg["mesh"], form, level)
+    rec = {"workload": cfg["name"], "mesh": cfg["mesh"], "level": level, "form": form, "dofs": n_unique,
+           "value": n_unique / (ms * 1e-3) / 1e9, "unit": "GDoF/s", "ms_per_step": ms, "steps": steps,
+           "l2": "inputs > 126 MB L2" if flush is None else "L2 flushed between steps",
+           "roofline": roofline(key, form, lattice_counts(nmac, level, form), kern_ms / max(kern_n, 1), ms,
+                                fp64_peak)}
+    del op, x, y, ctx
+    torch.cuda.synchronize()
+    return rec
+
+
 def run_gpu(a):
     import torch
     import torch.distributed as dist
@@ -226,6 +333,7 @@ def run_gpu(a):
         nccl_id = obj[0]
     t_setup = time.time()
     ctx = tm.Context(cfg["mesh"], device=local, rank=rank, nranks=ws, nccl_id=nccl_id)
+    comm_info = ctx.transport_info()  # "nccl rank r of N (cuda device d)": the communicator's own rank count
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     nmac_global, nmac_local = ctx.num_macros()
@@ -314,51 +422,20 @@ def run_gpu(a):
 
     # ---------------- roofline of the dominant (element) kernel
     kern_avg_ms = kern_ms / max(kern_n, 1)
-    # DRAM traffic of the dominant kernel per apply, from the committed ncu
-    # --set full capture of this configuration (None if not captured)
-    traffic = None
-    try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json"))).get(a.config)
-    except Exception:
-        pass
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    local_counts = lattice_counts(nmac_local, level, form)
-    if form in ("N1", "P2V"):
-        nd1_local = local_counts["nd1_edges"]
-        p1_local = local_counts["p1_points"]
-        flops = FLOP_PER_ELEM[form] * local_counts["elements"]
-        fp64_peak = ctx.fp64_peak(1.0) if a.fp64_peak else None
-        # N1: x, y (edges) + alpha, beta (points); P2V: x, k, y (points + edges)
-        bytes_alg = 8.0 * ((2 * nd1_local + 2 * p1_local) if form == "N1" else 3 * (nd1_local + p1_local))
-        roof = {"bound": "fp64", "achieved": flops / (kern_avg_ms * 1e-3) / 1e12,
-                "peak": fp64_peak, "unit": "TFLOP/s",
-                "traffic": traffic["bytes_per_launch"] if traffic else None,
-                "traffic_source": traffic["source"] if traffic else None,
-                "frac": (flops / (kern_avg_ms * 1e-3) / 1e12) / fp64_peak if fp64_peak else None,
-                "flop_per_launch": flops, "flop_per_element": FLOP_PER_ELEM[form],
-                "peak_source": "measured FP64 DFMA-chain probe (tetmf_measure_fp64_peak) on this GPU",
-                "hbm": {"achieved": bytes_alg / (kern_avg_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                        "bytes_per_launch": bytes_alg}}
-    else:
-        p1_local = local_counts["p1_points"]
-        nbytes = 8.0 * p1_local * (3 if form == "P1K" else 2)
-        roof = {"bound": "hbm", "achieved": nbytes / (kern_avg_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                "frac": nbytes / (kern_avg_ms * 1e-3) / 1e9 / hbm_peak,
-                "traffic": traffic["bytes_per_launch"] if traffic else None,
-                "traffic_source": traffic["source"] if traffic else None,
-                "bytes_per_launch": nbytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
-    roof["kernel_ms"] = kern_avg_ms
-    roof["kernel_share_of_step"] = kern_avg_ms / ms_per_step
+    fp64_peak = ctx.fp64_peak(1.0) if a.fp64_peak and form in ("N1", "P2V") else None
+    roof = roofline(a.config, form, lattice_counts(nmac_local, level, form), kern_avg_ms, ms_per_step, fp64_peak)
 
     # ---------------- end to end through the public API (host buffers)
     e2e = None
     if a.e2e:
         e2e = run_e2e(a, tm, torch, dist, ctx, op, x, y, level, ws, rank, n_unique, barrier)
+
+    # the other operators' rooflines at their bandwidth-bound sizes (1 GPU)
+    subs = {}
+    if a.subrecords and ws == 1 and a.config == "c5":
+        del x, y
+        for key in ("c4", "c2l", "p2v"):
+            subs[key] = sub_record(tm, torch, key, max(a.steps, 10), 3, local, fp64_peak)
 
     cpu = None
     if rank == 0 and ws == 1 and a.cpu_baseline:
@@ -377,12 +454,14 @@ def run_gpu(a):
             "data": "synthetic: x seeded uniform[-1,1] by canonical DoF key (SURVEY 8(d)); nodal coefficients (P1; P2 for P2V)",
             "config": {"workload": cfg["name"], "mesh": cfg["mesh"], "level": level, "form": form,
                        "macros": nmac_global, "dofs": n_unique, "elements": counts["elements"],
-                       "parallelism": f"macro partition over {ws} GPU(s)",
+                       "parallelism": f"macro partition over {ws} GPU(s)", "comm": comm_info,
                        "l2": "inputs > 126 MB L2" if flush is None else "L2 flushed between steps",
                        "setup_s": round(t_setup, 2)},
             "roofline": roof, "clocks": clk.summary(), "gpu_launches": launches,
             "e2e": e2e, "cpu_baseline": cpu,
         }
+        if subs:
+            out["subrecords"] = subs
         print(json.dumps(out), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -485,12 +564,40 @@ def main():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-fp64-peak", dest="fp64_peak", action="store_false")
     p.add_argument("--variant", type=int, default=0, help="kernel variant for A/B runs (0 = default)")
+    p.add_argument("--no-subrecords", dest="subrecords", action="store_false",
+                   help="c5 only: skip the c4 / c2l / p2v sub-records")
     a = p.parse_args()
     a.warmup = max(a.warmup, 3)
     if a.impl == "reference":
         run_reference_arm(a)
-    else:
-        run_gpu(a)
+        return
+    ws = int(os.environ.get("WORLD_SIZE", "0"))
+    if ws == 0 and a.gpus > 1:
+        sys.exit(launch_ranks(a))
+    if ws and ws != a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={ws}")
+    run_gpu(a)
+
+
+def launch_ranks(a) -> int:
+    """--gpus N without a launcher: re-exec this script under torchrun, one
+    rank per GPU (127.0.0.1 rendezvous). Fails loudly when fewer than N GPUs
+    are visible -- N ranks never share a device in the bench."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        print(json.dumps({"error": f"--gpus {a.gpus} requested but only {have} CUDA device(s) visible"}),
+              file=sys.stderr, flush=True)
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

@@ -6,7 +6,8 @@ K4 for rank-local interface groups, the exchange pack kernel, the transfer
 (device-to-device copies between the ranks' buffers instead of NCCL
 send/recv), the combine kernel, and the solver's scalar all-gather. The
 results must be bitwise equal to the single-rank apply (every interface sum
-runs in ascending global macro order, exchange.hpp), and within 1e-12 of the
+runs in ascending global macro order, exchange.hpp; P2V, whose cube kernels
+scatter with FP64 atomics, to 1e-13), and within 1e-12 of the
 reference's FormSystem::apply (oracle/_ref) after reassembly.
 
 Partitions: contiguous macro ranges (runtime.cpp partition_macros); cube6
@@ -85,8 +86,12 @@ def test_virtual_ranks_bitwise_equal_single_rank(tm, mesh, form, level, nranks):
         assert "loopback virtual rank" in c.transport_info()
         if not macros:
             continue
-        assert np.array_equal(y.reshape(-1, ms), y1[macros]), f"rank {c.rank}: apply differs"
-        assert np.array_equal(d.reshape(-1, ms), d1[macros]), f"rank {c.rank}: diagonal differs"
+        if form == "P2V":  # the P2V cube kernels scatter with FP64 atomics: order-dependent rounding
+            assert np.abs(y.reshape(-1, ms) - y1[macros]).max() <= 1e-13 * np.abs(y1).max(), f"rank {c.rank}"
+            assert np.abs(d.reshape(-1, ms) - d1[macros]).max() <= 1e-13 * np.abs(d1).max(), f"rank {c.rank}"
+        else:
+            assert np.array_equal(y.reshape(-1, ms), y1[macros]), f"rank {c.rank}: apply differs"
+            assert np.array_equal(d.reshape(-1, ms), d1[macros]), f"rank {c.rank}: diagonal differs"
     assert sorted(seen) == list(range(ctx1.num_macros()[0]))
 
 
