@@ -79,6 +79,14 @@ int tetmf_ctx_create(const char* mesh_desc, int device, tetmf_ctx** out);
  * nranks == 1 or planning-only contexts. */
 int tetmf_ctx_create_dist(const char* mesh_desc, int device, int rank, int nranks,
                           const void* nccl_unique_id, tetmf_ctx** out);
+/* In-memory macro mesh: the MacroMesh of FormSystem(Form, const MacroMesh&,
+ * int level) (forms.hpp:46; mesh.hpp:37-56): vertices[3 * num_vertices]
+ * (x, y, z per vertex), tets[4 * num_tets] (vertex ids; the local vertex order
+ * defines the lattice axes, as in the reference). Validated like
+ * MacroMesh::validate (mesh.cpp:76-94: ids in range, positive volumes, faces
+ * shared by at most two tets) -> TETMF_EINVAL. The arrays are copied. */
+int tetmf_ctx_create_mesh(const double* vertices, int num_vertices, const int* tets, int num_tets, int device,
+                          tetmf_ctx** out);
 /* Loopback group: nranks "virtual ranks" of ONE process on ONE device, each
  * driven by its own host thread (collective calls -- apply, dot, solvers --
  * must be made by every rank of the group). The interface exchange and the
@@ -190,6 +198,10 @@ int tetmf_op_set_variant(tetmf_op* op, int variant);
  * for d outside 0..6. */
 int tetmf_op_set_quadrature(tetmf_op* op, int degree);
 int tetmf_op_kernel_stats(tetmf_op* op, double* total_ms, int64_t* launches);
+/* Negative control ("deliberately corrupted table"): adds delta
+ * to entry `index` (flat double index over all geometry groups) of the
+ * level's per-orientation table image the element kernel reads. Test hook. */
+int tetmf_op_debug_perturb_table(tetmf_op* op, int level, int64_t index, double delta);
 /* kernels launched by this library so far (process-wide) */
 int tetmf_launch_count(int64_t* count);
 

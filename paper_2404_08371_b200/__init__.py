@@ -56,6 +56,8 @@ _SIGS = {
     "tetmf_ctx_create_dist": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_vp,
                                              ctypes.POINTER(_c_vp)]),
     "tetmf_ctx_destroy": (ctypes.c_int, [_c_vp]),
+    "tetmf_ctx_create_mesh": (ctypes.c_int, [_c_dp, ctypes.c_int, _c_ip, ctypes.c_int, ctypes.c_int,
+                                             ctypes.POINTER(_c_vp)]),
     "tetmf_loopback_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_c_vp)]),
     "tetmf_loopback_destroy": (ctypes.c_int, [_c_vp]),
     "tetmf_ctx_create_loopback": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _c_vp, ctypes.c_int,
@@ -117,6 +119,7 @@ _SIGS = {
     "tetmf_op_set_variant": (ctypes.c_int, [_c_vp, ctypes.c_int]),
     "tetmf_op_set_quadrature": (ctypes.c_int, [_c_vp, ctypes.c_int]),
     "tetmf_op_kernel_stats": (ctypes.c_int, [_c_vp, _c_dp, _c_i64p]),
+    "tetmf_op_debug_perturb_table": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int64, ctypes.c_double]),
     "tetmf_launch_count": (ctypes.c_int, [_c_i64p]),
 }
 
@@ -242,6 +245,20 @@ class Context:
         self.device = device
         self.rank = rank
         self.nranks = nranks
+
+    @classmethod
+    def from_arrays(cls, vertices, tets, device: int = 0, name: str = "in-memory") -> "Context":
+        """Context over an in-memory macro mesh (tetmf_ctx_create_mesh):
+        vertices (nv, 3) float64, tets (nt, 4) int vertex ids."""
+        v = np.ascontiguousarray(vertices, dtype=np.float64).reshape(-1, 3)
+        t = np.ascontiguousarray(tets, dtype=np.int32).reshape(-1, 4)
+        self = cls.__new__(cls)
+        h = _c_vp()
+        _check(lib().tetmf_ctx_create_mesh(v.ctypes.data_as(_c_dp), v.shape[0], t.ctypes.data_as(_c_ip), t.shape[0],
+                                           device, ctypes.byref(h)))
+        self._h = h
+        self.mesh, self.device, self.rank, self.nranks = name, device, 0, 1
+        return self
 
     @classmethod
     def loopback(cls, group: "LoopbackGroup", mesh: str, rank: int, device: int = 0) -> "Context":
@@ -509,6 +526,10 @@ class Operator:
         """degree Chebyshev-Jacobi steps towards A x = b (x updated in place)."""
         _check(lib().tetmf_chebyshev_smooth(self._h, diag.handle, b.handle, x.handle, level, degree, lambda_max,
                                             eig_ratio))
+
+    def debug_perturb_table(self, level: int, index: int, delta: float):
+        """Negative-control hook: corrupts one table entry the kernel reads."""
+        _check(lib().tetmf_op_debug_perturb_table(self._h, level, index, delta))
 
     def diagonal(self, d: Function, level: int):
         """d = diag(A) (the assembled operator's diagonal; all copies hold the sum)."""

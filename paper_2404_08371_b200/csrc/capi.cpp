@@ -106,6 +106,26 @@ int tetmf_ctx_create_dist(const char* mesh_desc, int device, int rank, int nrank
   });
 }
 
+int tetmf_ctx_create_mesh(const double* vertices, int num_vertices, const int* tets, int num_tets, int device,
+                          tetmf_ctx** out) {
+  return guard([&] {
+    need(vertices, "vertices");
+    need(tets, "tets");
+    need(out, "out");
+    if (num_vertices < 4 || num_tets < 1) fail_arg("mesh needs at least 4 vertices and 1 tetrahedron");
+    MacroMesh mesh;
+    mesh.vertices.resize(num_vertices);
+    for (int v = 0; v < num_vertices; ++v)
+      for (int r = 0; r < 3; ++r) mesh.vertices[v][r] = vertices[3 * v + r];
+    mesh.tets.resize(num_tets);
+    for (int t = 0; t < num_tets; ++t)
+      for (int i = 0; i < 4; ++i) mesh.tets[t][i] = tets[4 * t + i];
+    auto c = std::make_unique<tetmf_ctx>();
+    c->impl = std::make_unique<Context>(std::move(mesh), device, 0, 1, std::vector<int>{});
+    *out = c.release();
+  });
+}
+
 int tetmf_loopback_create(int nranks, tetmf_loopback** out) {
   return guard([&] {
     need(out, "out");
@@ -516,6 +536,13 @@ int tetmf_op_set_quadrature(tetmf_op* op, int degree) {
   return guard([&] {
     need(op, "op");
     op->impl->set_quadrature(degree);
+  });
+}
+
+int tetmf_op_debug_perturb_table(tetmf_op* op, int level, int64_t index, double delta) {
+  return guard([&] {
+    need(op, "op");
+    op->impl->debug_perturb_table(level, index, delta);
   });
 }
 

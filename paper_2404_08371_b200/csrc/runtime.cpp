@@ -74,7 +74,10 @@ std::vector<int> partition_macros(int num_macros, int rank, int nranks) {
 
 // ---------------------------------------------------------------- context
 Context::Context(const std::string& mesh_desc, int device, int rank, int nranks, std::vector<int> macros)
-    : mesh_(mesh_by_name(mesh_desc)), topo_(mesh_), device_(device), rank_(rank), nranks_(nranks) {
+    : Context(mesh_by_name(mesh_desc), device, rank, nranks, std::move(macros)) {}
+
+Context::Context(MacroMesh mesh, int device, int rank, int nranks, std::vector<int> macros)
+    : mesh_((mesh.validate(), std::move(mesh))), topo_(mesh_), device_(device), rank_(rank), nranks_(nranks) {
   if (nranks < 1 || rank < 0 || rank >= nranks) fail_arg("context: bad rank / world size");
   macros_ = macros.empty() && nranks == 1 ? partition_macros(mesh_.num_tets(), 0, 1) : std::move(macros);
   std::sort(macros_.begin(), macros_.end());
@@ -521,6 +524,33 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
   if (ev_stop) TETMF_CUDA(cudaEventRecord(ev_stop, s));
   ld.interface_sum(y, s);
   if (ld.exchange) ld.exchange->run(y, s);
+}
+
+void Operator::debug_perturb_table(int level, i64 index, double delta) {
+  auto& t = tables(level);
+  double* base = nullptr;
+  std::size_t count = 0;
+  if (form_ == Form::N1CurlCurlMass) {  // the fold kernel's Gram table
+    base = reinterpret_cast<double*>(t.n1g.get());
+    count = t.n1g.size() * sizeof(N1GramTable) / sizeof(double);
+  } else if (form_ == Form::P2VDiffusion) {
+    base = reinterpret_cast<double*>(t.p2v.get());
+    count = t.p2v.size() * sizeof(P2VTable) / sizeof(double);
+  } else {
+    base = reinterpret_cast<double*>(t.p1.get());
+    count = t.p1.size() * sizeof(P1DeviceTable) / sizeof(double);
+  }
+  if (index < 0 || static_cast<std::size_t>(index) >= count)
+    fail_arg("debug_perturb_table: index out of range (" + std::to_string(count) + " table entries)");
+  double v = 0.0;
+  const cudaStream_t s = ctx_->stream();
+  TETMF_CUDA(cudaMemcpyAsync(&v, base + index, sizeof(double), cudaMemcpyDeviceToHost, s));
+  TETMF_CUDA(cudaStreamSynchronize(s));
+  v += delta;
+  TETMF_CUDA(cudaMemcpyAsync(base + index, &v, sizeof(double), cudaMemcpyHostToDevice, s));
+  TETMF_CUDA(cudaStreamSynchronize(s));
+  if (form_ == Form::N1CurlCurlMass && !t.n1g_host.empty())
+    (&t.n1g_host[0].o[0][0])[index] += delta;  // the parameter-bank variant's host copy
 }
 
 void Operator::set_quadrature(int degree) {

@@ -76,6 +76,9 @@ class Context {
 public:
   // macros: the macro ids this rank stores (empty = all, single rank)
   Context(const std::string& mesh_desc, int device, int rank, int nranks, std::vector<int> macros);
+  // an in-memory mesh (FormSystem(Form, const MacroMesh&, int), forms.hpp:46);
+  // validated like the reference's (mesh.cpp:76-94)
+  Context(MacroMesh mesh, int device, int rank, int nranks, std::vector<int> macros);
   ~Context();
 
   const MacroMesh& mesh() const { return mesh_; }
@@ -201,6 +204,11 @@ public:
   // P1K are exact for every d; N1 is under-integrated for d <= 2, P2V for
   // d <= 3 ("U", forms.cpp:12)
   void set_quadrature(int degree);
+  // negative control: adds delta to entry `index` of the level's
+  // device table image the element kernel reads (N1 Gram table, P1 / P1K
+  // stencil + stiffness table, P2V table; all geometry groups, flat double
+  // index) -- a corrupted table must make parity fail
+  void debug_perturb_table(int level, i64 index, double delta);
   int quadrature() const { return quad_degree_; }
 
 private:

@@ -226,3 +226,40 @@ def test_parity_config5_mesh(tm, tmp_path, form, level):
     w, _ = r.apply(x, c0, c1, degree=0)
     got, _ = gpu_apply(tm, "cubes2", form, level, 0, via_import=x, coeffs_ref=(c0, c1))
     assert relerr(got, w) <= RTOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mesh,form,level,index,delta", [
+    ("cube6", "N1", 3, 24, 1e-9),    # one Gram metric entry g of orientation WU, group 0
+    ("cube6", "N1", 3, 3, 1e-6),     # one curl-curl entry Kc of orientation WU
+    ("cube6", "P1", 4, 0, 1e-9),     # the centre weight of the interior stencil
+    ("single-tet", "P1K", 3, 256 + 1, 1e-9),  # one packed stiffness entry K_o
+])
+def test_negative_control_corrupted_table(tm, mesh, form, level, index, delta):
+    """SPEC.md:599's negative control: a deliberately corrupted table entry
+    must make the parity check fail, and restoring it must make it pass --
+    the 1e-12 comparison is sensitive to the tables the kernels read."""
+    fid, sid = FORMS[form]
+    w_ref, x_ref, coeffs = ref_apply(mesh, form, level, seed=42)
+    ctx = tm.Context(mesh, device=0)
+    x, y = tm.Function(ctx, sid), tm.Function(ctx, sid)
+    cf = []
+    if form == "N1":
+        a, b = tm.Function(ctx, tm.SPACE_P1), tm.Function(ctx, tm.SPACE_P1)
+        a.fill_coefficient(level, tm.COEFF_ALPHA)
+        b.fill_coefficient(level, tm.COEFF_BETA)
+        cf = [a, b]
+    elif form == "P1K":
+        k = tm.Function(ctx, tm.SPACE_P1)
+        k.fill_coefficient(level, tm.COEFF_K)
+        cf = [k]
+    op = tm.Operator(ctx, fid, cf)
+    x.fill_seeded(level, 42)
+    op.apply(x, y, level)
+    assert relerr(y.export_ref(level), w_ref) <= RTOL
+    op.debug_perturb_table(level, index, delta)
+    op.apply(x, y, level)
+    assert relerr(y.export_ref(level), w_ref) > RTOL  # corrupted -> parity fails
+    op.debug_perturb_table(level, index, -delta)
+    op.apply(x, y, level)
+    assert relerr(y.export_ref(level), w_ref) <= RTOL  # restored -> passes again
