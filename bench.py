@@ -315,6 +315,10 @@ def run_gpu(a):
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
+    # one explicit (non-default) stream for torch's events / flushes and the
+    # library's kernels: tetmf_ctx_set_stream(NULL) would select the
+    # context's own stream, and torch's default stream handle is NULL
+    torch.cuda.set_stream(torch.cuda.Stream())
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = dict(CONFIGS[a.config])

@@ -103,7 +103,12 @@ int tetmf_ctx_create_loopback(const char* mesh_desc, int device, tetmf_loopback*
  * "loopback virtual rank r of N ...", "single rank") */
 int tetmf_ctx_transport_info(const tetmf_ctx* ctx, char* buf, int buflen);
 int tetmf_ctx_destroy(tetmf_ctx* ctx);
-int tetmf_ctx_set_stream(tetmf_ctx* ctx, void* cuda_stream); /* NULL -> own stream */
+/* All later work of the context is ordered on cuda_stream; NULL selects the
+ * context's own (non-blocking) stream again. Work queued on the previous
+ * stream is ordered before the new stream's later work (event + wait), so a
+ * switch never races with an apply still running. To use the legacy default
+ * stream pass cudaStreamLegacy ((void*)1). */
+int tetmf_ctx_set_stream(tetmf_ctx* ctx, void* cuda_stream);
 int tetmf_ctx_synchronize(tetmf_ctx* ctx);
 int tetmf_ctx_num_macros(const tetmf_ctx* ctx, int* global_count, int* local_count);
 int tetmf_ctx_local_macros(const tetmf_ctx* ctx, int* out /* local_count */);

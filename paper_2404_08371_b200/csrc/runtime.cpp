@@ -93,7 +93,18 @@ Context::Context(MacroMesh mesh, int device, int rank, int nranks, std::vector<i
 
 Context::~Context() {
   levels_.clear();
+  if (switch_event_) cudaEventDestroy(switch_event_);
   if (own_stream_) cudaStreamDestroy(own_stream_);
+}
+
+void Context::set_stream(cudaStream_t s) {
+  if (device_ < 0) fail_arg("set_stream: planning-only context has no device");
+  const cudaStream_t next = s ? s : own_stream_;
+  if (next == stream_) return;
+  if (!switch_event_) TETMF_CUDA(cudaEventCreateWithFlags(&switch_event_, cudaEventDisableTiming));
+  TETMF_CUDA(cudaEventRecord(switch_event_, stream_));
+  TETMF_CUDA(cudaStreamWaitEvent(next, switch_event_, 0));
+  stream_ = next;
 }
 
 void Context::synchronize() const {
@@ -414,8 +425,16 @@ void Operator::check(const Function& src, const Function& dst, int level) const 
     if (!c->has_level(level)) fail_arg("coefficient field has wrong space or level");
 }
 
+// The element kernels form in-macro offsets in 32 bits (row starts, class
+// offsets, stencil windows into the guard regions): one check for all of them.
+static void check_offsets_32(const LevelLayout& lay) {
+  if (lay.macro_stride + 2 * storage_guard(lay.n) >= (i64(1) << 31))
+    fail_arg("level " + std::to_string(lay.level) + ": a macro's storage exceeds the kernels' 32-bit offsets");
+}
+
 void Operator::kernel_apply(const double* x, double* y, int level) {
   auto& ld = ctx_->level(info().trial, level);
+  check_offsets_32(ld.lay);
   const int nm = static_cast<int>(ld.lay.macros.size());
   const cudaStream_t s = ctx_->stream();
   if (nm == 0) {  // a rank without macros still takes part in the exchange
@@ -572,6 +591,7 @@ void Operator::diagonal(Function& d, int level) {
   for (const Function* c : coeffs_)
     if (!c->has_level(level)) fail_arg("diagonal: coefficient function has no data at this level");
   auto& ld = ctx_->level(info().trial, level);
+  check_offsets_32(ld.lay);
   const int nm = static_cast<int>(ld.lay.macros.size());
   double* y = d.data(level);
   const cudaStream_t s = ctx_->stream();

@@ -90,7 +90,10 @@ public:
   const std::vector<int>& geometry_group() const { return group_; }  // per local macro
   int num_geometry_groups() const { return ngroups_; }
   cudaStream_t stream() const { return stream_; }
-  void set_stream(cudaStream_t s) { stream_ = s; }
+  // s == nullptr selects the context's own stream (tetmf_ctx_set_stream);
+  // work already queued on the old stream is ordered before anything the new
+  // stream runs afterwards (event record + stream wait)
+  void set_stream(cudaStream_t s);
   void synchronize() const;
 
   struct LevelData {
@@ -152,6 +155,7 @@ private:
   int ngroups_ = 0;
   cudaStream_t stream_ = nullptr;
   cudaStream_t own_stream_ = nullptr;
+  cudaEvent_t switch_event_ = nullptr;
   std::map<std::pair<int, int>, std::unique_ptr<LevelData>> levels_;
   std::shared_ptr<Transport> transport_;
 };

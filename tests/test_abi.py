@@ -300,3 +300,31 @@ def test_host_bodies(tm):
     tm.host_combine(y, np.array([2.0]), np.array([0, 2], dtype=np.int64),
                     np.array([(0 << 2), (0 << 2) | 2], dtype=np.int64))
     assert y.tolist() == [3.0, 10.0]
+
+
+@pytest.mark.gpu
+def test_set_stream_switch_orders_pending_work(tm):
+    """switching streams must order the old stream's pending work
+    before the new stream's (tetmf_ctx_set_stream records an event on the old
+    stream and makes the new one wait); NULL selects the context's own stream."""
+    import torch
+    level = 7
+    ctx = tm.Context("cube6", device=0)
+    a, b = tm.Function(ctx, tm.SPACE_ND1), tm.Function(ctx, tm.SPACE_ND1)
+    al, be = tm.Function(ctx, tm.SPACE_P1), tm.Function(ctx, tm.SPACE_P1)
+    al.fill_coefficient(level, tm.COEFF_ALPHA)
+    be.fill_coefficient(level, tm.COEFF_BETA)
+    op = tm.Operator(ctx, tm.FORM_N1, [al, be])
+    a.fill_seeded(level, 3)
+    op.apply(a, b, level)
+    ctx.synchronize()
+    want = b.download(level)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        ctx.set_stream(s1.cuda_stream)
+        op.apply(a, b, level)           # queued on s1
+        ctx.set_stream(s2.cuda_stream)  # download runs on s2: must see the finished apply
+        assert np.array_equal(b.download(level), want)
+        ctx.set_stream(None)            # back to the context's own stream
+        op.apply(a, b, level)
+        assert np.array_equal(b.download(level), want)

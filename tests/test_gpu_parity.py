@@ -263,3 +263,40 @@ def test_negative_control_corrupted_table(tm, mesh, form, level, index, delta):
     op.debug_perturb_table(level, index, -delta)
     op.apply(x, y, level)
     assert relerr(y.export_ref(level), w_ref) <= RTOL  # restored -> passes again
+
+
+@pytest.mark.gpu
+def test_apply_ref_host_batch_pinned(tm):
+    """The pinned-memory path bench.py measures: host vectors in
+    page-locked memory from tetmf_host_alloc, distinct outputs per vector,
+    nvec = 6 > the two staging buffers each way -- every w_k bitwise equal to
+    the synchronous tetmf_apply_ref_host of v_k."""
+    import ctypes
+    mesh, form, level = "cube6", "N1", 4
+    fid, sid = FORMS[form]
+    ctx = tm.Context(mesh, device=0)
+    src, dst = tm.Function(ctx, sid), tm.Function(ctx, sid)
+    a, b = tm.Function(ctx, tm.SPACE_P1), tm.Function(ctx, tm.SPACE_P1)
+    a.fill_coefficient(level, tm.COEFF_ALPHA)
+    b.fill_coefficient(level, tm.COEFF_BETA)
+    op = tm.Operator(ctx, fid, [a, b])
+    nd = src.num_ref_dofs(level)
+    nvec = 6
+    hv = [tm.host_alloc(8 * nd) for _ in range(nvec)]
+    hw = [tm.host_alloc(8 * nd) for _ in range(nvec)]
+    try:
+        view = lambda p: np.ctypeslib.as_array(ctypes.cast(ctypes.c_void_p(p), ctypes.POINTER(ctypes.c_double)),
+                                               shape=(nd,))
+        rng = np.random.default_rng(11)
+        for p in hv:
+            view(p)[:] = rng.uniform(-1.0, 1.0, nd)
+        for p in hw:
+            view(p)[:] = np.nan
+        op.apply_ref_host_batch(src, dst, level, hv, hw)
+        for p, q in zip(hv, hw):
+            one = np.zeros(nd)
+            op.apply_ref_host(src, dst, level, view(p).copy(), one)
+            assert np.array_equal(view(q), one)
+    finally:
+        for p in hv + hw:
+            tm.host_free(p)
