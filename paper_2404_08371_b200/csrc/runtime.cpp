@@ -147,28 +147,12 @@ Context::LevelData& Context::level(Space s, int level) {
       if (rank_of[m] != rank_) fail_arg("context: multi-rank contexts use the default partition");
   }
   if (s == Space::P1) {
+    // the default K1 kernel's task list (the A/B variants' lists are built on
+    // first use, ensure_p1_variant_tasks) and K2's
     std::vector<int> tasks;
-    build_stencil2_tasks(static_cast<int>(macros_.size()), n, tasks);
-    ld->ntasks = static_cast<int>(tasks.size() / 4);
-    ld->tasks.upload(tasks.data(), tasks.size(), stream_);
-    build_stencil_tile_tasks(static_cast<int>(macros_.size()), n, tasks);
-    ld->ntasks4 = static_cast<int>(tasks.size() / 4);
-    ld->tasks4.upload(tasks.data(), tasks.size(), stream_);
-    build_stencil_tma_tasks(static_cast<int>(macros_.size()), n, tasks);
-    ld->ntasks3 = static_cast<int>(tasks.size() / 4);
-    ld->tasks3.upload(tasks.data(), tasks.size(), stream_);
-    build_stencil7_tasks(static_cast<int>(macros_.size()), n, tasks);
-    ld->ntasks7 = static_cast<int>(tasks.size() / 4);
-    ld->tasks7.upload(tasks.data(), tasks.size(), stream_);
     build_stencil6_tasks(static_cast<int>(macros_.size()), n, tasks);
     ld->ntasks6 = static_cast<int>(tasks.size() / 4);
     ld->tasks6.upload(tasks.data(), tasks.size(), stream_);
-    build_stencil5_tasks(static_cast<int>(macros_.size()), n, tasks);
-    ld->ntasks5 = static_cast<int>(tasks.size() / 4);
-    ld->tasks5.upload(tasks.data(), tasks.size(), stream_);
-    build_stencil_tasks(static_cast<int>(macros_.size()), n, tasks);
-    ld->ntasks2 = static_cast<int>(tasks.size() / 4);
-    ld->tasks2.upload(tasks.data(), tasks.size(), stream_);
     build_p1k_tasks(static_cast<int>(macros_.size()), n, tasks);
     ld->np1k_tasks = static_cast<int>(tasks.size() / 4);
     ld->p1k_tasks.upload(tasks.data(), tasks.size(), stream_);
@@ -255,6 +239,31 @@ Context::LevelData& Context::level(Space s, int level) {
   auto& ref = *ld;
   levels_.emplace(key, std::move(ld));
   return ref;
+}
+
+void Context::ensure_p1_variant_tasks(LevelData& ld) {
+  if (ld.variant_tasks_built) return;
+  const int nm = static_cast<int>(macros_.size()), n = ld.lay.n;
+  std::vector<int> tasks;
+  build_stencil2_tasks(nm, n, tasks);
+  ld.ntasks = static_cast<int>(tasks.size() / 4);
+  ld.tasks.upload(tasks.data(), tasks.size(), stream_);
+  build_stencil_tile_tasks(nm, n, tasks);
+  ld.ntasks4 = static_cast<int>(tasks.size() / 4);
+  ld.tasks4.upload(tasks.data(), tasks.size(), stream_);
+  build_stencil_tma_tasks(nm, n, tasks);
+  ld.ntasks3 = static_cast<int>(tasks.size() / 4);
+  ld.tasks3.upload(tasks.data(), tasks.size(), stream_);
+  build_stencil7_tasks(nm, n, tasks);
+  ld.ntasks7 = static_cast<int>(tasks.size() / 4);
+  ld.tasks7.upload(tasks.data(), tasks.size(), stream_);
+  build_stencil5_tasks(nm, n, tasks);
+  ld.ntasks5 = static_cast<int>(tasks.size() / 4);
+  ld.tasks5.upload(tasks.data(), tasks.size(), stream_);
+  build_stencil_tasks(nm, n, tasks);
+  ld.ntasks2 = static_cast<int>(tasks.size() / 4);
+  ld.tasks2.upload(tasks.data(), tasks.size(), stream_);
+  ld.variant_tasks_built = true;
 }
 
 Context::LevelData& Context::ref_level(Space s, int level) {
@@ -454,6 +463,7 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
     ev_stop = events_[events_used_].second;
     ++events_used_;
   }
+  if (form_ == Form::P1Diffusion && kernel_variant_ >= 2) ctx_->ensure_p1_variant_tasks(ld);
   switch (form_) {
     case Form::P1Diffusion:
       if (kernel_variant_ == 1)

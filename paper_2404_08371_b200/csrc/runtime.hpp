@@ -126,6 +126,7 @@ public:
     int ntasks7 = 0;
     DeviceBuffer<int> tasks4;           // P1: register-tile tasks (variant 4)
     int ntasks4 = 0;
+    bool variant_tasks_built = false;   // P1: the A/B variants' lists (built on first use)
     DeviceBuffer<int> p1k_tasks;        // P1: row tasks of the P1K gather kernel (K2)
     int np1k_tasks = 0;
     // solver (solver.hpp): per local macro, [support mask] -> {bit 0 interior,
@@ -141,6 +142,7 @@ public:
   };
   LevelData& level(Space s, int level);
   LevelData& ref_level(Space s, int level);  // level() + reference numbering
+  void ensure_p1_variant_tasks(LevelData& ld);  // K1 A/B variants' task lists
 
   // NCCL (one process per GPU) or loopback (virtual ranks on one GPU)
   void attach_transport(std::shared_ptr<Transport> t) { transport_ = std::move(t); }
