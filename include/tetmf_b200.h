@@ -79,6 +79,16 @@ int tetmf_ctx_create(const char* mesh_desc, int device, tetmf_ctx** out);
  * nranks == 1 or planning-only contexts. */
 int tetmf_ctx_create_dist(const char* mesh_desc, int device, int rank, int nranks,
                           const void* nccl_unique_id, tetmf_ctx** out);
+/* partitions of the macro mesh over ranks:
+ * MACRO  whole macros, contiguous by id (every form);
+ * SLAB   (macro, z-slab) units of the P1 lattice points, cuts on multiples of
+ *        8 planes, balanced point counts, every rank stores every macro and
+ *        computes y on its units only (x read on ghost planes from its own
+ *        copy) -- the strong-scaling partition of config 4; P1 -Laplace
+ *        apply only (TETMF_EINVAL for other forms, dot and solvers). */
+enum { TETMF_PARTITION_MACRO = 0, TETMF_PARTITION_SLAB = 1 };
+int tetmf_ctx_create_dist_part(const char* mesh_desc, int device, int rank, int nranks,
+                               const void* nccl_unique_id, int partition, tetmf_ctx** out);
 /* In-memory macro mesh: the MacroMesh of FormSystem(Form, const MacroMesh&,
  * int level) (forms.hpp:46; mesh.hpp:37-56): vertices[3 * num_vertices]
  * (x, y, z per vertex), tets[4 * num_tets] (vertex ids; the local vertex order
@@ -98,7 +108,8 @@ int tetmf_ctx_create_mesh(const double* vertices, int num_vertices, const int* t
  * single-device test mode of the multi-rank apply. */
 int tetmf_loopback_create(int nranks, tetmf_loopback** out);
 int tetmf_loopback_destroy(tetmf_loopback* group);
-int tetmf_ctx_create_loopback(const char* mesh_desc, int device, tetmf_loopback* group, int rank, tetmf_ctx** out);
+int tetmf_ctx_create_loopback(const char* mesh_desc, int device, tetmf_loopback* group, int rank, int partition,
+                              tetmf_ctx** out);
 /* one line describing the context's transport ("nccl rank r of N ...",
  * "loopback virtual rank r of N ...", "single rank") */
 int tetmf_ctx_transport_info(const tetmf_ctx* ctx, char* buf, int buflen);
@@ -230,6 +241,9 @@ int tetmf_plan_exchange(tetmf_ctx* ctx, int space, int level, int* npeers, int64
                         int64_t* ngroups, int64_t* nentries, int* peers, int64_t* send_offsets,
                         int64_t* recv_offsets, int64_t* send_index, int64_t* group_offsets,
                         int64_t* group_entries);
+/* slab partition (TETMF_PARTITION_SLAB) of a mesh with num_macros macros at
+ * a level: rank's units as (macro, za, zb) triples, planes za <= z < zb */
+int tetmf_plan_slab_units(int num_macros, int level, int nranks, int rank, int* nunits, int* units);
 /* the product's pack / combine / local-sum bodies run on host arrays */
 int tetmf_host_local_sum(const int64_t* offsets, const int64_t* copies, int64_t ngroups, double* y);
 int tetmf_host_pack(const double* y, const int64_t* send_index, int64_t nsend, double* send);

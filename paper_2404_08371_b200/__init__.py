@@ -30,6 +30,7 @@ COEFF_ALPHA, COEFF_BETA, COEFF_K, COEFF_CONST = 0, 1, 2, 3
 FORM_SPACE = {FORM_P1: SPACE_P1, FORM_P1K: SPACE_P1, FORM_N1: SPACE_ND1, FORM_P2V: SPACE_P2}
 
 EINVAL, EINTERNAL, EDEVICE, ECOMM = 1, 2, 3, 4
+PARTITION_MACRO, PARTITION_SLAB = 0, 1
 
 
 class TetmfError(RuntimeError):
@@ -60,8 +61,10 @@ _SIGS = {
                                              ctypes.POINTER(_c_vp)]),
     "tetmf_loopback_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_c_vp)]),
     "tetmf_loopback_destroy": (ctypes.c_int, [_c_vp]),
-    "tetmf_ctx_create_loopback": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _c_vp, ctypes.c_int,
+    "tetmf_ctx_create_loopback": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _c_vp, ctypes.c_int, ctypes.c_int,
                                                  ctypes.POINTER(_c_vp)]),
+    "tetmf_ctx_create_dist_part": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_vp,
+                                                  ctypes.c_int, ctypes.POINTER(_c_vp)]),
     "tetmf_ctx_transport_info": (ctypes.c_int, [_c_vp, ctypes.c_char_p, ctypes.c_int]),
     "tetmf_ctx_set_stream": (ctypes.c_int, [_c_vp, _c_vp]),
     "tetmf_ctx_synchronize": (ctypes.c_int, [_c_vp]),
@@ -97,6 +100,7 @@ _SIGS = {
     "tetmf_plan_exchange": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, _c_ip, _c_i64p, _c_i64p, _c_i64p,
                                            _c_i64p, _c_ip, _c_i64p, _c_i64p, _c_i64p, _c_i64p, _c_i64p]),
     "tetmf_host_local_sum": (ctypes.c_int, [_c_i64p, _c_i64p, ctypes.c_int64, _c_dp]),
+    "tetmf_plan_slab_units": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_ip, _c_ip]),
     "tetmf_host_pack": (ctypes.c_int, [_c_dp, _c_i64p, ctypes.c_int64, _c_dp]),
     "tetmf_host_combine": (ctypes.c_int, [_c_dp, _c_dp, _c_i64p, _c_i64p, ctypes.c_int64]),
     "tetmf_measure_fp64_peak": (ctypes.c_int, [_c_vp, ctypes.c_double, _c_dp]),
@@ -122,6 +126,15 @@ _SIGS = {
     "tetmf_op_debug_perturb_table": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int64, ctypes.c_double]),
     "tetmf_launch_count": (ctypes.c_int, [_c_i64p]),
 }
+
+
+def slab_units(num_macros: int, level: int, nranks: int, rank: int) -> list[tuple[int, int, int]]:
+    """(macro, za, zb) units of `rank` in the slab partition (planes za <= z < zb)."""
+    n = ctypes.c_int()
+    _check(lib().tetmf_plan_slab_units(num_macros, level, nranks, rank, ctypes.byref(n), None))
+    buf = (ctypes.c_int * max(3 * n.value, 1))()
+    _check(lib().tetmf_plan_slab_units(num_macros, level, nranks, rank, ctypes.byref(n), buf))
+    return [tuple(buf[3 * i:3 * i + 3]) for i in range(n.value)]
 
 
 def launch_count() -> int:
@@ -191,8 +204,8 @@ class LoopbackGroup:
     def handle(self):
         return self._h
 
-    def contexts(self, mesh: str, device: int = 0) -> list["Context"]:
-        return [Context.loopback(self, mesh, r, device) for r in range(self.nranks)]
+    def contexts(self, mesh: str, device: int = 0, partition: int = PARTITION_MACRO) -> list["Context"]:
+        return [Context.loopback(self, mesh, r, device, partition) for r in range(self.nranks)]
 
     def close(self):
         if getattr(self, "_h", None):
@@ -234,12 +247,12 @@ class Context:
     """Mesh + topology + device + rank partition (FormSystem's inputs)."""
 
     def __init__(self, mesh: str, device: int = 0, rank: int = 0, nranks: int = 1,
-                 nccl_id: Optional[bytes] = None):
+                 nccl_id: Optional[bytes] = None, partition: int = PARTITION_MACRO):
         h = _c_vp()
         idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
-        _check(lib().tetmf_ctx_create_dist(mesh.encode(), device, rank, nranks,
-                                           ctypes.cast(idbuf, _c_vp) if idbuf is not None else None,
-                                           ctypes.byref(h)))
+        _check(lib().tetmf_ctx_create_dist_part(mesh.encode(), device, rank, nranks,
+                                                ctypes.cast(idbuf, _c_vp) if idbuf is not None else None,
+                                                partition, ctypes.byref(h)))
         self._h = h
         self.mesh = mesh
         self.device = device
@@ -261,11 +274,13 @@ class Context:
         return self
 
     @classmethod
-    def loopback(cls, group: "LoopbackGroup", mesh: str, rank: int, device: int = 0) -> "Context":
+    def loopback(cls, group: "LoopbackGroup", mesh: str, rank: int, device: int = 0,
+                 partition: int = PARTITION_MACRO) -> "Context":
         """Virtual rank `rank` of a loopback group (tetmf_ctx_create_loopback)."""
         self = cls.__new__(cls)
         h = _c_vp()
-        _check(lib().tetmf_ctx_create_loopback(mesh.encode(), device, group.handle, rank, ctypes.byref(h)))
+        _check(lib().tetmf_ctx_create_loopback(mesh.encode(), device, group.handle, rank, partition,
+                                               ctypes.byref(h)))
         self._h = h
         self.mesh, self.device, self.rank, self.nranks = mesh, device, rank, group.nranks
         self._group = group  # keeps the group alive as long as its contexts

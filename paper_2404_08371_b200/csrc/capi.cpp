@@ -91,13 +91,18 @@ int tetmf_ctx_create(const char* mesh_desc, int device, tetmf_ctx** out) {
 
 int tetmf_ctx_create_dist(const char* mesh_desc, int device, int rank, int nranks, const void* nccl_unique_id,
                           tetmf_ctx** out) {
+  return tetmf_ctx_create_dist_part(mesh_desc, device, rank, nranks, nccl_unique_id, TETMF_PARTITION_MACRO, out);
+}
+
+int tetmf_ctx_create_dist_part(const char* mesh_desc, int device, int rank, int nranks, const void* nccl_unique_id,
+                               int partition, tetmf_ctx** out) {
   return guard([&] {
     need(mesh_desc, "mesh_desc");
     need(out, "out");
     if (nranks < 1 || rank < 0 || rank >= nranks) fail_arg("bad rank / world size");
     auto c = std::make_unique<tetmf_ctx>();
     const int nm = mesh_by_name(mesh_desc).num_tets();
-    c->impl = std::make_unique<Context>(mesh_desc, device, rank, nranks, partition_macros(nm, rank, nranks));
+    c->impl = std::make_unique<Context>(mesh_desc, device, rank, nranks, partition_macros(nm, rank, nranks), partition);
     if (nranks > 1 && device >= 0) {
       need(nccl_unique_id, "nccl_unique_id");
       c->impl->attach_transport(make_nccl_transport(nranks, nccl_unique_id, rank));
@@ -140,7 +145,8 @@ int tetmf_loopback_destroy(tetmf_loopback* g) {
   return guard([&] { delete g; });
 }
 
-int tetmf_ctx_create_loopback(const char* mesh_desc, int device, tetmf_loopback* group, int rank, tetmf_ctx** out) {
+int tetmf_ctx_create_loopback(const char* mesh_desc, int device, tetmf_loopback* group, int rank, int partition,
+                              tetmf_ctx** out) {
   return guard([&] {
     need(mesh_desc, "mesh_desc");
     need(group, "group");
@@ -150,7 +156,7 @@ int tetmf_ctx_create_loopback(const char* mesh_desc, int device, tetmf_loopback*
     if (rank < 0 || rank >= nranks) fail_arg("bad rank / world size");
     auto c = std::make_unique<tetmf_ctx>();
     const int nm = mesh_by_name(mesh_desc).num_tets();
-    c->impl = std::make_unique<Context>(mesh_desc, device, rank, nranks, partition_macros(nm, rank, nranks));
+    c->impl = std::make_unique<Context>(mesh_desc, device, rank, nranks, partition_macros(nm, rank, nranks), partition);
     if (nranks > 1) c->impl->attach_transport(make_loopback_transport(group->hub, rank));
     *out = c.release();
   });
@@ -624,7 +630,10 @@ int tetmf_plan_local_groups(tetmf_ctx* ctx, int space, int level, int64_t* ngrou
     need(ctx, "ctx");
     const Context& c = *ctx->impl;
     const auto lay = LevelLayout::make(space_of(space), level, c.mesh().num_tets(), c.macros());
-    const auto g = local_groups_only(c.mesh(), c.topo(), lay, rank_of(c), c.rank());
+    const auto g = c.partition() == Context::kPartitionSlab
+                       ? local_groups_slab(c.mesh(), c.topo(), lay, slab_partition(c.mesh().num_tets(), lay.n,
+                                                                                     c.nranks()), c.rank())
+                       : local_groups_only(c.mesh(), c.topo(), lay, rank_of(c), c.rank());
     if (ngroups) *ngroups = g.num_groups();
     if (ncopies) *ncopies = static_cast<int64_t>(g.copies.size());
     if (offsets) std::memcpy(offsets, g.offsets.data(), g.offsets.size() * sizeof(int64_t));
@@ -640,7 +649,10 @@ int tetmf_plan_exchange(tetmf_ctx* ctx, int space, int level, int* npeers, int64
     need(ctx, "ctx");
     const Context& c = *ctx->impl;
     const auto lay = LevelLayout::make(space_of(space), level, c.mesh().num_tets(), c.macros());
-    const auto p = build_exchange_plan(c.mesh(), c.topo(), lay, rank_of(c), c.rank());
+    const auto p = c.partition() == Context::kPartitionSlab
+                       ? build_exchange_plan_slab(c.mesh(), c.topo(), lay,
+                                                  slab_partition(c.mesh().num_tets(), lay.n, c.nranks()), c.rank())
+                       : build_exchange_plan(c.mesh(), c.topo(), lay, rank_of(c), c.rank());
     if (npeers) *npeers = static_cast<int>(p.peers.size());
     if (nsend) *nsend = p.send_total();
     if (nrecv) *nrecv = p.recv_total();
@@ -655,6 +667,22 @@ int tetmf_plan_exchange(tetmf_ctx* ctx, int space, int level, int* npeers, int64
     cp(send_index, p.send_index);
     cp(group_offsets, p.group_offsets);
     cp(group_entries, p.group_entries);
+  });
+}
+
+int tetmf_plan_slab_units(int num_macros, int level, int nranks, int rank, int* nunits, int* units) {
+  return guard([&] {
+    need(nunits, "nunits");
+    if (level < 0 || level > 14) fail_arg("level out of range");
+    const auto all = slab_partition(num_macros, 1 << level, nranks);
+    if (rank < 0 || rank >= nranks) fail_arg("bad rank / world size");
+    *nunits = static_cast<int>(all[rank].size());
+    if (units)
+      for (std::size_t i = 0; i < all[rank].size(); ++i) {
+        units[3 * i] = all[rank][i].macro;
+        units[3 * i + 1] = all[rank][i].za;
+        units[3 * i + 2] = all[rank][i].zb;
+      }
   });
 }
 

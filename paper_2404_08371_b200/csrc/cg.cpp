@@ -28,6 +28,8 @@ SlotSpace slot_space(const Context::LevelData& ld) {
 double masked_dot(const Function& a, const Function& b, int level) {
   if (a.space() != b.space() || &a.ctx() != &b.ctx()) fail_arg("dot: functions of different spaces / contexts");
   Context& ctx = a.ctx();
+  if (ctx.partition() == Context::kPartitionSlab)
+    fail_arg("dot / solvers: slab partitions hold unowned macro storage (apply only)");
   auto& ld = ctx.level(a.space(), level);
   const cudaStream_t s = ctx.stream();
   double* scratch = ld.dot_scratch.get();

@@ -65,8 +65,11 @@ void launch_p1_stencil5(const double* x, double* y, const int* d_tasks, int ntas
                         int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
 // K1 variant 6: shared-memory boxes filled by per-row TMA bulk copies (k_p1_stencil5.cu)
 void build_stencil6_tasks(int nmacros, int n, std::vector<int>& out);
+// zrange (optional, slab partition): per local macro {za, zb}, the planes this
+// rank computes (the task list holds only boxes of those planes)
 void launch_p1_stencil6(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
-                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
+                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s,
+                        const int* zrange = nullptr);
 // K1 variant 7: persistent double-buffered shared-memory boxes (k_p1_stencil5.cu)
 void build_stencil7_tasks(int nmacros, int n, std::vector<int>& out);
 void launch_p1_stencil7(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,

@@ -53,6 +53,29 @@ ExchangePlan build_exchange_plan(const MacroMesh& mesh, const Topology& topo, co
 InterfaceGroups local_groups_only(const MacroMesh& mesh, const Topology& topo, const LevelLayout& lay,
                                   const std::vector<int>& rank_of, int rank);
 
+// ---- (macro, z-slab) partition (SURVEY.md 8(e), config 4 strong scaling).
+// A unit is a range of lattice planes [za, zb) of one macro; rank r computes
+// y at the P1 points of its units (the stencil kernel needs x of the ghost
+// planes za - 1 and zb, read from the rank's own copy). Cuts lie on multiples
+// of the K1 box height (8 planes); units are contiguous in (macro, plane)
+// order with balanced point counts. Every rank stores every macro (the
+// storage outside its units is not computed).
+struct SlabUnit {
+  int macro, za, zb;
+};
+constexpr int kSlabAlign = 8;  // K1 box planes (k_p1_stencil5.cu kBoxPlanes6)
+// all ranks' units: result[r] = the units of rank r (ascending macro)
+std::vector<std::vector<SlabUnit>> slab_partition(int num_macros, int n, int nranks);
+// rank computing the P1 point of plane z in macro m
+int slab_rank(const std::vector<std::vector<SlabUnit>>& units, int macro, int z);
+
+// Exchange plan and rank-local groups when every rank stores every macro and
+// each copy belongs to copy_rank(macro, z) (slab partition)
+ExchangePlan build_exchange_plan_slab(const MacroMesh& mesh, const Topology& topo, const LevelLayout& lay,
+                                      const std::vector<std::vector<SlabUnit>>& units, int rank);
+InterfaceGroups local_groups_slab(const MacroMesh& mesh, const Topology& topo, const LevelLayout& lay,
+                                  const std::vector<std::vector<SlabUnit>>& units, int rank);
+
 // signed_values = false: orientation signs ignored (operator diagonals)
 TM_HD void exchange_pack_one(const double* y, const i64* send_index, double* send, i64 i,
                              bool signed_values = true) {

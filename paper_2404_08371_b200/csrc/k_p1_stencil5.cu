@@ -121,7 +121,8 @@ __device__ __forceinline__ double gather_point(const double* __restrict__ X, con
 // S(b) = b(2n+3-b)/2); x = a, and y (f = 0) or z (f = 1) = b.
 __device__ __forceinline__ void face_point(const double* __restrict__ xin, double* __restrict__ yout, i64 stride,
                                            int n, const P1DeviceTable* __restrict__ tabs,
-                                           const MacroDesc* __restrict__ macros, int li, int f, int q) {
+                                           const MacroDesc* __restrict__ macros, int li, int f, int q,
+                                           const int2* __restrict__ zrange = nullptr) {
   const float c = 2.0f * n + 3.0f;
   int b = static_cast<int>((c - sqrtf(fmaxf(c * c - 8.0f * q, 0.0f))) * 0.5f);
   b = min(max(b, 0), n);
@@ -130,6 +131,7 @@ __device__ __forceinline__ void face_point(const double* __restrict__ xin, doubl
   const int a = q - b * (2 * n + 3 - b) / 2;
   const int x = a, y = f == 0 ? b : 0, z = f == 0 ? 0 : b;
   if (f == 1 && z == 0) return;  // on the z = 0 face
+  if (zrange && (z < zrange[li].x || z >= zrange[li].y)) return;  // slab partition: another rank's plane
   const int type = (x == 0 ? 1 : 0) | (y == 0 ? 2 : 0) | (z == 0 ? 4 : 0) | (x + y + z == n ? 8 : 0);
   const double* __restrict__ X = xin + static_cast<i64>(li) * stride;
   const double* __restrict__ wt = &tabs[macros[li].group].stencil[type][0];
@@ -563,7 +565,7 @@ __global__ void __launch_bounds__(32 * kWarps6)
 #endif
 p1_box_kernel(const double* __restrict__ xin, double* __restrict__ yout, const Task5* __restrict__ tasks, int ntasks,
               int nboxctas, int nmacros, i64 stride, int n, const P1DeviceTable* __restrict__ tabs,
-              const MacroDesc* __restrict__ macros) {
+              const MacroDesc* __restrict__ macros, const int2* __restrict__ zrange) {
   if (static_cast<int>(blockIdx.x) >= nboxctas) {
     // face CTAs after the boxes (same launch, they fill the tail): faces z = 0
     // and y = 0 of every macro, one point per thread
@@ -571,7 +573,7 @@ p1_box_kernel(const double* __restrict__ xin, double* __restrict__ yout, const T
     const int gid = (static_cast<int>(blockIdx.x) - nboxctas) * static_cast<int>(blockDim.x) + static_cast<int>(threadIdx.x);
     const int li = gid / (2 * T), rem = gid - li * 2 * T;
     if (li < nmacros)
-      face_point(xin, yout, stride, n, tabs, macros, li, rem >= T ? 1 : 0, rem >= T ? rem - T : rem);
+      face_point(xin, yout, stride, n, tabs, macros, li, rem >= T ? 1 : 0, rem >= T ? rem - T : rem, zrange);
     return;
   }
   extern __shared__ __align__(128) double sm[];
@@ -898,8 +900,9 @@ void build_stencil6_tasks(int nmacros, int n, std::vector<int>& out) {
 
 template <bool kPersistent>
 static void launch_p1_box(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
-                          int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
-  if (ntasks == 0) return;
+                          int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s,
+                          const int* zrange = nullptr) {
+  if (ntasks == 0 && !zrange) return;
   if (tet_count(n) + n + 96 >= (i64(1) << 31)) fail_arg("p1 box kernel: level too large for 32-bit lattice offsets");
   // per stage: the box rows + a margin (in slab mode lanes past the short rows
   // read up to a segment beyond the last plane's stretch; never stored)
@@ -919,13 +922,15 @@ static void launch_p1_box(const double* x, double* y, const int* d_tasks, int nt
   const int T = (n + 1) * (n + 2) / 2;
   const int face_ctas = (2 * T * nmacros + 32 * kWarps6 - 1) / (32 * kWarps6);
   p1_box_kernel<kPersistent><<<static_cast<unsigned>(nbox + face_ctas), 32 * kWarps6, smem, s>>>(
-      x, y, reinterpret_cast<const Task5*>(d_tasks), ntasks, nbox, nmacros, macro_stride, n, d_tables, d_macros);
+      x, y, reinterpret_cast<const Task5*>(d_tasks), ntasks, nbox, nmacros, macro_stride, n, d_tables, d_macros,
+      reinterpret_cast<const int2*>(zrange));
   check_launch("p1_box");
 }
 
 void launch_p1_stencil6(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
-                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
-  launch_p1_box<false>(x, y, d_tasks, ntasks, macro_stride, n, nmacros, d_tables, d_macros, s);
+                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s,
+                        const int* zrange) {
+  launch_p1_box<false>(x, y, d_tasks, ntasks, macro_stride, n, nmacros, d_tables, d_macros, s, zrange);
 }
 
 void launch_p1_stencil10(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,

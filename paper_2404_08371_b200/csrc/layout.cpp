@@ -331,7 +331,7 @@ std::vector<SharedCarrier> shared_carriers(const MacroMesh& mesh, const Topology
                        const int o = topo.owner(m, mask);
                        const Mapped mp = o == m ? Mapped{a[0], a[1], a[2], cls, slot, false}
                                                 : map_carrier(mesh, lay, m, cls, a, o);
-                       out.push_back({o, mp.slot, m, baseIdx + slot, mp.flipped, mask});
+                       out.push_back({o, mp.slot, m, baseIdx + slot, mp.flipped, mask, a[2]});
                      });
     });
   }

@@ -129,6 +129,7 @@ struct SharedCarrier {
   i64 index;      // storage index in the local function
   bool negative;  // sign relative to the owner orientation
   unsigned mask;  // support mask in the holding macro (sharers: topo.sharers[macro][mask])
+  int z;          // base point (P1) / anchor (ND1) plane in the holding macro
 };
 std::vector<SharedCarrier> shared_carriers(const MacroMesh& mesh, const Topology& topo, const LevelLayout& lay);
 

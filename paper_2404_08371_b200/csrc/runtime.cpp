@@ -73,13 +73,18 @@ std::vector<int> partition_macros(int num_macros, int rank, int nranks) {
 }
 
 // ---------------------------------------------------------------- context
-Context::Context(const std::string& mesh_desc, int device, int rank, int nranks, std::vector<int> macros)
-    : Context(mesh_by_name(mesh_desc), device, rank, nranks, std::move(macros)) {}
+Context::Context(const std::string& mesh_desc, int device, int rank, int nranks, std::vector<int> macros,
+                 int partition)
+    : Context(mesh_by_name(mesh_desc), device, rank, nranks, std::move(macros), partition) {}
 
-Context::Context(MacroMesh mesh, int device, int rank, int nranks, std::vector<int> macros)
-    : mesh_((mesh.validate(), std::move(mesh))), topo_(mesh_), device_(device), rank_(rank), nranks_(nranks) {
+Context::Context(MacroMesh mesh, int device, int rank, int nranks, std::vector<int> macros, int partition)
+    : mesh_((mesh.validate(), std::move(mesh))), topo_(mesh_), device_(device), rank_(rank), nranks_(nranks),
+      partition_(partition) {
   if (nranks < 1 || rank < 0 || rank >= nranks) fail_arg("context: bad rank / world size");
-  macros_ = macros.empty() && nranks == 1 ? partition_macros(mesh_.num_tets(), 0, 1) : std::move(macros);
+  if (partition != kPartitionMacro && partition != kPartitionSlab) fail_arg("context: unknown partition");
+  if (partition == kPartitionSlab) macros.clear();  // slab partition: every rank stores every macro
+  macros_ = macros.empty() && (nranks == 1 || partition == kPartitionSlab) ? partition_macros(mesh_.num_tets(), 0, 1)
+                                                                           : std::move(macros);
   std::sort(macros_.begin(), macros_.end());
   for (int m : macros_)
     if (m < 0 || m >= mesh_.num_tets()) fail_arg("context: macro id out of range");
@@ -137,8 +142,10 @@ Context::LevelData& Context::level(Space s, int level) {
     }
   }
   ld->macros.upload(descs.data(), descs.size(), stream_);
+  if (partition_ == kPartitionSlab && s != Space::P1)
+    fail_arg("slab partition: P1 functions only (the P1 -Laplace stencil apply, config 4)");
   std::vector<int> rank_of(mesh_.num_tets(), -1);
-  if (nranks_ == 1) {
+  if (nranks_ == 1 || partition_ == kPartitionSlab) {
     std::fill(rank_of.begin(), rank_of.end(), 0);
   } else {
     for (int r = 0; r < nranks_; ++r)
@@ -151,6 +158,21 @@ Context::LevelData& Context::level(Space s, int level) {
     // first use, ensure_p1_variant_tasks) and K2's
     std::vector<int> tasks;
     build_stencil6_tasks(static_cast<int>(macros_.size()), n, tasks);
+    if (partition_ == kPartitionSlab) {
+      // keep the boxes of this rank's planes (box heights divide the cuts)
+      const auto units = slab_partition(mesh_.num_tets(), n, nranks_);
+      std::vector<int> zr(2 * macros_.size(), 0), kept;
+      for (const SlabUnit& u : units[rank_]) {
+        zr[2 * u.macro] = u.za;
+        zr[2 * u.macro + 1] = u.zb;
+      }
+      for (std::size_t t = 0; t < tasks.size(); t += 4) {
+        const int li = tasks[t], z0 = tasks[t + 1];
+        if (z0 >= zr[2 * li] && z0 < zr[2 * li + 1]) kept.insert(kept.end(), tasks.begin() + t, tasks.begin() + t + 4);
+      }
+      tasks.swap(kept);
+      ld->zrange.upload(zr.data(), zr.size(), stream_);
+    }
     ld->ntasks6 = static_cast<int>(tasks.size() / 4);
     ld->tasks6.upload(tasks.data(), tasks.size(), stream_);
     build_p1k_tasks(static_cast<int>(macros_.size()), n, tasks);
@@ -209,7 +231,10 @@ Context::LevelData& Context::level(Space s, int level) {
     ld->slot_table.upload(table.data(), table.size(), stream_);
     ld->dot_scratch.reset(static_cast<std::size_t>(masked_dot_partials() + 2 * (nranks_ + 1)));
   }
-  ld->groups = local_groups_only(mesh_, topo_, ld->lay, rank_of, rank_);
+  std::vector<std::vector<SlabUnit>> units;
+  if (partition_ == kPartitionSlab) units = slab_partition(mesh_.num_tets(), n, nranks_);
+  ld->groups = partition_ == kPartitionSlab ? local_groups_slab(mesh_, topo_, ld->lay, units, rank_)
+                                            : local_groups_only(mesh_, topo_, ld->lay, rank_of, rank_);
   ld->group_offsets.upload(ld->groups.offsets.data(), ld->groups.offsets.size(), stream_);
   ld->group_copies.upload(ld->groups.copies.data(), ld->groups.copies.size(), stream_);
   if (ld->lay.total() < (i64(1) << 31)) {
@@ -234,8 +259,10 @@ Context::LevelData& Context::level(Space s, int level) {
     ld->packed = true;
   }
   if (nranks_ > 1)
-    ld->exchange = std::make_unique<Exchange>(build_exchange_plan(mesh_, topo_, ld->lay, rank_of, rank_),
-                                              transport_.get());
+    ld->exchange = std::make_unique<Exchange>(
+        partition_ == kPartitionSlab ? build_exchange_plan_slab(mesh_, topo_, ld->lay, units, rank_)
+                                     : build_exchange_plan(mesh_, topo_, ld->lay, rank_of, rank_),
+        transport_.get());
   auto& ref = *ld;
   levels_.emplace(key, std::move(ld));
   return ref;
@@ -363,6 +390,8 @@ void Function::export_ref(int level, double* host_ref) {
 Operator::Operator(Context& ctx, Form form, std::vector<const Function*> coeffs)
     : ctx_(&ctx), form_(form), coeffs_(std::move(coeffs)) {
   const FormInfo& fi = form_info(form);
+  if (ctx.partition() == Context::kPartitionSlab && form != Form::P1Diffusion)
+    fail_arg("slab partition: the P1 -Laplace operator only (config 4)");
 
   if (coeffs_.size() != fi.coeffSpaces.size())
     fail_arg(std::string("form ") + fi.name + " expects " + std::to_string(fi.coeffSpaces.size()) +
@@ -463,6 +492,8 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
     ev_stop = events_[events_used_].second;
     ++events_used_;
   }
+  if (ctx_->partition() == Context::kPartitionSlab && kernel_variant_ != 0)
+    fail_arg("slab partition: the default K1 kernel only");
   if (form_ == Form::P1Diffusion && kernel_variant_ >= 2) ctx_->ensure_p1_variant_tasks(ld);
   switch (form_) {
     case Form::P1Diffusion:
@@ -497,7 +528,7 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
                            ld.macros.get(), s);
       else
         launch_p1_stencil6(x, y, ld.tasks6.get(), ld.ntasks6, ld.lay.macro_stride, ld.lay.n, nm, t.p1.get(),
-                           ld.macros.get(), s);
+                           ld.macros.get(), s, ld.zrange.get());
       break;
     case Form::P1KDiffusion:
       if (kernel_variant_ == 1)

@@ -75,10 +75,17 @@ class Exchange;  // multi-rank interface exchange (exchange.hpp)
 class Context {
 public:
   // macros: the macro ids this rank stores (empty = all, single rank)
-  Context(const std::string& mesh_desc, int device, int rank, int nranks, std::vector<int> macros);
+  // partition: kPartitionMacro (whole macros per rank, `macros` = this
+  // rank's) or kPartitionSlab ((macro, z-slab) units of P1 points, every
+  // rank stores every macro; exchange.hpp slab_partition)
+  static constexpr int kPartitionMacro = 0, kPartitionSlab = 1;
+  Context(const std::string& mesh_desc, int device, int rank, int nranks, std::vector<int> macros,
+          int partition = kPartitionMacro);
   // an in-memory mesh (FormSystem(Form, const MacroMesh&, int), forms.hpp:46);
   // validated like the reference's (mesh.cpp:76-94)
-  Context(MacroMesh mesh, int device, int rank, int nranks, std::vector<int> macros);
+  Context(MacroMesh mesh, int device, int rank, int nranks, std::vector<int> macros,
+          int partition = kPartitionMacro);
+  int partition() const { return partition_; }
   ~Context();
 
   const MacroMesh& mesh() const { return mesh_; }
@@ -127,6 +134,7 @@ public:
     DeviceBuffer<int> tasks4;           // P1: register-tile tasks (variant 4)
     int ntasks4 = 0;
     bool variant_tasks_built = false;   // P1: the A/B variants' lists (built on first use)
+    DeviceBuffer<int> zrange;           // slab partition: per local macro {za, zb} computed here
     DeviceBuffer<int> p1k_tasks;        // P1: row tasks of the P1K gather kernel (K2)
     int np1k_tasks = 0;
     // solver (solver.hpp): per local macro, [support mask] -> {bit 0 interior,
@@ -153,6 +161,7 @@ private:
   Topology topo_;
   int device_, rank_, nranks_;
   std::vector<int> macros_;
+  int partition_ = kPartitionMacro;
   std::vector<int> group_;
   int ngroups_ = 0;
   cudaStream_t stream_ = nullptr;

@@ -115,3 +115,121 @@ def test_two_rank_exchange(mesh, form, level):
         assert not isinstance(err, str), err
         assert npeers == 1 and ngroups > 0
         assert err <= 1e-13, (rank, err)
+
+
+def _slab_worker(rank, world, port, mesh, level, q):
+    """(macro, z-slab) partition (TETMF_PARTITION_SLAB): every rank stores
+    every macro but only its units' planes are computed; copies elsewhere are
+    poisoned (NaN) so that any use of a non-owned copy shows."""
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import ctypes
+
+        import paper_2404_08371_b200 as tm
+        from oracle.refapi import PortSystem, port_lib
+
+        space = tm.SPACE_P1
+        ctx = tm.Context(mesh, device=-1, rank=rank, nranks=world, partition=tm.PARTITION_SLAB)
+        macros = ctx.local_macros()
+        nmac = ctx.num_macros()[0]
+        assert macros == list(range(nmac))  # every rank stores every macro
+        ms, _ = ctx.layout(space, level)
+        ref_map, nd = ctx.ref_map(space, level)
+        n = 1 << level
+        tet = lambda k: (k + 1) * (k + 2) * (k + 3) // 6
+        starts = np.array([tet(n) - tet(n - z) for z in range(n + 1)])
+        zslot = np.searchsorted(starts, np.arange(ms), side="right") - 1  # plane of each in-macro slot
+        units = tm.slab_units(nmac, level, world, rank)
+        own = np.zeros((nmac, ms), dtype=bool)
+        for m, za, zb in units:
+            own[m] = (zslot >= za) & (zslot < zb) & (np.arange(ms) < tet(n))
+        port = PortSystem(mesh, "P1", level)
+        x = port.seeded_input(42)
+        w_full, _ = port.apply(x, None, None)
+        L = port_lib().L
+        L.port_apply_macros.restype = ctypes.c_int
+        dp = ctypes.POINTER(ctypes.c_double)
+        L.port_apply_macros.argtypes = [ctypes.c_void_p, dp, dp, dp, ctypes.c_int, ctypes.POINTER(ctypes.c_ubyte), dp]
+        y = np.full(ms * nmac, np.nan)
+        for m in range(nmac):
+            mask = np.zeros(nmac, dtype=np.uint8)
+            mask[m] = 1
+            wm = np.empty(port.num_dofs)
+            assert L.port_apply_macros(port.h, x.ctypes.data_as(dp), None, None, 0,
+                                       mask.ctypes.data_as(ctypes.POINTER(ctypes.c_ubyte)),
+                                       wm.ctypes.data_as(dp)) == 0
+            e = ref_map[m * ms:(m + 1) * ms]
+            sel = (e >= 0) & own[m]
+            y[m * ms:(m + 1) * ms][sel] = wm[e[sel] >> 2]
+        off, cp = ctx.local_groups(space, level)
+        tm.host_local_sum(off, cp, y)
+        plan = ctx.exchange_plan(space, level)
+        send = tm.host_pack(y, plan["send_index"])
+        recv = np.zeros(int(plan["recv_offsets"][-1]))
+        reqs = []
+        for i, peer in enumerate(plan["peers"]):
+            so, se = plan["send_offsets"][i], plan["send_offsets"][i + 1]
+            ro, re_ = plan["recv_offsets"][i], plan["recv_offsets"][i + 1]
+            reqs.append(dist.isend(torch.from_numpy(send[so:se].copy()), peer))
+            buf = torch.zeros(int(re_ - ro), dtype=torch.float64)
+            dist.recv(buf, peer)
+            recv[ro:re_] = buf.numpy()
+        for r in reqs:
+            r.wait()
+        tm.host_combine(y, recv, plan["group_offsets"], plan["group_entries"])
+        sel = (ref_map >= 0) & own.ravel()
+        expect = w_full[ref_map[sel] >> 2]
+        err = np.abs(y[sel] - expect).max() / np.abs(w_full).max()
+        q.put((rank, float(err), int(sel.sum()), units))
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+        q.put((rank, "error: " + traceback.format_exc(), 0, None))
+
+
+@pytest.mark.parametrize("mesh,level,world", [("cube6", 4, 2), ("cube6", 4, 4), ("cube6", 5, 4),
+                                              ("cubes1x1x2", 4, 3)])
+def test_slab_partition_exchange(mesh, level, world):
+    """Config 4's strong-scaling partition: (macro, z-slab) units, exchange
+    of the macro-interface copies across ranks; every owned copy equals the
+    full apply and every lattice point is owned by exactly one rank."""
+    import paper_2404_08371_b200 as tm
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, world, port, mesh, level, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    owned = 0
+    for rank, err, cnt, units in res:
+        assert not isinstance(err, str), err
+        assert err <= 1e-13, (rank, err)
+        owned += cnt
+    # every stored point of every macro is owned once (units tile the planes)
+    nmac = tm.Context(mesh, device=-1).num_macros()[0]
+    n = 1 << level
+    assert owned == nmac * (n + 1) * (n + 2) * (n + 3) // 6
+
+
+def test_slab_units_balanced():
+    import paper_2404_08371_b200 as tm
+    n, L = 256, 8
+    for world in (2, 4, 8):
+        work = []
+        covered = {}
+        for r in range(world):
+            w = 0
+            for m, za, zb in tm.slab_units(6, L, world, r):
+                assert za % 8 == 0 and (zb % 8 == 0 or zb == n + 1)
+                for z in range(za, zb):
+                    assert (m, z) not in covered
+                    covered[(m, z)] = r
+                    w += (n + 1 - z) * (n + 2 - z) // 2
+            work.append(w)
+        assert len(covered) == 6 * (n + 1)
+        assert max(work) / (sum(work) / world) < 1.03, work  # within 3 % of perfect balance

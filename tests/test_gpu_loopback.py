@@ -153,3 +153,47 @@ def test_virtual_ranks_cg_and_dot(tm):
         assert abs(it - it1) <= 1
         assert np.abs(sol.reshape(-1, ms) - sol1[c.local_macros()]).max() <= 1e-8 * np.abs(sol1).max()
     assert len({o[0] for o in out}) == 1  # every rank sees the same scalar
+
+
+@pytest.mark.parametrize("mesh,level,nranks", [("cube6", 6, 2), ("cube6", 6, 4), ("cube6", 7, 8), ("cubes2", 5, 8),
+                                               ("cube6", 8, 8)])
+def test_slab_partition_virtual_ranks_bitwise(tm, mesh, level, nranks):
+    """Config 4's strong-scaling partition on one GPU: (macro, z-slab) units
+    (TETMF_PARTITION_SLAB), the K1 box kernel restricted to each rank's
+    planes, the exchange of macro-interface copies between slabs through the
+    loopback transport. Every rank's owned points equal the single-rank apply
+    bitwise."""
+    ctx1, y1, _, ms = _single(tm, mesh, "P1", level)
+    group = tm.LoopbackGroup(nranks)
+    ctxs = group.contexts(mesh, device=0, partition=tm.PARTITION_SLAB)
+    objs = [_setup(tm, c, "P1", level) for c in ctxs]
+
+    def body(r):
+        x, y, op, _ = objs[r]
+        op.apply(x, y, level)
+        ctxs[r].synchronize()
+        return y.download(level)
+
+    res = tm.run_ranks(body, nranks)
+    n = 1 << level
+    tet = lambda k: (k + 1) * (k + 2) * (k + 3) // 6
+    starts = np.array([tet(n) - tet(n - z) for z in range(n + 1)])
+    zslot = np.searchsorted(starts, np.arange(ms), side="right") - 1
+    real = np.arange(ms) < tet(n)
+    nmac = ctx1.num_macros()[0]
+    owned = np.zeros((nmac, ms), dtype=int)
+    for r, y in enumerate(res):
+        y = y.reshape(nmac, ms)
+        for m, za, zb in tm.slab_units(nmac, level, nranks, r):
+            sel = (zslot >= za) & (zslot < zb) & real
+            owned[m] += sel
+            assert np.array_equal(y[m][sel], y1[m][sel]), f"rank {r} macro {m} planes [{za}, {zb})"
+    assert (owned[:, real] == 1).all()  # every point computed by exactly one rank
+
+
+def test_slab_partition_rejects_other_forms(tm):
+    group = tm.LoopbackGroup(2)
+    ctx = tm.Context.loopback(group, "cube6", 0, device=0, partition=tm.PARTITION_SLAB)
+    a, b = tm.Function(ctx, tm.SPACE_P1), tm.Function(ctx, tm.SPACE_P1)
+    with pytest.raises(tm.InvalidArgument, match="slab partition"):
+        tm.Operator(ctx, tm.FORM_N1, [a, b])
