@@ -336,7 +336,10 @@ def run_gpu(a):
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     t_setup = time.time()
-    ctx = tm.Context(cfg["mesh"], device=local, rank=rank, nranks=ws, nccl_id=nccl_id)
+    # config 4 (strong scaling, 6 macros): (macro, z-slab) units over the ranks
+    slab = a.config == "c4" and ws > 1
+    ctx = tm.Context(cfg["mesh"], device=local, rank=rank, nranks=ws, nccl_id=nccl_id,
+                     partition=tm.PARTITION_SLAB if slab else tm.PARTITION_MACRO)
     comm_info = ctx.transport_info()  # "nccl rank r of N (cuda device d)": the communicator's own rank count
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
@@ -427,7 +430,12 @@ def run_gpu(a):
     # ---------------- roofline of the dominant (element) kernel
     kern_avg_ms = kern_ms / max(kern_n, 1)
     fp64_peak = ctx.fp64_peak(1.0) if a.fp64_peak and form in ("N1", "P2V") else None
-    roof = roofline(a.config, form, lattice_counts(nmac_local, level, form), kern_avg_ms, ms_per_step, fp64_peak)
+    local_counts = lattice_counts(nmac_local, level, form)
+    if slab:  # this rank's points: its units' planes
+        n = 1 << level
+        local_counts["p1_points"] = sum((n + 1 - z) * (n + 2 - z) // 2 for _, za, zb in
+                                        tm.slab_units(nmac_global, level, ws, rank) for z in range(za, zb))
+    roof = roofline(a.config, form, local_counts, kern_avg_ms, ms_per_step, fp64_peak)
 
     # ---------------- end to end through the public API (host buffers)
     e2e = None
@@ -458,7 +466,8 @@ def run_gpu(a):
             "data": "synthetic: x seeded uniform[-1,1] by canonical DoF key (SURVEY 8(d)); nodal coefficients (P1; P2 for P2V)",
             "config": {"workload": cfg["name"], "mesh": cfg["mesh"], "level": level, "form": form,
                        "macros": nmac_global, "dofs": n_unique, "elements": counts["elements"],
-                       "parallelism": f"macro partition over {ws} GPU(s)", "comm": comm_info,
+                       "parallelism": (f"(macro, z-slab) partition over {ws} GPU(s)" if slab else
+                                       f"macro partition over {ws} GPU(s)"), "comm": comm_info,
                        "l2": "inputs > 126 MB L2" if flush is None else "L2 flushed between steps",
                        "setup_s": round(t_setup, 2)},
             "roofline": roof, "clocks": clk.summary(), "gpu_launches": launches,
