@@ -101,7 +101,11 @@ void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, 
                     i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s,
                     const N1GramTable* ptab = nullptr);
 int n1_kernel_mode();
-// K2 default: per-point gather over the 24 incident elements (k_p1k_gather.cu)
+// K2 default: the gather walked along y with register windows (k_p1k_gather.cu)
+void build_p1k_walk_tasks(int nmacros, int n, std::vector<int>& out);
+void launch_p1k_walk(const double* x, const double* k, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
+                     int n, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
+// K2 round 1: per-point gather over the 24 incident elements (k_p1k_gather.cu)
 void build_p1k_tasks(int nmacros, int n, std::vector<int>& out);
 void launch_p1k_gather(const double* x, const double* k, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
                        int n, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);

@@ -178,6 +178,9 @@ Context::LevelData& Context::level(Space s, int level) {
     build_p1k_tasks(static_cast<int>(macros_.size()), n, tasks);
     ld->np1k_tasks = static_cast<int>(tasks.size() / 4);
     ld->p1k_tasks.upload(tasks.data(), tasks.size(), stream_);
+    build_p1k_walk_tasks(static_cast<int>(macros_.size()), n, tasks);
+    ld->np1k_walk = static_cast<int>(tasks.size() / 4);
+    ld->p1k_walk.upload(tasks.data(), tasks.size(), stream_);
   } else if (s == Space::ND1) {
     std::vector<int> all, part;
     ld->group_tasks.assign(ngroups_, {0, 0, 0, 0});
@@ -534,9 +537,12 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
       if (kernel_variant_ == 1)
         launch_p1k_cubes(x, coeffs_[0]->data(level), y, ld.macros.get(), nm, ld.lay.macro_stride, ld.lay.n,
                          t.p1.get(), s);
-      else
+      else if (kernel_variant_ == 2)  // round-1 default: one 32-point row segment per warp
         launch_p1k_gather(x, coeffs_[0]->data(level), y, ld.p1k_tasks.get(), ld.np1k_tasks, ld.lay.macro_stride,
                           ld.lay.n, t.p1.get(), ld.macros.get(), s);
+      else
+        launch_p1k_walk(x, coeffs_[0]->data(level), y, ld.p1k_walk.get(), ld.np1k_walk, ld.lay.macro_stride,
+                        ld.lay.n, t.p1.get(), ld.macros.get(), s);
       break;
     case Form::N1CurlCurlMass: {
       auto& cl = ctx_->level(Space::P1, level);

@@ -135,7 +135,9 @@ public:
     int ntasks4 = 0;
     bool variant_tasks_built = false;   // P1: the A/B variants' lists (built on first use)
     DeviceBuffer<int> zrange;           // slab partition: per local macro {za, zb} computed here
-    DeviceBuffer<int> p1k_tasks;        // P1: row tasks of the P1K gather kernel (K2)
+    DeviceBuffer<int> p1k_tasks;        // P1: row tasks of the P1K gather kernel (K2 round 1, diagonal)
+    int np1k_walk = 0;
+    DeviceBuffer<int> p1k_walk;         // P1: column-walk tasks of the P1K walk kernel (K2)
     int np1k_tasks = 0;
     // solver (solver.hpp): per local macro, [support mask] -> {bit 0 interior,
     // bit 1 owner copy}; reduction scratch
