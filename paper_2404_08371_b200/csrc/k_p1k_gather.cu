@@ -198,7 +198,6 @@ p1k_walk_kernel(const double* __restrict__ x, const double* __restrict__ kc, dou
   const RowTask t = tasks[warp];
   const int pz = t.z, px = t.x0 + (threadIdx.x & 31);
   const int yend = min(t.y + kWalkRows, n - pz - px + 1);  // rows of this column in the chunk
-  if (t.y >= yend) return;
 #if TETMF_P1K_SMEMK
   // the group's 36 off-diagonal K_o[i][j] / 4 in this warp's shared slot (broadcast loads)
   __shared__ double skt[kWarps][36];
@@ -211,8 +210,9 @@ p1k_walk_kernel(const double* __restrict__ x, const double* __restrict__ kc, dou
       const int i = r < 3 ? 0 : r < 5 ? 1 : 2, j = r < 3 ? r + 1 : r < 5 ? r - 1 : 3;
       Kt[e] = 0.25 * __ldg(K + o * 10 + sym4(i, j));
     }
-    __syncwarp();
+    __syncwarp();  // every lane of the warp took part (no lane has left yet)
   }
+  if (t.y >= yend) return;  // this column has no row in the chunk
 #else
   double Kt[36];
   {
@@ -224,6 +224,7 @@ p1k_walk_kernel(const double* __restrict__ x, const double* __restrict__ kc, dou
 #pragma unroll
         for (int j = i + 1; j < 4; ++j) Kt[offdiag(o, i, j)] = 0.25 * __ldg(K + o * 10 + sym4(i, j));
   }
+  if (t.y >= yend) return;
 #endif
   const double* __restrict__ xm = x + static_cast<i64>(t.macro) * stride;
   const double* __restrict__ km = kc + static_cast<i64>(t.macro) * stride;
