@@ -201,8 +201,9 @@ int tetmf_chebyshev_smooth(tetmf_op* op, const tetmf_fn* diag, const tetmf_fn* b
  * the context stream (enable resets the totals); stats synchronize. */
 int tetmf_op_profile(tetmf_op* op, int enable);
 /* 0 = optimized kernels (default); 1 = first-version kernels (A/B tests);
- * P1 -Laplace also 2..9 = the alternative K1 kernels kept for A/B runs
- * (bitwise equal to the default) */
+ * P1 -Laplace also 5, 7, 8, 9, 10 = alternative K1 kernels kept for A/B runs
+ * (bitwise equal to the default); P1K 2 = the round-1
+ * per-point gather. Other values: TETMF_EINVAL at the next apply. */
 int tetmf_op_set_variant(tetmf_op* op, int variant);
 
 /* Integration rule of tetmf_apply / tetmf_op_diagonal: 0 = exact (default;

@@ -51,10 +51,6 @@ void launch_axpy(double* y, const double* x, double a, i64 count, cudaStream_t s
 
 void launch_p1_stencil(const double* x, double* y, const MacroDesc* d_macros, int nmacros, i64 macro_stride,
                        int n, const P1DeviceTable* d_tables, cudaStream_t s);
-// K1 v2: warp-per-(macro, z, x-segment) row walk (k_p1_stencil.cu)
-void build_stencil_tasks(int nmacros, int n, std::vector<int>& out);
-void launch_p1_stencil_v2(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
-                          const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
 // K1 default: two-plane row walk (k_p1_stencil2.cu)
 void build_stencil2_tasks(int nmacros, int n, std::vector<int>& out);
 void launch_p1_stencil2(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
@@ -80,26 +76,14 @@ void launch_p1_stencil8(const double* x, double* y, const int* d_tasks, int ntas
 // K1 variant 10: variant 6's boxes in a persistent double-buffered CTA loop (k_p1_stencil5.cu)
 void launch_p1_stencil10(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
                          int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
-// K1 variant 4: 32 x 4 register tiles (k_p1_stencil_tile.cu)
-void build_stencil_tile_tasks(int nmacros, int n, std::vector<int>& out);
-void launch_p1_stencil_tile(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
-                            const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
-// K1 v3: TMA plane streaming (k_p1_stencil_tma.cu)
-void build_stencil_tma_tasks(int nmacros, int n, std::vector<int>& out);
-void launch_p1_stencil_tma(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
-                           const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
 // K3 v2: cube walk, two layer-parity passes, one launch per geometry group
 void build_n1_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out);
-void launch_n1_cubes_v2(const N1DeviceTable* table, const N1GramTable* gram, int pass, const double* x, const double* alpha,
-                        const double* beta, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
-                        i64 class_stride, i64 coeff_stride, int n, cudaStream_t s);
 // K3 default: folded cube walk (k_n1_fold.cu); same task-list / launch contract
 void build_n1_fold_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out);
 void pad_n1_fold_tasks(std::vector<int>& tasks);
 void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, const double* x, const double* alpha,
                     const double* beta, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
-                    i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s,
-                    const N1GramTable* ptab = nullptr);
+                    i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s);
 int n1_kernel_mode();
 // K2 default: the gather walked along y with register windows (k_p1k_gather.cu)
 void build_p1k_walk_tasks(int nmacros, int n, std::vector<int>& out);

@@ -2,10 +2,11 @@
 // with folded lane columns.
 //
 // Same element formula (n1_common.cuh element_gram), edge ownership, parity
-// passes and write-back rules as k_n1_cubes.cu; what changes is which cube a
+// passes and write-back rules as the round-1 segment walk (removed in round 2,
+// git history: k_n1_cubes.cu); what changes is which cube a
 // lane processes at each step, so that no lane idles at the row ends.
 //
-// Layer z holds the cubes x + y <= L = n-1-z. In k_n1_cubes.cu a warp owns a
+// Layer z holds the cubes x + y <= L = n-1-z. In the segment walk a warp owns a
 // 31-column segment and walks y upward; column x ends at y = L - x, so the
 // lanes of a segment go idle one by one (a 31x31/2 triangle per segment, 16 %
 // of all lane-steps at L8). Here the layer's K full segments S_k = [31k,
@@ -39,7 +40,7 @@
 // slot may hold the other phase's row; that only happens for values the top
 // cube of a column (one element, WU) does not use, and stale slots hold
 // zeros or older finite values, which only reach zero-coefficient elements.
-// Copied addresses are the ones k_n1_cubes.cu reads.
+// Copied addresses are the ones the segment walk read.
 //
 // Pass 1 (odd layers) adds to in-plane partial sums written by pass 0; those
 // six values per cube are staged by cp.async one step ahead as well (one slot
@@ -115,26 +116,11 @@ struct FoldIn {
   }
 };
 
-// Gram table of one geometry group as a kernel parameter (the launch's
-// constant bank): every table read has a compile-time offset, so it is a
-// c[0x0][imm] operand of the DFMA -- no shared-memory loads, no registers.
-struct ParamTab {
-  const double* p;
-  template <int I>
-  __device__ __forceinline__ double get() const { return p[I]; }
-};
-struct ParamTabs {
-  const N1GramTable& t;
-  template <int O>
-  __device__ __forceinline__ ParamTab tab() const { return ParamTab{t.o[O]}; }
-};
-
-// PTAB = false: the group's table is staged in shared memory (one launch per
-// pass covers all groups); PTAB = true: it is the parameter `ptab` (one
-// launch per pass and group).
-template <int PASS, int RULE, bool PTAB>
+// The group's Gram table is staged in shared memory; one launch per pass
+// covers all geometry groups.
+template <int PASS, int RULE>
 __global__ void __launch_bounds__(32 * kWarps, TETMF_N1F_MIN_BLOCKS)
-n1_fold_kernel(const __grid_constant__ N1GramTable ptab, const N1GramTable* __restrict__ gram,
+n1_fold_kernel(const N1GramTable* __restrict__ gram,
                const MacroDesc* __restrict__ macros,
                const double* __restrict__ xin, const double* __restrict__ alpha, const double* __restrict__ beta,
                double* __restrict__ yout, const FoldTask* __restrict__ tasks, int ntasks, i64 stride, i64 cstride,
@@ -144,7 +130,7 @@ n1_fold_kernel(const __grid_constant__ N1GramTable ptab, const N1GramTable* __re
   // one launch covers every geometry group of a pass; task lists are padded
   // per group to whole CTAs, so the CTA's first task (always real) names
   // the group of all its warps
-  if (!PTAB) {
+  {
     const N1GramTable* gt = gram + macros[tasks[blockIdx.x * kWarps].macro].group;
     for (int i = threadIdx.x; i < 6 * kGramRow; i += blockDim.x) (&sg.o[0][0])[i] = __ldg(&gt->o[0][0] + i);
   }
@@ -303,12 +289,8 @@ n1_fold_kernel(const __grid_constant__ N1GramTable ptab, const N1GramTable* __re
 #pragma unroll
     for (int k = 0; k < 19; ++k) Y[k] = 0.0;
     const int s = X + y + z;
-    if (PTAB)
-      cube_elements<RULE>(ParamTabs{ptab}, FoldIn{r0, r1, r0 + dq, r1 + dq}, Y, cube && s <= n - 1,
-                          cube && s <= n - 2, cube && s <= n - 3);
-    else
-      cube_elements<RULE>(SmemTabs{sg}, FoldIn{r0, r1, r0 + dq, r1 + dq}, Y, cube && s <= n - 1, cube && s <= n - 2,
-                          cube && s <= n - 3);
+    cube_elements<RULE>(SmemTabs{sg}, FoldIn{r0, r1, r0 + dq, r1 + dq}, Y, cube && s <= n - 1, cube && s <= n - 2,
+                        cube && s <= n - 3);
     __syncwarp();  // ring slot tt mod 3 is refilled by the next step's copies
 
     // contributions of the x-1 neighbour cube (same row)
@@ -435,26 +417,19 @@ void pad_n1_fold_tasks(std::vector<int>& tasks) {
   }
 }
 
-// gram: tables of all geometry groups; macros: local macro descriptors;
-// ptab (optional): the host copy of ONE group's table -> the parameter-bank
-// kernel for a task range of that group only
+// gram: tables of all geometry groups; macros: local macro descriptors
 void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, const double* x, const double* alpha,
                     const double* beta, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
-                    i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s, const N1GramTable* ptab) {
+                    i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s) {
   if (ntasks == 0) return;
   if (rule < 0 || rule > 2) fail_internal("n1_fold: rule index out of range");
   constexpr int smem = static_cast<int>(sizeof(N1GramTable) + sizeof(double) * kWarpSmem * kWarps);
-  using K = decltype(&n1_fold_kernel<0, 0, false>);
-  static const K kerns[2][2][3] = {
-      {{n1_fold_kernel<0, 0, false>, n1_fold_kernel<0, 1, false>, n1_fold_kernel<0, 2, false>},
-       {n1_fold_kernel<1, 0, false>, n1_fold_kernel<1, 1, false>, n1_fold_kernel<1, 2, false>}},
-      {{n1_fold_kernel<0, 0, true>, n1_fold_kernel<0, 1, true>, n1_fold_kernel<0, 2, true>},
-       {n1_fold_kernel<1, 0, true>, n1_fold_kernel<1, 1, true>, n1_fold_kernel<1, 2, true>}}};
+  using K = decltype(&n1_fold_kernel<0, 0>);
+  static const K kerns[2][3] = {{n1_fold_kernel<0, 0>, n1_fold_kernel<0, 1>, n1_fold_kernel<0, 2>},
+                                {n1_fold_kernel<1, 0>, n1_fold_kernel<1, 1>, n1_fold_kernel<1, 2>}};
   static const bool attr = [] {
-    for (int t = 0; t < 2; ++t)
-      for (int p = 0; p < 2; ++p)
-        for (int r = 0; r < 3; ++r)
-          cudaFuncSetAttribute(kerns[t][p][r], cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int p = 0; p < 2; ++p)
+      for (int r = 0; r < 3; ++r) cudaFuncSetAttribute(kerns[p][r], cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     double R[2][4][10];
     n1_rule_moments(1, R[0]);
     n1_rule_moments(2, R[1]);
@@ -463,11 +438,17 @@ void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, 
   }();
   (void)attr;
   const unsigned grid = static_cast<unsigned>((ntasks + kWarps - 1) / kWarps);
-  static const N1GramTable zero{};
-  kerns[ptab ? 1 : 0][pass][rule]<<<grid, 32 * kWarps, smem, s>>>(
-      ptab ? *ptab : zero, gram, macros, x, alpha, beta, y, reinterpret_cast<const FoldTask*>(d_tasks), ntasks,
-      macro_stride, class_stride, coeff_stride, n);
+  kerns[pass][rule]<<<grid, 32 * kWarps, smem, s>>>(gram, macros, x, alpha, beta, y,
+                                                    reinterpret_cast<const FoldTask*>(d_tasks), ntasks, macro_stride,
+                                                    class_stride, coeff_stride, n);
   check_launch("n1_fold");
+}
+
+// the N1 apply is the fold kernel; task lists per geometry group and pass
+int n1_kernel_mode() { return 3; }
+
+void build_n1_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out) {
+  build_n1_fold_tasks(local_macros, n, parity, out);
 }
 
 } // namespace tetmf

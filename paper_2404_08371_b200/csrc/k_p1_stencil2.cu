@@ -8,7 +8,7 @@
 // one plane per warp needs 7), keeps the older rows in a register window and
 // computes both planes' points with 15 DFMA each. The chunk loop is fully
 // unrolled; two independent point streams per warp double the memory-level
-// parallelism of the single-plane walk (k_p1_stencil.cu).
+// parallelism of the single-plane walk (variant 2, removed in round 2).
 //
 // No bounds predicates on the window loads (guard-padded level buffers; all
 // out-of-lattice values meet zero weights). Rows whose points of both planes

@@ -278,21 +278,12 @@ void Context::ensure_p1_variant_tasks(LevelData& ld) {
   build_stencil2_tasks(nm, n, tasks);
   ld.ntasks = static_cast<int>(tasks.size() / 4);
   ld.tasks.upload(tasks.data(), tasks.size(), stream_);
-  build_stencil_tile_tasks(nm, n, tasks);
-  ld.ntasks4 = static_cast<int>(tasks.size() / 4);
-  ld.tasks4.upload(tasks.data(), tasks.size(), stream_);
-  build_stencil_tma_tasks(nm, n, tasks);
-  ld.ntasks3 = static_cast<int>(tasks.size() / 4);
-  ld.tasks3.upload(tasks.data(), tasks.size(), stream_);
   build_stencil7_tasks(nm, n, tasks);
   ld.ntasks7 = static_cast<int>(tasks.size() / 4);
   ld.tasks7.upload(tasks.data(), tasks.size(), stream_);
   build_stencil5_tasks(nm, n, tasks);
   ld.ntasks5 = static_cast<int>(tasks.size() / 4);
   ld.tasks5.upload(tasks.data(), tasks.size(), stream_);
-  build_stencil_tasks(nm, n, tasks);
-  ld.ntasks2 = static_cast<int>(tasks.size() / 4);
-  ld.tasks2.upload(tasks.data(), tasks.size(), stream_);
   ld.variant_tasks_built = true;
 }
 
@@ -439,7 +430,6 @@ Operator::LevelTables& Operator::tables(int level) {
         done[grp[li]] = true;
       }
     lt->n1g.upload(gt.data(), gt.size(), ctx_->stream());
-    lt->n1g_host = gt;
   } else {
     std::vector<P1DeviceTable> t(ng);
     std::vector<bool> done(ng, false);
@@ -497,17 +487,15 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
   }
   if (ctx_->partition() == Context::kPartitionSlab && kernel_variant_ != 0)
     fail_arg("slab partition: the default K1 kernel only");
+  if ((form_ == Form::P1Diffusion && kernel_variant_ >= 2 && kernel_variant_ <= 4) ||
+      (form_ == Form::N1CurlCurlMass && kernel_variant_ >= 2) || (form_ == Form::P2VDiffusion && kernel_variant_ >= 2) ||
+      (form_ == Form::P1KDiffusion && kernel_variant_ >= 3))
+    fail_arg("kernel variant " + std::to_string(kernel_variant_) + " does not exist for this form");
   if (form_ == Form::P1Diffusion && kernel_variant_ >= 2) ctx_->ensure_p1_variant_tasks(ld);
   switch (form_) {
     case Form::P1Diffusion:
       if (kernel_variant_ == 1)
         launch_p1_stencil(x, y, ld.macros.get(), nm, ld.lay.macro_stride, ld.lay.n, t.p1.get(), s);
-      else if (kernel_variant_ == 2)
-        launch_p1_stencil_v2(x, y, ld.tasks2.get(), ld.ntasks2, ld.lay.macro_stride, ld.lay.n, t.p1.get(),
-                             ld.macros.get(), s);
-      else if (kernel_variant_ == 3)
-        launch_p1_stencil_tma(x, y, ld.tasks3.get(), ld.ntasks3, ld.lay.macro_stride, ld.lay.n, t.p1.get(),
-                              ld.macros.get(), s);
       else if (kernel_variant_ == 8)
         launch_p1_stencil8(x, y, ld.tasks7.get(), ld.ntasks7, ld.lay.macro_stride, ld.lay.n, nm, t.p1.get(),
                            ld.macros.get(), s);
@@ -520,9 +508,6 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
       else if (kernel_variant_ == 5)
         launch_p1_stencil5(x, y, ld.tasks5.get(), ld.ntasks5, ld.lay.macro_stride, ld.lay.n, nm, t.p1.get(),
                            ld.macros.get(), s);
-      else if (kernel_variant_ == 4)
-        launch_p1_stencil_tile(x, y, ld.tasks4.get(), ld.ntasks4, ld.lay.macro_stride, ld.lay.n, t.p1.get(),
-                               ld.macros.get(), s);
       else if (kernel_variant_ == 10)
         launch_p1_stencil10(x, y, ld.tasks6.get(), ld.ntasks6, ld.lay.macro_stride, ld.lay.n, nm, t.p1.get(),
                             ld.macros.get(), s);
@@ -549,30 +534,12 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
       if (kernel_variant_ == 1) {
         launch_n1_cubes(x, coeffs_[0]->data(level), coeffs_[1]->data(level), y, ld.macros.get(), nm,
                         ld.lay.macro_stride, ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, t.n1.get(), s);
-      } else if (n1_kernel_mode() == 3 && kernel_variant_ == 2) {
-        // parameter-bank tables: one launch per pass and geometry group
-        const int rule = rule_index();
-        for (int pass = 0; pass < 2; ++pass)
-          for (std::size_t g = 0; g < ld.fold_group_range.size(); ++g) {
-            const auto& r = ld.fold_group_range[g];
-            launch_n1_fold(t.n1g.get(), ld.macros.get(), pass, x, coeffs_[0]->data(level), coeffs_[1]->data(level), y,
-                           ld.fold_tasks.get() + 4 * r[2 * pass], r[2 * pass + 1], ld.lay.macro_stride,
-                           ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, rule, s, &t.n1g_host[g]);
-          }
-      } else if (n1_kernel_mode() == 3) {
+      } else {
         const int rule = rule_index();
         for (int pass = 0; pass < 2; ++pass)
           launch_n1_fold(t.n1g.get(), ld.macros.get(), pass, x, coeffs_[0]->data(level), coeffs_[1]->data(level), y,
                          ld.fold_tasks.get() + 4 * ld.fold_range[2 * pass], ld.fold_range[2 * pass + 1],
                          ld.lay.macro_stride, ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, rule, s);
-      } else {
-        for (int pass = 0; pass < 2; ++pass)
-          for (std::size_t g = 0; g < ld.group_tasks.size(); ++g) {
-            const auto& gt = ld.group_tasks[g];
-            launch_n1_cubes_v2(t.n1.get() + g, t.n1g.get() + g, pass, x, coeffs_[0]->data(level), coeffs_[1]->data(level), y,
-                               ld.tasks.get() + 4 * gt[2 * pass], gt[2 * pass + 1], ld.lay.macro_stride,
-                               ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, s);
-          }
       }
       break;
     }
@@ -615,8 +582,6 @@ void Operator::debug_perturb_table(int level, i64 index, double delta) {
   v += delta;
   TETMF_CUDA(cudaMemcpyAsync(base + index, &v, sizeof(double), cudaMemcpyHostToDevice, s));
   TETMF_CUDA(cudaStreamSynchronize(s));
-  if (form_ == Form::N1CurlCurlMass && !t.n1g_host.empty())
-    (&t.n1g_host[0].o[0][0])[index] += delta;  // the parameter-bank variant's host copy
 }
 
 void Operator::set_quadrature(int degree) {

@@ -121,18 +121,12 @@ public:
     std::unique_ptr<Exchange> exchange; // nranks > 1
     DeviceBuffer<int> tasks;            // kernel task list (per space / level)
     int ntasks = 0;
-    DeviceBuffer<int> tasks2;           // P1: row-walk stencil tasks (variant 2)
-    int ntasks2 = 0;
-    DeviceBuffer<int> tasks3;           // P1: TMA plane-streaming tasks (variant 3)
-    int ntasks3 = 0;
     DeviceBuffer<int> tasks5;           // P1: interior row-walk CTA tasks (variant 5)
     int ntasks5 = 0;
     DeviceBuffer<int> tasks6;           // P1: shared-memory box tasks (variant 6)
     int ntasks6 = 0;
     DeviceBuffer<int> tasks7;           // P1: persistent double-buffered box tasks (variant 7)
     int ntasks7 = 0;
-    DeviceBuffer<int> tasks4;           // P1: register-tile tasks (variant 4)
-    int ntasks4 = 0;
     bool variant_tasks_built = false;   // P1: the A/B variants' lists (built on first use)
     DeviceBuffer<int> zrange;           // slab partition: per local macro {za, zb} computed here
     DeviceBuffer<int> p1k_tasks;        // P1: row tasks of the P1K gather kernel (K2 round 1, diagonal)
@@ -235,7 +229,6 @@ private:
     DeviceBuffer<P1DeviceTable> p1;
     DeviceBuffer<N1DeviceTable> n1;
     DeviceBuffer<N1GramTable> n1g;       // Gram form per geometry group (K3 v2)
-    std::vector<N1GramTable> n1g_host;   // host copies (parameter-bank K3 launches)
     DeviceBuffer<P2VTable> p2v;          // P2V coefficient-basis tables per geometry group
   };
   LevelTables& tables(int level);
