@@ -446,7 +446,7 @@ def run_gpu(a):
     subs = {}
     if a.subrecords and ws == 1 and a.config == "c5":
         del x, y
-        for key in ("c4", "c2l", "p2v"):
+        for key in ("c4", "c2l", "p2v", "c1", "c2", "c3"):
             subs[key] = sub_record(tm, torch, key, max(a.steps, 10), 3, local, fp64_peak)
 
     cpu = None
@@ -609,7 +609,7 @@ def main():
     p.add_argument("--no-fp64-peak", dest="fp64_peak", action="store_false")
     p.add_argument("--variant", type=int, default=0, help="kernel variant for A/B runs (0 = default)")
     p.add_argument("--no-subrecords", dest="subrecords", action="store_false",
-                   help="c5 only: skip the c4 / c2l / p2v sub-records")
+                   help="c5 only: skip the c4 / c2l / p2v / c1-c3 sub-records")
     a = p.parse_args()
     a.warmup = max(a.warmup, 3)
     if a.impl == "reference":
