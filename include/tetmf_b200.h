@@ -142,6 +142,18 @@ int tetmf_fn_num_ref_dofs(tetmf_fn* fn, int level, int64_t* count);
 int tetmf_fn_import_ref(tetmf_fn* fn, int level, const double* host_ref);
 int tetmf_fn_export_ref(tetmf_fn* fn, int level, double* host_ref);
 
+/* Multi-rank I/O in reference numbering (macro partition): this rank's owned
+ * slice [lo, hi) of the global FieldVector -- the carriers whose owner macro
+ * (lowest sharing macro id, fespace.cpp:216-231) is local; contiguous because
+ * the reference numbering sorts by owner macro first (fespace.cpp:283-295).
+ * import_ref_owned sets every local copy of an owned carrier and then the
+ * ghost copies (carriers owned elsewhere) from their owners: collective over
+ * the ranks. export_ref_owned writes the owned slice. Together they are
+ * FormSystem::apply's host I/O for one rank of a distributed vector. */
+int tetmf_fn_ref_owned_range(tetmf_fn* fn, int level, int64_t* lo, int64_t* hi);
+int tetmf_fn_import_ref_owned(tetmf_fn* fn, int level, const double* host_owned);
+int tetmf_fn_export_ref_owned(tetmf_fn* fn, int level, double* host_owned);
+
 int tetmf_op_create(tetmf_ctx* ctx, int form, tetmf_fn* const* coeffs, int ncoeffs, tetmf_op** out);
 int tetmf_op_destroy(tetmf_op* op);
 int tetmf_apply(tetmf_op* op, const tetmf_fn* src, tetmf_fn* dst, int level, int update);

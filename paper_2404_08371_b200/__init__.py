@@ -82,6 +82,9 @@ _SIGS = {
     "tetmf_fn_num_ref_dofs": (ctypes.c_int, [_c_vp, ctypes.c_int, _c_i64p]),
     "tetmf_fn_import_ref": (ctypes.c_int, [_c_vp, ctypes.c_int, _c_dp]),
     "tetmf_fn_export_ref": (ctypes.c_int, [_c_vp, ctypes.c_int, _c_dp]),
+    "tetmf_fn_ref_owned_range": (ctypes.c_int, [_c_vp, ctypes.c_int, _c_i64p, _c_i64p]),
+    "tetmf_fn_import_ref_owned": (ctypes.c_int, [_c_vp, ctypes.c_int, _c_dp]),
+    "tetmf_fn_export_ref_owned": (ctypes.c_int, [_c_vp, ctypes.c_int, _c_dp]),
     "tetmf_op_create": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.POINTER(_c_vp), ctypes.c_int,
                                        ctypes.POINTER(_c_vp)]),
     "tetmf_op_destroy": (ctypes.c_int, [_c_vp]),
@@ -454,6 +457,27 @@ class Function:
     def export_ref(self, level: int) -> np.ndarray:
         out = np.empty(self.num_ref_dofs(level), dtype=np.float64)
         _check(lib().tetmf_fn_export_ref(self._h, level, _dptr(out)))
+        return out
+
+    def owned_ref_range(self, level: int) -> tuple[int, int]:
+        """[lo, hi): this rank's owned slice of the reference numbering."""
+        lo, hi = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().tetmf_fn_ref_owned_range(self._h, level, ctypes.byref(lo), ctypes.byref(hi)))
+        return lo.value, hi.value
+
+    def import_ref_owned(self, level: int, v):
+        """Owned slice in (numpy array of hi - lo entries, or a raw pinned host
+        pointer), ghost copies from their owners (collective)."""
+        lo, hi = self.owned_ref_range(level)
+        p = _dptr(v, hi - lo) if isinstance(v, np.ndarray) else ctypes.cast(_c_vp(v), _c_dp)
+        _check(lib().tetmf_fn_import_ref_owned(self._h, level, p))
+
+    def export_ref_owned(self, level: int, out=None):
+        lo, hi = self.owned_ref_range(level)
+        if out is None:
+            out = np.empty(hi - lo)
+        p = _dptr(out, hi - lo) if isinstance(out, np.ndarray) else ctypes.cast(_c_vp(out), _c_dp)
+        _check(lib().tetmf_fn_export_ref_owned(self._h, level, p))
         return out
 
     def dot(self, other: "Function", level: int) -> float:

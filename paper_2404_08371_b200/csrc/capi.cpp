@@ -309,6 +309,38 @@ int tetmf_fn_export_ref(tetmf_fn* fn, int level, double* host_ref) {
   });
 }
 
+int tetmf_fn_ref_owned_range(tetmf_fn* fn, int level, int64_t* lo, int64_t* hi) {
+  return guard([&] {
+    need(fn, "fn");
+    need(lo, "lo");
+    need(hi, "hi");
+    i64 a = 0, b = 0;
+    fn->impl->owned_ref_range(level, &a, &b);
+    *lo = a;
+    *hi = b;
+  });
+}
+
+int tetmf_fn_import_ref_owned(tetmf_fn* fn, int level, const double* host_owned) {
+  return guard([&] {
+    need(fn, "fn");
+    i64 a = 0, b = 0;
+    fn->impl->owned_ref_range(level, &a, &b);
+    if (b > a) need(host_owned, "host_owned");
+    fn->impl->import_ref_owned(level, host_owned);
+  });
+}
+
+int tetmf_fn_export_ref_owned(tetmf_fn* fn, int level, double* host_owned) {
+  return guard([&] {
+    need(fn, "fn");
+    i64 a = 0, b = 0;
+    fn->impl->owned_ref_range(level, &a, &b);
+    if (b > a) need(host_owned, "host_owned");
+    fn->impl->export_ref_owned(level, host_owned);
+  });
+}
+
 int tetmf_op_create(tetmf_ctx* ctx, int form, tetmf_fn* const* coeffs, int ncoeffs, tetmf_op** out) {
   return guard([&] {
     need(ctx, "ctx");

@@ -43,6 +43,13 @@ void launch_import_ref(double* lat, const i64* map, i64 total, const double* ref
 void launch_export_ref(const double* lat, const i64* map, i64 total, double* ref, cudaStream_t s);
 void launch_interface_sum(double* y, const i64* offsets, const i64* copies, i64 ngroups, cudaStream_t s,
                           bool signed_values = true);
+// one rank's owned slice [lo, hi) of the reference numbering (multi-rank I/O)
+void launch_import_ref_range(double* lat, const i64* map, i64 total, const double* ref, i64 lo, i64 hi,
+                             cudaStream_t s);
+void launch_export_ref_range(const double* lat, const i64* map, i64 total, double* ref, i64 lo, i64 hi,
+                             cudaStream_t s);
+// ghost update of rank-local interface groups: copies := owner copy (signed)
+void launch_interface_owner(double* y, const i64* offsets, const i64* copies, i64 ngroups, cudaStream_t s);
 // K4 with two-copy groups packed as 32-bit pairs (one thread per pair) and
 // the remaining groups in CSR form, one launch; same sums as interface_sum
 void launch_interface_sum_packed(double* y, const unsigned* pairs, i64 npairs, const i64* offsets, const i64* copies,

@@ -15,9 +15,9 @@ __global__ void pack_kernel(const double* y, const i64* send_index, double* send
 }
 
 __global__ void combine_kernel(double* y, const double* recv, const i64* offsets, const i64* entries, i64 ngroups,
-                               bool sgn) {
+                               bool sgn, bool owner) {
   const i64 g = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
-  if (g < ngroups) exchange_combine_one(y, recv, offsets, entries, g, sgn);
+  if (g < ngroups) exchange_combine_one(y, recv, offsets, entries, g, sgn, owner);
 }
 
 template <typename T>
@@ -47,7 +47,11 @@ Exchange::~Exchange() {
   cudaFree(d_recv_);
 }
 
-void Exchange::run(double* y, cudaStream_t stream, bool signed_values) {
+void Exchange::run(double* y, cudaStream_t stream, bool signed_values) { run_mode(y, stream, signed_values, false); }
+
+void Exchange::broadcast_owner(double* y, cudaStream_t stream) { run_mode(y, stream, true, true); }
+
+void Exchange::run_mode(double* y, cudaStream_t stream, bool signed_values, bool owner) {
   if (!transport_) throw CommError("exchange: no transport attached to the context");
   const i64 ns = plan_.send_total();
   if (ns > 0) {
@@ -60,7 +64,7 @@ void Exchange::run(double* y, cudaStream_t stream, bool signed_values) {
   if (ng > 0) {
     combine_kernel<<<static_cast<unsigned>((ng + 255) / 256), 256, 0, stream>>>(y, d_recv_, d_group_offsets_,
                                                                                  d_group_entries_, ng,
-                                                                                 signed_values);
+                                                                                 signed_values, owner);
     check_launch("exchange_combine");
   }
 }

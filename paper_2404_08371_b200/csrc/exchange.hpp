@@ -84,11 +84,13 @@ TM_HD void exchange_pack_one(const double* y, const i64* send_index, double* sen
   send[i] = (signed_values && (e & 1)) ? -v : v;
 }
 
+// owner = true: ghost update instead of a sum -- every local copy takes the
+// owner copy's value (the first entry: entries are in ascending macro id)
 TM_HD void exchange_combine_one(double* y, const double* recv, const i64* offsets, const i64* entries, i64 g,
-                                bool signed_values = true) {
+                                bool signed_values = true, bool owner = false) {
   const i64 b = offsets[g], e = offsets[g + 1];
   double s = 0.0;
-  for (i64 k = b; k < e; ++k) {
+  for (i64 k = b; k < (owner ? b + 1 : e); ++k) {
     const i64 c = entries[k];
     const double v = (c & 2) ? recv[c >> 2] : y[c >> 2];
     s += (signed_values && (c & 1)) ? -v : v;
@@ -125,9 +127,12 @@ public:
   // orientation signs ignored, for operator diagonals). Collective: every
   // rank calls it, also ranks without cross-rank carriers.
   void run(double* y, cudaStream_t stream, bool signed_values = true);
+  // ghost update: every copy of a cross-rank carrier := its owner's value
+  void broadcast_owner(double* y, cudaStream_t stream);
   const ExchangePlan& plan() const { return plan_; }
 
 private:
+  void run_mode(double* y, cudaStream_t stream, bool signed_values, bool owner);
   ExchangePlan plan_;
   Transport* transport_;
   i64* d_send_index_ = nullptr;

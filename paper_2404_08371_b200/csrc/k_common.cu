@@ -192,6 +192,50 @@ __global__ void export_ref_kernel(const double* lat, const i64* map, i64 total, 
   ref[e >> 2] = (e & 2) ? -v : v;
 }
 
+// Owned slice [lo, hi) of the reference numbering (one rank's share): import
+// sets every local copy of an owned carrier (others are ghosts, filled by the
+// owner broadcast below); export writes the owner copies.
+__global__ void import_ref_range_kernel(double* lat, const i64* map, i64 total, const double* ref, i64 lo, i64 hi) {
+  const i64 tid = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (tid >= total) return;
+  const i64 e = map[tid];
+  if (e < 0) {
+    lat[tid] = 0.0;
+    return;
+  }
+  const i64 id = e >> 2;
+  if (id < lo || id >= hi) return;
+  const double v = ref[id - lo];
+  lat[tid] = (e & 2) ? -v : v;
+}
+
+__global__ void export_ref_range_kernel(const double* lat, const i64* map, i64 total, double* ref, i64 lo, i64 hi) {
+  const i64 tid = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (tid >= total) return;
+  const i64 e = map[tid];
+  if (e < 0 || !(e & 1)) return;
+  const i64 id = e >> 2;
+  if (id < lo || id >= hi) return;
+  const double v = lat[tid];
+  ref[id - lo] = (e & 2) ? -v : v;
+}
+
+// Ghost update of rank-local interface groups: every copy takes the owner
+// copy's value (the first copy: copies are sorted by macro id, the owner is
+// the lowest), with its orientation sign.
+__global__ void interface_owner_kernel(double* y, const i64* offsets, const i64* copies, i64 ngroups) {
+  const i64 g = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (g >= ngroups) return;
+  const i64 b = offsets[g], e = offsets[g + 1];
+  const i64 c0 = copies[b];
+  const double v0 = y[c0 >> 1];
+  const double s = (c0 & 1) ? -v0 : v0;
+  for (i64 k = b + 1; k < e; ++k) {
+    const i64 c = copies[k];
+    y[c >> 1] = (c & 1) ? -s : s;
+  }
+}
+
 // K4: one thread per shared carrier; copies are summed in macro-id order so
 // every copy receives a bitwise-identical total.
 // SIGNED: ND1 copies carry their orientation sign relative to the owner;
@@ -307,6 +351,24 @@ void launch_import_ref(double* lat, const i64* map, i64 total, const double* ref
 void launch_export_ref(const double* lat, const i64* map, i64 total, double* ref, cudaStream_t s) {
   export_ref_kernel<<<grid_for(total), kThreads, 0, s>>>(lat, map, total, ref);
   check_launch("export_ref");
+}
+
+void launch_import_ref_range(double* lat, const i64* map, i64 total, const double* ref, i64 lo, i64 hi,
+                             cudaStream_t s) {
+  import_ref_range_kernel<<<grid_for(total), kThreads, 0, s>>>(lat, map, total, ref, lo, hi);
+  check_launch("import_ref_range");
+}
+
+void launch_export_ref_range(const double* lat, const i64* map, i64 total, double* ref, i64 lo, i64 hi,
+                             cudaStream_t s) {
+  export_ref_range_kernel<<<grid_for(total), kThreads, 0, s>>>(lat, map, total, ref, lo, hi);
+  check_launch("export_ref_range");
+}
+
+void launch_interface_owner(double* y, const i64* offsets, const i64* copies, i64 ngroups, cudaStream_t s) {
+  if (ngroups <= 0) return;
+  interface_owner_kernel<<<grid_for(ngroups), kThreads, 0, s>>>(y, offsets, copies, ngroups);
+  check_launch("interface_owner");
 }
 
 void launch_interface_sum(double* y, const i64* offsets, const i64* copies, i64 ngroups, cudaStream_t s,

@@ -292,6 +292,17 @@ Context::LevelData& Context::ref_level(Space s, int level) {
   if (!ld.ref) {
     ld.ref = std::make_unique<RefNumbering>(build_ref_numbering(mesh_, topo_, ld.lay));
     ld.ref_map.upload(ld.ref->map.data(), ld.ref->map.size(), stream_);
+    // owned ids are contiguous: the numbering sorts by owner macro first
+    // (fespace.cpp:283-295) and ranks hold contiguous macro ranges
+    i64 lo = -1, hi = -1;
+    for (i64 e : ld.ref->map)
+      if (e >= 0 && (e & 1)) {
+        const i64 id = e >> 2;
+        lo = lo < 0 ? id : std::min(lo, id);
+        hi = std::max(hi, id + 1);
+      }
+    ld.ref_lo = lo < 0 ? 0 : lo;
+    ld.ref_hi = lo < 0 ? 0 : hi;
   }
   return ld;
 }
@@ -361,6 +372,43 @@ void Function::import_ref_device(int level, const double* dev_ref) {
 void Function::export_ref_device(int level, double* dev_ref) {
   auto& ld = ctx_->ref_level(space_, level);
   launch_export_ref(data(level), ld.ref_map.get(), ld.lay.total(), dev_ref, ctx_->stream());
+}
+
+void Function::owned_ref_range(int level, i64* lo, i64* hi) {
+  if (ctx_->partition() == Context::kPartitionSlab)
+    fail_arg("owned reference slices: macro partitions only (a slab rank owns scattered ids)");
+  auto& ld = ctx_->ref_level(space_, level);
+  *lo = ld.ref_lo;
+  *hi = ld.ref_hi;
+}
+
+void Function::import_ref_owned(int level, const double* host_owned) {
+  i64 lo = 0, hi = 0;
+  owned_ref_range(level, &lo, &hi);
+  auto& ld = ctx_->ref_level(space_, level);
+  const cudaStream_t s = ctx_->stream();
+  if (ld.ref_io.size() < static_cast<std::size_t>(hi - lo)) ld.ref_io.reset(static_cast<std::size_t>(hi - lo));
+  double* p = data(level);
+  if (hi > lo)
+    TETMF_CUDA(cudaMemcpyAsync(ld.ref_io.get(), host_owned, (hi - lo) * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (ld.lay.total() > 0) launch_import_ref_range(p, ld.ref_map.get(), ld.lay.total(), ld.ref_io.get(), lo, hi, s);
+  // ghost copies := owner values: rank-local groups, then across ranks
+  launch_interface_owner(p, ld.group_offsets.get(), ld.group_copies.get(), ld.groups.num_groups(), s);
+  if (ld.exchange) ld.exchange->broadcast_owner(p, s);
+  ctx_->synchronize();
+}
+
+void Function::export_ref_owned(int level, double* host_owned) {
+  i64 lo = 0, hi = 0;
+  owned_ref_range(level, &lo, &hi);
+  auto& ld = ctx_->ref_level(space_, level);
+  const cudaStream_t s = ctx_->stream();
+  if (ld.ref_io.size() < static_cast<std::size_t>(hi - lo)) ld.ref_io.reset(static_cast<std::size_t>(hi - lo));
+  if (ld.lay.total() > 0)
+    launch_export_ref_range(data(level), ld.ref_map.get(), ld.lay.total(), ld.ref_io.get(), lo, hi, s);
+  if (hi > lo)
+    TETMF_CUDA(cudaMemcpyAsync(host_owned, ld.ref_io.get(), (hi - lo) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  ctx_->synchronize();
 }
 
 void Function::import_ref(int level, const double* host_ref) {

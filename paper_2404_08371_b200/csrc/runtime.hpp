@@ -118,6 +118,8 @@ public:
     void interface_sum(double* y, cudaStream_t s, bool signed_values = true) const;
     std::unique_ptr<RefNumbering> ref;  // lazily, import/export only
     DeviceBuffer<i64> ref_map;
+    i64 ref_lo = 0, ref_hi = 0;         // this rank's owned slice of the reference numbering
+    DeviceBuffer<double> ref_io;        // staging of the owned slice (host I/O)
     std::unique_ptr<Exchange> exchange; // nranks > 1
     DeviceBuffer<int> tasks;            // kernel task list (per space / level)
     int ntasks = 0;
@@ -183,6 +185,12 @@ public:
   void export_ref(int level, double* host_ref);        // reference numbering out
   void import_ref_device(int level, const double* dev_ref);
   void export_ref_device(int level, double* dev_ref);
+  // multi-rank I/O in reference numbering: this rank's owned slice [lo, hi)
+  // (carriers whose owner macro -- the lowest sharing macro id -- is local);
+  // import fills the ghost copies by the owner broadcast (collective)
+  void owned_ref_range(int level, i64* lo, i64* hi);
+  void import_ref_owned(int level, const double* host_owned);
+  void export_ref_owned(int level, double* host_owned);
   i64 num_ref_dofs(int level);
 
 private:

@@ -197,3 +197,42 @@ def test_slab_partition_rejects_other_forms(tm):
     a, b = tm.Function(ctx, tm.SPACE_P1), tm.Function(ctx, tm.SPACE_P1)
     with pytest.raises(tm.InvalidArgument, match="slab partition"):
         tm.Operator(ctx, tm.FORM_N1, [a, b])
+
+
+@pytest.mark.parametrize("mesh,form,level,nranks", [("cubes2", "N1", 4, 4), ("cube6", "P1", 5, 8),
+                                                    ("cubes2", "P1K", 4, 3), ("cubes1x1x2", "N1", 4, 2)])
+def test_owned_reference_slices(tm, mesh, form, level, nranks):
+    """Multi-rank host I/O in reference numbering (tetmf_fn_import_ref_owned /
+    export_ref_owned): the ranks' owned slices tile the global vector; import
+    of the slices (ghost copies from their owners through the exchange) gives
+    every rank the single-rank storage bitwise; the exported slices of the
+    apply concatenate to the single-rank export_ref bitwise."""
+    ctx = tm.Context(mesh, device=0)
+    x, y, op, _ = _setup(tm, ctx, form, level)
+    ms, _ = ctx.layout(FORMS[form][1], level)
+    xr = x.export_ref(level)
+    op.apply(x, y, level)
+    w1 = y.export_ref(level)
+    xs1 = x.download(level).reshape(-1, ms)
+
+    group = tm.LoopbackGroup(nranks)
+    ctxs = group.contexts(mesh, device=0)
+    objs = [_setup(tm, c, form, level) for c in ctxs]
+
+    def body(r):
+        xx, yy, oo, _ = objs[r]
+        lo, hi = xx.owned_ref_range(level)
+        xx.fill_seeded(level, 999)  # overwritten by the import
+        xx.import_ref_owned(level, np.ascontiguousarray(xr[lo:hi]))
+        oo.apply(xx, yy, level)
+        return lo, hi, xx.download(level), yy.export_ref_owned(level)
+
+    out = tm.run_ranks(body, nranks)
+    pieces = sorted((lo, hi, w) for lo, hi, _, w in out)
+    assert pieces[0][0] == 0 and pieces[-1][1] == w1.size
+    for (lo, hi, _), (lo2, _, _) in zip(pieces, pieces[1:]):
+        assert hi == lo2
+    assert np.array_equal(np.concatenate([w for _, _, w in pieces]), w1)
+    for c, (_, _, xl, _) in zip(ctxs, out):
+        if c.local_macros():
+            assert np.array_equal(xl.reshape(-1, ms), xs1[c.local_macros()])
