@@ -228,7 +228,7 @@ def test_owned_reference_slices(tm, mesh, form, level, nranks):
         return lo, hi, xx.download(level), yy.export_ref_owned(level)
 
     out = tm.run_ranks(body, nranks)
-    pieces = sorted((lo, hi, w) for lo, hi, _, w in out)
+    pieces = sorted(((lo, hi, w) for lo, hi, _, w in out if hi > lo), key=lambda t: t[0])  # ranks without macros own nothing
     assert pieces[0][0] == 0 and pieces[-1][1] == w1.size
     for (lo, hi, _), (lo2, _, _) in zip(pieces, pieces[1:]):
         assert hi == lo2
