@@ -6,6 +6,8 @@
 #include <atomic>
 #include <cstring>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.hpp"
 #include "exchange.hpp"
 #include "runtime_check.hpp"
@@ -14,6 +16,13 @@ namespace tetmf {
 
 namespace {
 std::atomic<i64> g_launches{0};
+
+// NVTX range over one phase of an apply (element kernels / interface sum /
+// exchange) for nsys / ncu timelines; header-only NVTX v3, no cost without a tool
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 }
 void count_launch(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 i64 launch_count() { return g_launches.load(); }
@@ -603,8 +612,14 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
       fail_internal("kernel_apply: unsupported form");
   }
   if (ev_stop) TETMF_CUDA(cudaEventRecord(ev_stop, s));
-  ld.interface_sum(y, s);
-  if (ld.exchange) ld.exchange->run(y, s);
+  {
+    NvtxRange r("tetmf interface sum (K4)");
+    ld.interface_sum(y, s);
+  }
+  if (ld.exchange) {
+    NvtxRange r("tetmf exchange");
+    ld.exchange->run(y, s);
+  }
 }
 
 void Operator::debug_perturb_table(int level, i64 index, double delta) {
@@ -719,6 +734,7 @@ double* Operator::ref_scratch(i64 count) {
 }
 
 void Operator::apply(const Function& src, Function& dst, int level, Update upd) {
+  NvtxRange r(info().name);
   check(src, dst, level);
   const double* x = src.data(level);
   if (upd == Update::Replace) {
