@@ -197,6 +197,10 @@ constexpr OrientConsts make_orient_consts() {
 }
 __constant__ OrientConsts kOc = make_orient_consts();
 
+#ifndef TETMF_P2V_OUNROLL
+#define TETMF_P2V_OUNROLL 1  // orientation loop unroll (full unroll overflows the instruction cache)
+#endif
+constexpr int kOUnroll = TETMF_P2V_OUNROLL;
 #ifndef TETMF_P2V_MINB
 #define TETMF_P2V_MINB 1
 #endif
@@ -266,7 +270,7 @@ p2v_cubes2_kernel(const double* __restrict__ x, const double* __restrict__ kc, d
 #endif
   // orientations valid by anchor sum (orient_sum_limit): WU s <= n-1
   // (always), BU BD GU GD s <= n-2, WD s <= n-3
-#pragma unroll 1
+#pragma unroll kOUnroll
   for (int o = 0; o < 6; ++o) {
     if (s > (o == WU ? n - 1 : o == WD ? n - 3 : n - 2)) continue;
     double xv[10], kv[10], g[10];
