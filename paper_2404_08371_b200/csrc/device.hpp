@@ -84,13 +84,14 @@ void launch_p1_stencil8(const double* x, double* y, const int* d_tasks, int ntas
 void launch_p1_stencil10(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
                          int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
 // K3 v2: cube walk, two layer-parity passes, one launch per geometry group
-void build_n1_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out);
+void build_n1_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out, int chunk);
 // K3 default: folded cube walk (k_n1_fold.cu); same task-list / launch contract
-void build_n1_fold_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out);
+void build_n1_fold_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out, int chunk);
+int n1_fold_chunk(const std::vector<int>& local_macros, int n, int sms);
 void pad_n1_fold_tasks(std::vector<int>& tasks);
 void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, const double* x, const double* alpha,
                     const double* beta, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
-                    i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s);
+                    i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s, int chunk);
 int n1_kernel_mode();
 // K2 default: the gather walked along y with register windows (k_p1k_gather.cu)
 void build_p1k_walk_tasks(int nmacros, int n, std::vector<int>& out);

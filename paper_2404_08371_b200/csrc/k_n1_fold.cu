@@ -124,7 +124,7 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram,
                const MacroDesc* __restrict__ macros,
                const double* __restrict__ xin, const double* __restrict__ alpha, const double* __restrict__ beta,
                double* __restrict__ yout, const FoldTask* __restrict__ tasks, int ntasks, i64 stride, i64 cstride,
-               i64 cf_stride, int n) {
+               i64 cf_stride, int n, int chunk) {
   extern __shared__ __align__(16) double dsm[];
   N1GramTable& sg = *reinterpret_cast<N1GramTable*>(dsm);
   // one launch covers every geometry group of a pass; task lists are padded
@@ -161,7 +161,7 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram,
   const int nsteps = paired ? D + 2 : L - x0 + 1;
   const int t0 = tk.t0;
   const int ts = t0 > 0 ? t0 - 1 : 0;  // halo step: restores the carried sums
-  const int te = min(t0 + kChunk, nsteps);
+  const int te = min(t0 + chunk, nsteps);
 
   const int cs = static_cast<int>(cstride);
   const double* __restrict__ Xm = xin + static_cast<i64>(tk.macro) * stride;
@@ -386,8 +386,10 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram,
 
 // Task list of one level and parity pass: (macro, z, k, t0) per layer z of
 // the parity, segment pair (k, K-1-k) or unpaired segment, and chunk of
-// kChunk steps.
-void build_n1_fold_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out) {
+// `chunk` steps (kChunk by default; fewer for small levels, where the
+// chunks are the parallelism).
+void build_n1_fold_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out,
+                         int chunk) {
   out.clear();
   for (int z = parity; z <= n - 1; z += 2) {
     const int L = n - 1 - z, K = (L + 1) / kSeg;  // full segments
@@ -396,7 +398,7 @@ void build_n1_fold_tasks(const std::vector<int>& local_macros, int n, int parity
       if (k < K && K - 1 - k < k) continue;        // far half of a pair
       const bool paired = k < K && K - 1 - k > k;
       const int nsteps = paired ? 2 * L + 6 - kSeg * K : L - kSeg * k + 1;
-      for (int t0 = 0; t0 < nsteps; t0 += kChunk)
+      for (int t0 = 0; t0 < nsteps; t0 += chunk)
         for (int li : local_macros) {
           out.push_back(li);
           out.push_back(z);
@@ -420,9 +422,10 @@ void pad_n1_fold_tasks(std::vector<int>& tasks) {
 // gram: tables of all geometry groups; macros: local macro descriptors
 void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, const double* x, const double* alpha,
                     const double* beta, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
-                    i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s) {
+                    i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s, int chunk) {
   if (ntasks == 0) return;
   if (rule < 0 || rule > 2) fail_internal("n1_fold: rule index out of range");
+  if (chunk < 1) fail_internal("n1_fold: chunk < 1");
   constexpr int smem = static_cast<int>(sizeof(N1GramTable) + sizeof(double) * kWarpSmem * kWarps);
   using K = decltype(&n1_fold_kernel<0, 0>);
   static const K kerns[2][3] = {{n1_fold_kernel<0, 0>, n1_fold_kernel<0, 1>, n1_fold_kernel<0, 2>},
@@ -440,15 +443,30 @@ void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, 
   const unsigned grid = static_cast<unsigned>((ntasks + kWarps - 1) / kWarps);
   kerns[pass][rule]<<<grid, 32 * kWarps, smem, s>>>(gram, macros, x, alpha, beta, y,
                                                     reinterpret_cast<const FoldTask*>(d_tasks), ntasks, macro_stride,
-                                                    class_stride, coeff_stride, n);
+                                                    class_stride, coeff_stride, n, chunk);
   check_launch("n1_fold");
 }
 
 // the N1 apply is the fold kernel; task lists per geometry group and pass
 int n1_kernel_mode() { return 3; }
 
-void build_n1_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out) {
-  build_n1_fold_tasks(local_macros, n, parity, out);
+void build_n1_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out, int chunk) {
+  build_n1_fold_tasks(local_macros, n, parity, out, chunk);
+}
+
+// Steps per fold task for a level: kChunk, halved while one pass would not
+// give every SM several waves of warps (small meshes / small per-GPU shares
+// under strong scaling); each halving adds a halo step per 8-32 steps but
+// multiplies the tasks.
+int n1_fold_chunk(const std::vector<int>& local_macros, int n, int sms) {
+  std::vector<int> t;
+  int chunk = kChunk;
+  while (chunk > 8) {
+    build_n1_fold_tasks(local_macros, n, 0, t, chunk);
+    if (static_cast<long long>(t.size() / 4) >= 4LL * 12 * sms) break;
+    chunk /= 2;
+  }
+  return chunk;
 }
 
 } // namespace tetmf

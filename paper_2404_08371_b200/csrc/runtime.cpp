@@ -192,13 +192,20 @@ Context::LevelData& Context::level(Space s, int level) {
     ld->p1k_walk.upload(tasks.data(), tasks.size(), stream_);
   } else if (s == Space::ND1) {
     std::vector<int> all, part;
+    {
+      int sms = 148;
+      TETMF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+      std::vector<int> locals(macros_.size());
+      for (std::size_t li = 0; li < macros_.size(); ++li) locals[li] = static_cast<int>(li);
+      ld->fold_chunk = n1_fold_chunk(locals, n, sms);
+    }
     ld->group_tasks.assign(ngroups_, {0, 0, 0, 0});
     for (int g = 0; g < ngroups_; ++g) {
       std::vector<int> members;
       for (std::size_t li = 0; li < macros_.size(); ++li)
         if (group_[li] == g) members.push_back(static_cast<int>(li));
       for (int pass = 0; pass < 2; ++pass) {
-        build_n1_tasks(members, n, pass, part);
+        build_n1_tasks(members, n, pass, part, ld->fold_chunk);
         ld->group_tasks[g][2 * pass] = static_cast<int>(all.size() / 4);
         ld->group_tasks[g][2 * pass + 1] = static_cast<int>(part.size() / 4);
         all.insert(all.end(), part.begin(), part.end());
@@ -596,7 +603,7 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
         for (int pass = 0; pass < 2; ++pass)
           launch_n1_fold(t.n1g.get(), ld.macros.get(), pass, x, coeffs_[0]->data(level), coeffs_[1]->data(level), y,
                          ld.fold_tasks.get() + 4 * ld.fold_range[2 * pass], ld.fold_range[2 * pass + 1],
-                         ld.lay.macro_stride, ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, rule, s);
+                         ld.lay.macro_stride, ld.lay.class_stride, cl.lay.macro_stride, ld.lay.n, rule, s, ld.fold_chunk);
       }
       break;
     }

@@ -144,6 +144,7 @@ public:
     // ND1, folded kernel: per pass, all groups' tasks padded to whole CTAs
     DeviceBuffer<int> fold_tasks;
     std::array<int, 4> fold_range{0, 0, 0, 0};    // {offset0, count0, offset1, count1}
+    int fold_chunk = 32;                          // steps per fold task (n1_fold_chunk)
     std::vector<std::array<int, 4>> fold_group_range;  // per geometry group, same layout
   };
   LevelData& level(Space s, int level);
