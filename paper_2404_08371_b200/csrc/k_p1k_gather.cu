@@ -152,6 +152,9 @@ p1k_gather_kernel(const double* __restrict__ x, const double* __restrict__ kc, d
 #ifndef TETMF_P1K_SMEMK
 #define TETMF_P1K_SMEMK 1  // 0: the 36 K entries in registers (230 registers, 8 warps/SM; measured slower)
 #endif
+#ifndef TETMF_P1K_PF2
+#define TETMF_P1K_PF2 0  // 1: fresh window slots prefetched two steps ahead
+#endif
 #ifndef TETMF_P1K_MINB
 #define TETMF_P1K_MINB 3  // CTAs per SM the register budget is sized for (168 registers)
 #endif
@@ -241,8 +244,16 @@ p1k_walk_kernel(const double* __restrict__ x, const double* __restrict__ kc, dou
   // shift from the row above)
   auto fresh = [](int q) { return used(q) && !((q / 3) % 3 < 2 && used(q + 3)); };
   double xv[27], kv[27], nx[27], nk[27];
+#if TETMF_P1K_PF2
+  double mx[27], mk[27];  // second prefetch stage: fresh slots two steps ahead
+#endif
 #pragma unroll
-  for (int q = 0; q < 27; ++q) xv[q] = kv[q] = nx[q] = nk[q] = 0.0;
+  for (int q = 0; q < 27; ++q) {
+    xv[q] = kv[q] = nx[q] = nk[q] = 0.0;
+#if TETMF_P1K_PF2
+    mx[q] = mk[q] = 0.0;
+#endif
+  }
   auto load = [&](double& xo, double& ko, int zz, int r, int dxo) {
     const int a = rowstart(zz, r) + px + dxo;
     xo = __ldg(xm + a);
@@ -258,6 +269,13 @@ p1k_walk_kernel(const double* __restrict__ x, const double* __restrict__ kc, dou
     for (int q = 0; q < 27; ++q)
       if (fresh(q)) load(nx[q], nk[q], pz + q / 9 - 1, t.y + 1 + (q / 3) % 3 - 1, q % 3 - 1);
   }
+#if TETMF_P1K_PF2
+  if (t.y + 2 < yend) {
+#pragma unroll
+    for (int q = 0; q < 27; ++q)
+      if (fresh(q)) load(mx[q], mk[q], pz + q / 9 - 1, t.y + 2 + (q / 3) % 3 - 1, q % 3 - 1);
+  }
+#endif
   for (int py = t.y; py < yend; ++py) {
     const int s = px + py + pz;
     double W[27];
@@ -271,23 +289,35 @@ p1k_walk_kernel(const double* __restrict__ x, const double* __restrict__ kc, dou
       if (used(q) && q != slot(0, 0, 0)) acc = fma(W[q], xv[q] - xc, acc);
     ym[rowstart(pz, py) + px] = acc;
     // move the window up one row: dy = -1 <- 0, dy = 0 <- +1 where both are
-    // used slots, the fresh slots from the prefetch; then prefetch row py + 2
+    // used slots, the fresh slots from the prefetch; then prefetch ahead
 #pragma unroll
     for (int q = 0; q < 27; ++q) {
       if (!used(q)) continue;
       if (fresh(q)) {
         xv[q] = nx[q];
         kv[q] = nk[q];
+#if TETMF_P1K_PF2
+        nx[q] = mx[q];
+        nk[q] = mk[q];
+#endif
       } else {
         xv[q] = xv[q + 3];
         kv[q] = kv[q + 3];
       }
     }
+#if TETMF_P1K_PF2
+    if (py + 3 < yend) {
+#pragma unroll
+      for (int q = 0; q < 27; ++q)
+        if (fresh(q)) load(mx[q], mk[q], pz + q / 9 - 1, py + 3 + (q / 3) % 3 - 1, q % 3 - 1);
+    }
+#else
     if (py + 2 < yend) {
 #pragma unroll
       for (int q = 0; q < 27; ++q)
         if (fresh(q)) load(nx[q], nk[q], pz + q / 9 - 1, py + 2 + (q / 3) % 3 - 1, q % 3 - 1);
     }
+#endif
   }
 }
 
