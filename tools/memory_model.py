@@ -10,7 +10,7 @@ the B200 L2) against the DRAM bytes ncu measured (committed profiles).
            (bytes the whole GPU touches between two uses of the same data)
            fits in the 126 MB L2; otherwise it is reloaded
 
-usage: python tools/memory_model.py  (prints the table in profiles/r1_memory_model.txt)
+usage: python tools/memory_model.py  (prints the table in profiles/r2_memory_model.txt)
 """
 
 L2 = 126e6  # bytes (B200)
@@ -79,11 +79,28 @@ def p2v(macros, level, measured):
                 lower=lower, upper=upper, lc=lc, tail=tail, measured=measured)
 
 
+def k2(macros, level, measured):
+    """P1 -div(k grad) column walk (k_p1k_gather.cu p1k_walk_kernel). A warp
+    walks 32 rows of one plane; its window holds rows y-1..y+1 of planes
+    z-1..z+1 (x and k). Plane z is read as the centre plane by its own tasks
+    and as a neighbour plane by the tasks of z-1 and z+1; tasks run z-major,
+    so the tail between those reads is about two planes of x and k of the
+    whole mesh (6 macros x ~n^2/2 points x 16 B), below L2 at L8."""
+    n, pts, _, elems = sizes(macros, level)
+    lower = 8.0 * 3 * pts                 # x, k read once, y written once
+    upper = 8.0 * elems * (4 + 4 + 2 * 4)
+    tail = 2 * macros * (n * n / 2) * 16.0
+    lc = lower if tail < L2 else 8.0 * (3 * 2 + 1) * pts
+    return dict(kernel="K2 P1K column walk", config=f"cube6 L{level}", lower=lower, upper=upper, lc=lc, tail=tail,
+                measured=measured)
+
+
 ROWS = [
     # measured: ncu dram__bytes_read.sum + dram__bytes_write.sum of the kernel launch(es) of one apply
     k1(6, 8, (138.851328e6 + 100.060416e6, "profiles/r1_k1_rowwalk_ncu_summary.txt")),
     k3(48, 8, (34092914432.0, "profiles/r1_traffic.json (both pass launches, ncu --set full)")),
     p2v(6, 7, (413.534720e6 + 112.126208e6, "profiles/r1_p2v_v2_ncu_summary.txt")),
+    k2(6, 8, (275.180288e6 + 117.081600e6, "profiles/r2_k2_walk_ncu_summary.txt")),
 ]
 
 
