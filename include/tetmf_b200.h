@@ -276,6 +276,9 @@ int tetmf_plan_stencil(tetmf_ctx* ctx, int level, int macro, double* out);
 /* FP64 DFMA-chain peak probe: returns the sustained FP64 TFLOP/s measured
  * on the context's device (bench.py roofline denominator). */
 int tetmf_measure_fp64_peak(tetmf_ctx* ctx, double seconds, double* tflops);
+/* the same, also returning the sustained rate: flops / time over the second
+ * half of the window (clocks settled under the power cap) */
+int tetmf_measure_fp64_peak2(tetmf_ctx* ctx, double seconds, double* burst_tflops, double* sustained_tflops);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

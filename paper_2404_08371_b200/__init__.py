@@ -107,6 +107,7 @@ _SIGS = {
     "tetmf_host_pack": (ctypes.c_int, [_c_dp, _c_i64p, ctypes.c_int64, _c_dp]),
     "tetmf_host_combine": (ctypes.c_int, [_c_dp, _c_dp, _c_i64p, _c_i64p, ctypes.c_int64]),
     "tetmf_measure_fp64_peak": (ctypes.c_int, [_c_vp, ctypes.c_double, _c_dp]),
+    "tetmf_measure_fp64_peak2": (ctypes.c_int, [_c_vp, ctypes.c_double, _c_dp, _c_dp]),
     "tetmf_plan_local_matrix": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                _c_dp, _c_dp, _c_dp]),
     "tetmf_plan_stencil": (ctypes.c_int, [_c_vp, ctypes.c_int, ctypes.c_int, _c_dp]),
@@ -391,6 +392,12 @@ class Context:
         tf = ctypes.c_double()
         _check(lib().tetmf_measure_fp64_peak(self._h, seconds, ctypes.byref(tf)))
         return tf.value
+
+    def fp64_peak2(self, seconds: float = 4.0) -> tuple[float, float]:
+        """(burst, sustained) FP64 TFLOP/s of the DFMA-chain probe."""
+        b, s = ctypes.c_double(), ctypes.c_double()
+        _check(lib().tetmf_measure_fp64_peak2(self._h, seconds, ctypes.byref(b), ctypes.byref(s)))
+        return b.value, s.value
 
 
 class Function:

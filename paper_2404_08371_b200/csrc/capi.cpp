@@ -792,6 +792,10 @@ int tetmf_plan_stencil(tetmf_ctx* ctx, int level, int macro, double* out /* 16 x
 }
 
 int tetmf_measure_fp64_peak(tetmf_ctx* ctx, double seconds, double* tflops) {
+  return tetmf_measure_fp64_peak2(ctx, seconds, tflops, nullptr);
+}
+
+int tetmf_measure_fp64_peak2(tetmf_ctx* ctx, double seconds, double* tflops, double* sustained) {
   return guard([&] {
     need(ctx, "ctx");
     need(tflops, "tflops");
@@ -805,8 +809,9 @@ int tetmf_measure_fp64_peak(tetmf_ctx* ctx, double seconds, double* tflops) {
     TETMF_CUDA(cudaEventCreate(&e0));
     TETMF_CUDA(cudaEventCreate(&e1));
     launch_fp64_peak(out.get(), blocks, threads, 64, c.stream());  // warm-up
-    double best = 0.0;
+    double best = 0.0, late_flops = 0.0, late_ms = 0.0;
     const auto t0 = std::chrono::steady_clock::now();
+    double elapsed = 0.0;
     do {
       TETMF_CUDA(cudaEventRecord(e0, c.stream()));
       launch_fp64_peak(out.get(), blocks, threads, iters, c.stream());
@@ -817,10 +822,16 @@ int tetmf_measure_fp64_peak(tetmf_ctx* ctx, double seconds, double* tflops) {
       const double flops = 2.0 * 8.0 * 16.0 * double(iters) * double(blocks) * double(threads);
       const double tf = flops / (ms * 1e-3) / 1e12;
       if (tf > best) best = tf;
-    } while (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() < seconds);
+      elapsed = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (elapsed >= 0.5 * seconds) {  // second half: the power / clock steady state
+        late_flops += flops;
+        late_ms += ms;
+      }
+    } while (elapsed < seconds);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     *tflops = best;
+    if (sustained) *sustained = late_ms > 0 ? late_flops / (late_ms * 1e-3) / 1e12 : best;
   });
 }
 
