@@ -89,6 +89,26 @@ public:
   // wait for the peers' copies out of OUR send buffer (so the next pack on
   // this stream cannot overwrite it while a peer still reads it)
   void exchange(const ExchangeIO& io, cudaStream_t s) override {
+    guarded([&] { exchange_impl(io, s); });
+  }
+  void allgather(const double* d_in, double* d_out, int count, cudaStream_t s) override {
+    guarded([&] { allgather_impl(d_in, d_out, count, s); });
+  }
+
+private:
+  // a rank that fails inside a collective step releases its peers from the
+  // barriers at once (they throw "aborted") instead of leaving them to the timeout
+  template <typename F>
+  void guarded(F&& f) {
+    try {
+      f();
+    } catch (...) {
+      hub_->barrier().abort();
+      throw;
+    }
+  }
+
+  void exchange_impl(const ExchangeIO& io, cudaStream_t s) {
     int dev = 0;
     TETMF_CUDA(cudaGetDevice(&dev));
     hub_->ensure_events(rank_, dev);
@@ -120,7 +140,7 @@ public:
     finish(*io.peers, s);
   }
 
-  void allgather(const double* d_in, double* d_out, int count, cudaStream_t s) override {
+  void allgather_impl(const double* d_in, double* d_out, int count, cudaStream_t s) {
     int dev = 0;
     TETMF_CUDA(cudaGetDevice(&dev));
     hub_->ensure_events(rank_, dev);
@@ -141,6 +161,7 @@ public:
     finish(all, s);
   }
 
+public:
   std::string describe() const override {
     return "loopback virtual rank " + std::to_string(rank_) + " of " + std::to_string(nranks()) +
            " (device-to-device copies on one GPU)";
