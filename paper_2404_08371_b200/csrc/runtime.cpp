@@ -190,6 +190,9 @@ Context::LevelData& Context::level(Space s, int level) {
     build_p1k_walk_tasks(static_cast<int>(macros_.size()), n, tasks);
     ld->np1k_walk = static_cast<int>(tasks.size() / 4);
     ld->p1k_walk.upload(tasks.data(), tasks.size(), stream_);
+    build_p1k_cube_tasks(static_cast<int>(macros_.size()), n, tasks);
+    ld->np1k_cube = static_cast<int>(tasks.size() / 4);
+    ld->p1k_cube.upload(tasks.data(), tasks.size(), stream_);
   } else if (s == Space::ND1) {
     std::vector<int> all, part;
     {
@@ -553,7 +556,7 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
     fail_arg("slab partition: the default K1 kernel only");
   if ((form_ == Form::P1Diffusion && kernel_variant_ >= 2 && kernel_variant_ <= 4) ||
       (form_ == Form::N1CurlCurlMass && kernel_variant_ >= 2) || (form_ == Form::P2VDiffusion && kernel_variant_ >= 2) ||
-      (form_ == Form::P1KDiffusion && kernel_variant_ >= 3))
+      (form_ == Form::P1KDiffusion && kernel_variant_ >= 4))
     fail_arg("kernel variant " + std::to_string(kernel_variant_) + " does not exist for this form");
   if (form_ == Form::P1Diffusion && kernel_variant_ >= 2) ctx_->ensure_p1_variant_tasks(ld);
   switch (form_) {
@@ -589,8 +592,11 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
       else if (kernel_variant_ == 2)  // round-1 default: one 32-point row segment per warp
         launch_p1k_gather(x, coeffs_[0]->data(level), y, ld.p1k_tasks.get(), ld.np1k_tasks, ld.lay.macro_stride,
                           ld.lay.n, t.p1.get(), ld.macros.get(), s);
-      else
+      else if (kernel_variant_ == 3)  // round-2 first kernel: the gather walked along y
         launch_p1k_walk(x, coeffs_[0]->data(level), y, ld.p1k_walk.get(), ld.np1k_walk, ld.lay.macro_stride,
+                        ld.lay.n, t.p1.get(), ld.macros.get(), s);
+      else
+        launch_p1k_cube(x, coeffs_[0]->data(level), y, ld.p1k_cube.get(), ld.np1k_cube, ld.lay.macro_stride,
                         ld.lay.n, t.p1.get(), ld.macros.get(), s);
       break;
     case Form::N1CurlCurlMass: {

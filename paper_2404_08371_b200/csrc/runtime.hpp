@@ -133,7 +133,9 @@ public:
     DeviceBuffer<int> zrange;           // slab partition: per local macro {za, zb} computed here
     DeviceBuffer<int> p1k_tasks;        // P1: row tasks of the P1K gather kernel (K2 round 1, diagonal)
     int np1k_walk = 0;
-    DeviceBuffer<int> p1k_walk;         // P1: column-walk tasks of the P1K walk kernel (K2)
+    DeviceBuffer<int> p1k_walk;         // P1: column-walk tasks of the P1K walk kernel (K2 variant 3)
+    int np1k_cube = 0;
+    DeviceBuffer<int> p1k_cube;         // P1: cube-walk tasks of the P1K cube kernel (K2 default)
     int np1k_tasks = 0;
     // solver (solver.hpp): per local macro, [support mask] -> {bit 0 interior,
     // bit 1 owner copy}; reduction scratch

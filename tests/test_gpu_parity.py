@@ -131,6 +131,38 @@ def test_optimized_vs_first_version(tm, mesh, form, level):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mesh,level", [("cube6", 8), ("single-tet", 9), ("cubes2", 6), ("cubes1x1x2", 5),
+                                        ("single-tet", 1), ("single-tet", 0)])
+def test_p1k_cube_kernel_vs_walk_and_gather(tm, mesh, level):
+    """K2: the default cube walk (per-cube edge weights, dynamic task queue)
+    against the round-2 row walk (variant 3) and the round-1 per-point gather
+    (variant 2) on identical inputs, every stored value overwritten (scribbled
+    outputs), and bitwise repeatable over launches (the task counters reset
+    themselves; each vertex is summed by one task in a fixed order)."""
+    ctx = tm.Context(mesh, device=0)
+    x, k = tm.Function(ctx, tm.SPACE_P1), tm.Function(ctx, tm.SPACE_P1)
+    x.fill_seeded(level, 21)
+    k.fill_coefficient(level, tm.COEFF_K)
+    op = tm.Operator(ctx, tm.FORM_P1K, [k])
+    outs = {}
+    for v in (0, 3, 2):
+        y = tm.Function(ctx, tm.SPACE_P1)
+        y.fill_seeded(level, 77)
+        op.set_variant(v)
+        op.apply(x, y, level)
+        outs[v] = y.download(level)
+    scale = np.abs(outs[2]).max()
+    assert np.abs(outs[0] - outs[3]).max() <= 1e-13 * scale
+    assert np.abs(outs[0] - outs[2]).max() <= 1e-13 * scale
+    op.set_variant(0)
+    y = tm.Function(ctx, tm.SPACE_P1)
+    for rep in range(3):
+        y.fill_seeded(level, 100 + rep)
+        op.apply(x, y, level)
+        assert np.array_equal(y.download(level), outs[0]), f"launch {rep} differs"
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("variant", [5, 7, 8, 9, 10])
 @pytest.mark.parametrize("mesh,level", [("cube6", 8), ("single-tet", 7), ("cubes2", 6), ("cubes1x1x2", 5),
                                         ("single-tet", 2)])
