@@ -47,12 +47,16 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 namespace tetmf {
 
 namespace {
 
-constexpr int kCWarps = 4;
+#ifndef TETMF_P1KC_WARPS
+#define TETMF_P1KC_WARPS 2  // warps per CTA
+#endif
+constexpr int kCWarps = TETMF_P1KC_WARPS;
 #ifndef TETMF_P1KC_ROWS
 #define TETMF_P1KC_ROWS 16  // C: cube rows per task (one halo row per task)
 #endif
@@ -60,9 +64,18 @@ constexpr int kCWarps = 4;
 #define TETMF_P1KC_LAYERS 16  // Z: layers per task (one halo layer per task)
 #endif
 #ifndef TETMF_P1KC_MINB
-#define TETMF_P1KC_MINB 3  // CTAs per SM the register budget is sized for
+#define TETMF_P1KC_MINB 4  // CTAs per SM the register budget is sized for (8 warps)
+#endif
+#ifndef TETMF_P1KC_PAIR
+#define TETMF_P1KC_PAIR 1  // 1: two layers per step (cubes z and z + 1 share the table loads)
+#endif
+#ifndef TETMF_P1KC_SPLIT
+#define TETMF_P1KC_SPLIT 1  // 1: separate accumulators for the upper cube of a pair
 #endif
 constexpr int kRows = TETMF_P1KC_ROWS;
+constexpr bool kPair = TETMF_P1KC_PAIR != 0;
+constexpr int kPl = kPair ? 3 : 2;  // planes per staged row
+constexpr int kWin = 4 * kPl;       // row window: x then k, (plane, x / x + 1) pairs
 constexpr int kLayers = TETMF_P1KC_LAYERS;
 constexpr int kSeg = 31;   // stored columns per task (lane 0 is the halo)
 constexpr int kSlots = 3;  // ring slots per warp (row issued two steps ahead)
@@ -151,28 +164,48 @@ __device__ __forceinline__ double edge_weight(const double (&kb)[6], const doubl
   return w;
 }
 
-// the cube's 19 edges into its corner sums c[0..7]
-template <int E>
-__device__ __forceinline__ void cube_edges(const double (&xv)[8], const double (&kb)[6],
-                                           const double2* __restrict__ T, double (&c)[8]) {
-  constexpr int a = kCE.a[E], b = kCE.b[E], f = kCE.first[E], l = kCE.first[E + 1], of = kCE.o[f];
+// the cube's 19 edges into its corner sums c[CO + 0 .. CO + 7]
+template <int E, int CO, int NC>
+__device__ __forceinline__ void cube_edges(const double (&xv)[NC], const double (&kb)[6],
+                                           const double2* __restrict__ T, double (&c)[NC]) {
+  constexpr int a = kCE.a[E] + CO, b = kCE.b[E] + CO, f = kCE.first[E], l = kCE.first[E + 1], of = kCE.o[f];
   double w = kb[of] * tab_at<f>(T);
   if constexpr (f + 1 < l) w = edge_weight<f + 1, l>(kb, T, w);
   const double d = xv[b] - xv[a];
   c[a] = fma(w, d, c[a]);
   c[b] = fma(-w, d, c[b]);
-  if constexpr (E + 1 < 19) cube_edges<E + 1>(xv, kb, T, c);
+  if constexpr (E + 1 < 19) cube_edges<E + 1, CO, NC>(xv, kb, T, c);
 }
 
-// A row window w[8] of one lane: x at (x, y, z), (x + 1, y, z), (x, y, z + 1),
-// (x + 1, y, z + 1), then k at the same four positions.
+// the six kbar of the cube with corner k values kv[CO + 0 .. CO + 7], 0 for
+// the orientations outside the macro (cube coordinate sum s)
+template <int CO, int NC>
+__device__ __forceinline__ void cube_kbar(const double (&kv)[NC], int s, int n, double (&kb)[6]) {
+  const double s34 = kv[CO + 3] + kv[CO + 4], s12 = kv[CO + 1] + kv[CO + 2], s56 = kv[CO + 5] + kv[CO + 6];
+  kb[WU] = s12 + (kv[CO + 0] + kv[CO + 4]);
+  kb[BU] = s34 + s12;
+  kb[BD] = s34 + (kv[CO + 2] + kv[CO + 6]);
+  kb[GU] = s34 + (kv[CO + 1] + kv[CO + 5]);
+  kb[GD] = s34 + s56;
+  kb[WD] = s56 + (kv[CO + 3] + kv[CO + 7]);
+  kb[WU] = s <= n - 1 ? kb[WU] : 0.0;
+  kb[BU] = s <= n - 2 ? kb[BU] : 0.0;
+  kb[BD] = s <= n - 2 ? kb[BD] : 0.0;
+  kb[GU] = s <= n - 2 ? kb[GU] : 0.0;
+  kb[GD] = s <= n - 2 ? kb[GD] : 0.0;
+  kb[WD] = s <= n - 3 ? kb[WD] : 0.0;
+}
+
+// A row window w[kWin] of one lane: x at (x, y, z), (x + 1, y, z), (x, y,
+// z + 1), (x + 1, y, z + 1) [, (x, y, z + 2), (x + 1, y, z + 2)], then k at
+// the same positions.
 __global__ void __launch_bounds__(32 * kCWarps, TETMF_P1KC_MINB)
 p1k_cube_kernel(const double* __restrict__ x, const double* __restrict__ kc, double* __restrict__ y,
                 const CubeTask* __restrict__ tasks, int ntasks, i64 stride, int n,
                 const P1DeviceTable* __restrict__ tabs, const MacroDesc* __restrict__ macros) {
   __shared__ __align__(16) double sT[kCWarps][36];
   __shared__ double sP[kCWarps][kRows][32];
-  __shared__ double sRing[kCWarps][kSlots][8][32];  // [warp][slot][window entry][lane]
+  __shared__ double sRing[kCWarps][kSlots][kWin][32];  // [warp][slot][window entry][lane]
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* __restrict__ P = &sP[wib][0][lane];  // this lane's column, stride 32
   const double2* __restrict__ T2 = reinterpret_cast<const double2*>(sT[wib]);
@@ -203,106 +236,151 @@ p1k_cube_kernel(const double* __restrict__ x, const double* __restrict__ kc, dou
     asm volatile("" : "+l"(xl), "+l"(kl), "+l"(yl));
     const int r0 = t.y0 == 0 ? 0 : -1;  // halo row unless the chunk starts at y = 0
     const int zs = t.z0 > 0 ? t.z0 - 1 : 0, ze = min(t.z0 + kLayers - 1, n);
-    for (int z = zs; z <= ze; ++z) {
+    for (int z = zs; z <= ze;) {
+      const bool two = kPair && z + 1 <= ze;
       const int rend = min(kRows - 1, n - z - t.x0 - t.y0);  // last row with a stored vertex
       if (rend < 0) break;                                  // and none in the layers above
-      const bool store = z >= t.z0;
-      const int len0 = n - z + 1, len1 = n - z;  // row-0 lengths of planes z, z + 1
+      const bool store0 = z >= t.z0, store1 = z + 1 >= t.z0;
+      int len[kPl];  // row-0 lengths of planes z, z + 1 (, z + 2)
+#pragma unroll
+      for (int j = 0; j < kPl; ++j) len[j] = n - z + 1 - j;
       int yy = t.y0 + r0;
       // row r of plane zz starts at plane_offset + r len - r (r - 1) / 2, so
       // row r + 1 starts len - r further
-      const int rs = yy * len0 - ((yy * (yy - 1)) >> 1), rs1 = yy * len1 - ((yy * (yy - 1)) >> 1);
-      int a0 = static_cast<int>(plane_offset(n, z)) + rs;  // (px, yy, z) relative to this lane's column
-      int gi0 = a0, gi1 = static_cast<int>(plane_offset(n, z + 1)) + rs1, rho_i = yy;  // next row to issue
+      int gi[kPl], rho_i = yy;  // next row to issue
+#pragma unroll
+      for (int j = 0; j < kPl; ++j)
+        gi[j] = static_cast<int>(plane_offset(n, z + j)) + yy * len[j] - ((yy * (yy - 1)) >> 1);
+      int a0 = gi[0], a1 = gi[1];  // (px, yy, z), (px, yy, z + 1) relative to this lane's column
       const int last = t.y0 + rend + 1;  // last row the layer reads
       // one commit group per row (empty once the layer's rows are issued):
       // the row taken is complete when at most kSlots - 2 younger groups pend
       auto issue_next = [&]() {
         if (rho_i <= last) {
-          const unsigned d = ring0 + static_cast<unsigned>(slot_i) * (8 * 32 * 8);
-          const double* s0x = xl + gi0;
-          const double* s1x = xl + gi1;
-          const double* s0k = kl + gi0;
-          const double* s1k = kl + gi1;
-          asm volatile(
-              "cp.async.ca.shared.global [%0], [%1], 8;\n"
-              "cp.async.ca.shared.global [%0+256], [%1+8], 8;\n"
-              "cp.async.ca.shared.global [%0+512], [%2], 8;\n"
-              "cp.async.ca.shared.global [%0+768], [%2+8], 8;\n"
-              "cp.async.ca.shared.global [%0+1024], [%3], 8;\n"
-              "cp.async.ca.shared.global [%0+1280], [%3+8], 8;\n"
-              "cp.async.ca.shared.global [%0+1536], [%4], 8;\n"
-              "cp.async.ca.shared.global [%0+1792], [%4+8], 8;\n" ::"r"(d),
-              "l"(s0x), "l"(s1x), "l"(s0k), "l"(s1k)
-              : "memory");
-          gi0 += len0 - rho_i;
-          gi1 += len1 - rho_i;
+          const unsigned d = ring0 + static_cast<unsigned>(slot_i) * (kWin * 32 * 8);
+#pragma unroll
+          for (int j = 0; j < kPl; ++j) {
+            const double* sx = xl + gi[j];
+            const double* sk = kl + gi[j];
+            asm volatile(
+                "cp.async.ca.shared.global [%0], [%2], 8;\n"
+                "cp.async.ca.shared.global [%0+256], [%2+8], 8;\n"
+                "cp.async.ca.shared.global [%1], [%3], 8;\n"
+                "cp.async.ca.shared.global [%1+256], [%3+8], 8;\n" ::"r"(d + 512u * j),
+                "r"(d + 512u * (kPl + j)), "l"(sx), "l"(sk)
+                : "memory");
+            gi[j] += len[j] - rho_i;
+          }
           ++rho_i;
           slot_i = slot_i == kSlots - 1 ? 0 : slot_i + 1;
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
       };
-      auto take = [&](double (&w)[8]) {
+      auto take = [&](double (&w)[kWin]) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) w[q] = sRing[wib][slot_t][q][lane];
+        for (int q = 0; q < kWin; ++q) w[q] = sRing[wib][slot_t][q][lane];
         slot_t = slot_t == kSlots - 1 ? 0 : slot_t + 1;
       };
-      double A[8], B[8];
+      double A[kWin], B[kWin];
 #pragma unroll
       for (int q = 0; q < kSlots; ++q) issue_next();
       asm volatile("cp.async.wait_group %0;" ::"n"(kSlots - 1) : "memory");
       take(A);  // row yy
       asm volatile("cp.async.wait_group %0;" ::"n"(kSlots - 2) : "memory");
       take(B);  // row yy + 1
-      // running sum of (x, y0, z): layer z - 1 only (without a halo row no step adds it)
-      double R = r0 == 0 ? P[0] : 0.0, Pn = 0.0;
-      // one cube row: lo = row yy, hi = row yy + 1; lo then receives row yy + 2
-      auto step = [&](double (&lo)[8], double(&hi)[8], int r) {
+      // running sums of (x, y0, z) (layer z - 1 only, without a halo row no
+      // step adds it) and of (x, y0, z + 1)
+      double R0 = r0 == 0 ? P[0] : 0.0, R1 = 0.0, Pn = 0.0;
+      // one cube row (one or two layers): lo = row yy, hi = row yy + 1; lo
+      // then receives row yy + 2
+      auto step = [&](auto two_c, double (&lo)[kWin], double(&hi)[kWin], int r) {
+        constexpr bool TWO = decltype(two_c)::value;
+        constexpr int NC = TWO ? 12 : 8;  // corners dx + 2 dy + 4 dz
         issue_next();
-        const double xv[8] = {lo[0], lo[1], hi[0], hi[1], lo[2], lo[3], hi[2], hi[3]};
-        const double kv[8] = {lo[4], lo[5], hi[4], hi[5], lo[6], lo[7], hi[6], hi[7]};
-        // kbar of the six elements of cube (px, yy, z), 0 outside the macro
-        const int s = px < 0 ? (1 << 29) : px + yy + z;
-        const double s34 = kv[3] + kv[4], s12 = kv[1] + kv[2], s56 = kv[5] + kv[6];
-        double kb[6];
-        kb[WU] = s12 + (kv[0] + kv[4]);
-        kb[BU] = s34 + s12;
-        kb[BD] = s34 + (kv[2] + kv[6]);
-        kb[GU] = s34 + (kv[1] + kv[5]);
-        kb[GD] = s34 + s56;
-        kb[WD] = s56 + (kv[3] + kv[7]);
-        kb[WU] = s <= n - 1 ? kb[WU] : 0.0;
-        kb[BU] = s <= n - 2 ? kb[BU] : 0.0;
-        kb[BD] = s <= n - 2 ? kb[BD] : 0.0;
-        kb[GU] = s <= n - 2 ? kb[GU] : 0.0;
-        kb[GD] = s <= n - 2 ? kb[GD] : 0.0;
-        kb[WD] = s <= n - 3 ? kb[WD] : 0.0;
-        double c[8];
-        c[0] = R;                                      // (x, y, z): layer z - 1 and row y - 1 so far
+        double xv[NC], kv[NC];
+#pragma unroll
+        for (int dz = 0; dz < NC / 4; ++dz)
+#pragma unroll
+          for (int dx = 0; dx < 2; ++dx) {
+            xv[dx + 4 * dz] = lo[2 * dz + dx], xv[dx + 2 + 4 * dz] = hi[2 * dz + dx];
+            kv[dx + 4 * dz] = lo[2 * kPl + 2 * dz + dx], kv[dx + 2 + 4 * dz] = hi[2 * kPl + 2 * dz + dx];
+          }
+        const int s = px < 0 ? (1 << 29) : px + yy + z;  // coordinate sum of cube (px, yy, z)
+        double c[NC];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) c[q] = 0.0;
+        c[0] = R0;                                     // (x, y, z): layer z - 1 and row y - 1 so far
         c[2] = r + 1 < kRows ? P[32 * (r + 1)] : 0.0;  // (x, y + 1, z): layer z - 1
-        c[4] = Pn;                                     // (x, y, z + 1): row y - 1 of this layer
-        c[1] = c[3] = c[5] = c[6] = c[7] = 0.0;
-        cube_edges<0>(xv, kb, T2, c);
-        // x + 1 corners come from the left neighbour's cube
+        if constexpr (TWO) {
+          c[4] = R1;  // (x, y, z + 1): row y - 1 so far
+          c[8] = Pn;  // (x, y, z + 2): row y - 1
+        } else {
+          c[4] = Pn;  // (x, y, z + 1): row y - 1 of this layer
+        }
+        {
+          double kb[6];
+          cube_kbar<0>(kv, s, n, kb);
+          cube_edges<0, 0>(xv, kb, T2, c);
+        }
+        if constexpr (TWO) {
+          double kb[6];
+          cube_kbar<4>(kv, s + 1, n, kb);
+#if TETMF_P1KC_SPLIT
+          // own accumulators for the upper cube: its plane z + 1 sums do not
+          // wait for the lower cube's (two independent FMA chains per corner)
+          double xu[8], u[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) xu[q] = xv[q + 4], u[q] = 0.0;
+          u[4] = c[8];
+          cube_edges<0, 0>(xu, kb, T2, u);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) c[4 + q] += u[q], c[8 + q] = u[4 + q];
+#else
+          cube_edges<0, 4>(xv, kb, T2, c);
+#endif
+        }
+        // x + 1 corners come from the left neighbour's cubes
+        const bool mine = r >= 0 && lane >= 1;
         const double l1 = __shfl_up_sync(0xffffffffu, c[1], 1), l3 = __shfl_up_sync(0xffffffffu, c[3], 1);
         const double l5 = __shfl_up_sync(0xffffffffu, c[5], 1), l7 = __shfl_up_sync(0xffffffffu, c[7], 1);
-        const double out = c[0] + l1;
-        R = c[2] + l3;
-        if (r >= 0) P[32 * r] = c[4] + l5;
-        Pn = c[6] + l7;
-        if (store && r >= 0 && lane >= 1 && s <= n) yl[a0] = out;
-        a0 += len0 - yy;
+        const double out0 = c[0] + l1;
+        R0 = c[2] + l3;
+        if (mine && store0 && s <= n) yl[a0] = out0;
+        if constexpr (TWO) {
+          const double l9 = __shfl_up_sync(0xffffffffu, c[9], 1), l11 = __shfl_up_sync(0xffffffffu, c[11], 1);
+          const double out1 = c[4] + l5;
+          R1 = c[6] + l7;
+          if (mine && store1 && s + 1 <= n) yl[a1] = out1;
+          if (r >= 0) P[32 * r] = c[8] + l9;
+          Pn = c[10] + l11;
+        } else {
+          if (r >= 0) P[32 * r] = c[4] + l5;
+          Pn = c[6] + l7;
+        }
+        a0 += len[0] - yy;
+        a1 += len[1] - yy;
         ++yy;
         if (r < rend) {
           asm volatile("cp.async.wait_group %0;" ::"n"(kSlots - 2) : "memory");
           take(lo);  // row yy + 1 of the next step
         }
       };
-      for (int r = r0;;) {
-        step(A, B, r);
-        if (++r > rend) break;
-        step(B, A, r);
-        if (++r > rend) break;
+      if (two) {
+        for (int r = r0;;) {
+          step(std::true_type{}, A, B, r);
+          if (++r > rend) break;
+          step(std::true_type{}, B, A, r);
+          if (++r > rend) break;
+        }
+        z += 2;
+      } else {
+        for (int r = r0;;) {
+          step(std::false_type{}, A, B, r);
+          if (++r > rend) break;
+          step(std::false_type{}, B, A, r);
+          if (++r > rend) break;
+        }
+        z += 1;
       }
     }
   }
