@@ -430,6 +430,9 @@ void launch_p1k_cube(const double* x, const double* k, double* y, const int* d_t
     int dev = 0, sms = 0, per_sm = 0;
     TETMF_CUDA(cudaGetDevice(&dev));
     TETMF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // registers, not the L1 / shared split, should bound the resident warps
+    TETMF_CUDA(cudaFuncSetAttribute(p1k_cube_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    cudaSharedmemCarveoutMaxShared));
     TETMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p1k_cube_kernel, 32 * kCWarps, 0));
     resident = std::max(1, sms * per_sm);
   }
