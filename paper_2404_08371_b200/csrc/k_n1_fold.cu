@@ -84,6 +84,9 @@ constexpr int kSlot = kArrays * kRow;    // doubles per ring slot
 constexpr int kRing = 3 * kSlot;         // input ring, doubles per warp
 constexpr int kRmw = 6 * 32;             // pass-1 staging slot, doubles per warp
 constexpr int kWarpSmem = kRing + kRmw;
+constexpr int kZeroTab = 6 * kGramRow + 8;         // doubles: zero table offset (+64 B bank phase)
+constexpr int kTabs = kZeroTab + 6 * kGramRow + 8;  // doubles before the warps' rings
+static_assert(sizeof(N1GramTable) == 6 * kGramRow * sizeof(double), "table layout");
 
 struct FoldTask {
   int macro, z, k, t0;  // layer, near segment, first step of the chunk
@@ -134,8 +137,14 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram,
     const N1GramTable* gt = gram + macros[tasks[blockIdx.x * kWarps].macro].group;
     for (int i = threadIdx.x; i < 6 * kGramRow; i += blockDim.x) (&sg.o[0][0])[i] = __ldg(&gt->o[0][0] + i);
   }
+  // all-zero table for elements outside the macro, 64 bytes off the real
+  // table's bank phase (a warp reading both stays conflict-free)
+  double* ztab = dsm + kZeroTab;
+  for (int i = threadIdx.x; i < 6 * kGramRow; i += blockDim.x) ztab[i] = 0.0;
+  const unsigned tab_a = static_cast<unsigned>(__cvta_generic_to_shared(dsm));
+  const unsigned zero_a = static_cast<unsigned>(__cvta_generic_to_shared(ztab));
   const int lane = threadIdx.x & 31;
-  double* ring = dsm + sizeof(N1GramTable) / sizeof(double) + (threadIdx.x >> 5) * kWarpSmem;
+  double* ring = dsm + kTabs + (threadIdx.x >> 5) * kWarpSmem;
   for (int i = lane; i < kRing; i += 32) ring[i] = 0.0;  // unfilled positions must read finite
   double* rmw = ring + kRing + lane;                     // [6][32]
   __syncthreads();
@@ -286,11 +295,18 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram,
     const int dq = p1 ? 1 : -1;  // x+1 neighbour position
 
     double Y[19];
+    const int s = X + y + z;
+#if TETMF_N1_ZW
+    cube_elements_zw<RULE>(SmemTabs3{opaque_u32(cube && s <= n - 1 ? tab_a : zero_a),
+                                     opaque_u32(cube && s <= n - 2 ? tab_a : zero_a),
+                                     opaque_u32(cube && s <= n - 3 ? tab_a : zero_a)},
+                           FoldIn{r0, r1, r0 + dq, r1 + dq}, Y);
+#else
 #pragma unroll
     for (int k = 0; k < 19; ++k) Y[k] = 0.0;
-    const int s = X + y + z;
     cube_elements<RULE>(SmemTabs{sg}, FoldIn{r0, r1, r0 + dq, r1 + dq}, Y, cube && s <= n - 1, cube && s <= n - 2,
                         cube && s <= n - 3);
+#endif
     __syncwarp();  // ring slot tt mod 3 is refilled by the next step's copies
 
     // contributions of the x-1 neighbour cube (same row)
@@ -426,7 +442,7 @@ void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, 
   if (ntasks == 0) return;
   if (rule < 0 || rule > 2) fail_internal("n1_fold: rule index out of range");
   if (chunk < 1) fail_internal("n1_fold: chunk < 1");
-  constexpr int smem = static_cast<int>(sizeof(N1GramTable) + sizeof(double) * kWarpSmem * kWarps);
+  constexpr int smem = static_cast<int>(sizeof(double) * (kTabs + kWarpSmem * kWarps));
   using K = decltype(&n1_fold_kernel<0, 0>);
   static const K kerns[2][3] = {{n1_fold_kernel<0, 0>, n1_fold_kernel<0, 1>, n1_fold_kernel<0, 2>},
                                 {n1_fold_kernel<1, 0>, n1_fold_kernel<1, 1>, n1_fold_kernel<1, 2>}};

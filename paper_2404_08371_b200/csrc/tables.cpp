@@ -193,6 +193,7 @@ N1GramTable n1_gram_table(const MacroMesh& mesh, int macro, int level) {
       for (int y = x; y < 4; ++y) out.o[o][22 + sym4(x, y)] = g.vol / 120.0 * dot(G[x], G[y]);
     for (int e = 0; e < 6; ++e)
       out.o[o][32 + e] = -2.0 * out.o[o][22 + sym4(local_edge_vertex(e, 0), local_edge_vertex(e, 1))];
+    out.o[o][21] = 7200.0 / g.vol;  // kappa of the ZW form (curl-curl folded into B)
   }
   return out;
 }

@@ -80,7 +80,7 @@ N1DeviceTable pack_n1(const N1Tables& t);
 // with -2 g_ab stored per local edge (one FP64 op fewer per diagonal entry).
 constexpr int kGramRow = 40;
 struct N1GramTable {
-  double o[6][kGramRow];  // [orientation][Kc 0..20, pad 21, g 22..31, -2 g_ab 32..37, pad]
+  double o[6][kGramRow];  // [orientation][Kc 0..20, kappa = 7200/vol 21, g 22..31, -2 g_ab 32..37, pad]
 };
 N1GramTable n1_gram_table(const MacroMesh& mesh, int macro, int level);
 

@@ -260,7 +260,7 @@ def test_parity_config5_mesh(tm, tmp_path, form, level):
 @pytest.mark.gpu
 @pytest.mark.parametrize("mesh,form,level,index,delta", [
     ("cube6", "N1", 3, 24, 1e-9),    # one Gram metric entry g of orientation WU, group 0
-    ("cube6", "N1", 3, 3, 1e-6),     # one curl-curl entry Kc of orientation WU
+    ("cube6", "N1", 3, 21, 1.0),     # kappa = 7200/vol of orientation WU (curl-curl scale, ~2.2e7)
     ("cube6", "P1", 4, 0, 1e-9),     # the centre weight of the interior stencil
     ("single-tet", "P1K", 3, 256 + 1, 1e-9),  # one packed stiffness entry K_o
 ])
