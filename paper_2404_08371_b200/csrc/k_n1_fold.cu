@@ -46,6 +46,8 @@
 // six values per cube are staged by cp.async one step ahead as well (one slot
 // per lane, filled at the end of the previous step), so the read-modify-write
 // costs no load latency.
+#include <cstdlib>
+
 #include "device.hpp"
 #include "n1_common.cuh"
 #include "runtime_check.hpp"
@@ -400,6 +402,22 @@ n1_fold_kernel(const N1GramTable* __restrict__ gram,
 
 } // namespace
 
+// the layer-pair walk (k_n1_fold2.cu, default) and this file's one-layer walk
+void build_n1_fold2_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out, int chunk);
+void pad_n1_fold2_tasks(std::vector<int>& tasks);
+int n1_fold2_chunk(const std::vector<int>& local_macros, int n, int sms);
+void launch_n1_fold2(const N1GramTable* gram, const MacroDesc* macros, int pass, const double* x, const double* alpha,
+                     const double* beta, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
+                     i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s, int chunk);
+// TETMF_N1_WALK (read once): 2 = layer pairs (default), 1 = one layer per step
+int n1_walk_layers() {
+  static const int v = [] {
+    const char* e = std::getenv("TETMF_N1_WALK");
+    return e && e[0] == '1' ? 1 : 2;
+  }();
+  return v;
+}
+
 // Task list of one level and parity pass: (macro, z, k, t0) per layer z of
 // the parity, segment pair (k, K-1-k) or unpaired segment, and chunk of
 // `chunk` steps (kChunk by default; fewer for small levels, where the
@@ -427,6 +445,7 @@ void build_n1_fold_tasks(const std::vector<int>& local_macros, int n, int parity
 
 // Padding of one group's task list to whole CTAs (dummy tasks macro = -1).
 void pad_n1_fold_tasks(std::vector<int>& tasks) {
+  if (n1_walk_layers() == 2) return pad_n1_fold2_tasks(tasks);
   while ((tasks.size() / 4) % kWarps) {
     tasks.push_back(-1);
     tasks.push_back(0);
@@ -439,6 +458,9 @@ void pad_n1_fold_tasks(std::vector<int>& tasks) {
 void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, const double* x, const double* alpha,
                     const double* beta, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
                     i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s, int chunk) {
+  if (n1_walk_layers() == 2)
+    return launch_n1_fold2(gram, macros, pass, x, alpha, beta, y, d_tasks, ntasks, macro_stride, class_stride,
+                           coeff_stride, n, rule, s, chunk);
   if (ntasks == 0) return;
   if (rule < 0 || rule > 2) fail_internal("n1_fold: rule index out of range");
   if (chunk < 1) fail_internal("n1_fold: chunk < 1");
@@ -467,6 +489,7 @@ void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, 
 int n1_kernel_mode() { return 3; }
 
 void build_n1_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out, int chunk) {
+  if (n1_walk_layers() == 2) return build_n1_fold2_tasks(local_macros, n, parity, out, chunk);
   build_n1_fold_tasks(local_macros, n, parity, out, chunk);
 }
 
@@ -475,6 +498,7 @@ void build_n1_tasks(const std::vector<int>& local_macros, int n, int parity, std
 // under strong scaling); each halving adds a halo step per 8-32 steps but
 // multiplies the tasks.
 int n1_fold_chunk(const std::vector<int>& local_macros, int n, int sms) {
+  if (n1_walk_layers() == 2) return n1_fold2_chunk(local_macros, n, sms);
   std::vector<int> t;
   int chunk = kChunk;
   while (chunk > 8) {

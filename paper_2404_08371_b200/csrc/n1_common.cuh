@@ -194,14 +194,17 @@ __host__ __device__ constexpr bool touched_before(int o, int ce) {
       if (cube_edge(kCubeOrder[k], le) == ce) return true;
   return false;
 }
-template <int O, int I>
+// SEED: the cube's bottom-face accumulators 0, 1, 3, 7, 10 arrive holding the
+// top-face sums of the cube below (k_n1_fold2.cu)
+__host__ __device__ constexpr bool seeded_edge(int ce) { return ce == 0 || ce == 1 || ce == 3 || ce == 7 || ce == 10; }
+template <int O, int I, bool SEED = false>
 __device__ __forceinline__ void zw_out(const double (&Bp)[10], const double (&Z)[4][3], const double (&Z3)[4],
                                        double (&Y)[19]) {
   constexpr int a = local_edge_vertex(I, 0), b = local_edge_vertex(I, 1);
   constexpr bool s = local_edge_ref(O, I).flipped;  // Y_e += s_e y_ab
   constexpr int ce = cube_edge(O, I);
   double acc;
-  if constexpr (touched_before(O, ce)) {
+  if constexpr (touched_before(O, ce) || (SEED && seeded_edge(ce))) {
     acc = zw_term<s, a, 0, b>(Bp, Z, Z3, Y[ce]);
   } else {
     constexpr bool neg = s != (b == 3);
@@ -215,7 +218,7 @@ __device__ __forceinline__ void zw_out(const double (&Bp)[10], const double (&Z)
   acc = zw_term<s, a, 3, b>(Bp, Z, Z3, acc);
   acc = zw_term<!s, b, 3, a>(Bp, Z, Z3, acc);
   Y[ce] = acc;
-  if constexpr (I + 1 < 6) zw_out<O, I + 1>(Bp, Z, Z3, Y);
+  if constexpr (I + 1 < 6) zw_out<O, I + 1, SEED>(Bp, Z, Z3, Y);
 }
 template <int O, int P, typename Tab>
 __device__ __forceinline__ void zw_rows(const Tab& tb, const double (&xe)[6], double (&Z)[4][3], double (&Z3)[4]) {
@@ -226,7 +229,36 @@ __device__ __forceinline__ void zw_rows(const Tab& tb, const double (&xe)[6], do
   if constexpr (P + 1 < 4) zw_rows<O, P + 1>(tb, xe, Z, Z3);
 }
 
-template <int O, int RULE = 0, typename Tab, typename In>
+// p-major order: row P of Z is formed and at once consumed by the six edge
+// outputs (terms B'_aP Z_Pb and B'_bP Z_Pa), so only one Z row is live
+template <int O, int P, int I, bool SEED = false>
+__device__ __forceinline__ void zw_prow_out(const double (&Bp)[10], const double (&Zr)[4], double (&Y)[19]) {
+  constexpr int a = local_edge_vertex(I, 0), b = local_edge_vertex(I, 1);
+  constexpr bool s = local_edge_ref(O, I).flipped;
+  constexpr int ce = cube_edge(O, I);
+  constexpr bool nb = s != (b == 3), na = (!s) != (a == 3);  // Z_P3 = -Zr[3]
+  if constexpr (P == 0 && !touched_before(O, ce) && !(SEED && seeded_edge(ce)))
+    Y[ce] = (nb ? -Bp[sym4(a, P)] : Bp[sym4(a, P)]) * Zr[b];
+  else
+    Y[ce] = fma(nb ? -Bp[sym4(a, P)] : Bp[sym4(a, P)], Zr[b], Y[ce]);
+  Y[ce] = fma(na ? -Bp[sym4(b, P)] : Bp[sym4(b, P)], Zr[a], Y[ce]);
+  if constexpr (I + 1 < 6) zw_prow_out<O, P, I + 1, SEED>(Bp, Zr, Y);
+}
+template <int O, int P, bool SEED, typename Tab>
+__device__ __forceinline__ void zw_prows(const Tab& tb, const double (&xe)[6], const double (&Bp)[10], double (&Y)[19]) {
+  double Zr[4];
+  Zr[0] = zw_z<O, P, 0>(tb, xe);
+  Zr[1] = zw_z<O, P, 1>(tb, xe);
+  Zr[2] = zw_z<O, P, 2>(tb, xe);
+  Zr[3] = (Zr[0] + Zr[1]) + Zr[2];
+  zw_prow_out<O, P, 0, SEED>(Bp, Zr, Y);
+  if constexpr (P + 1 < 4) zw_prows<O, P + 1, SEED>(tb, xe, Bp, Y);
+}
+#ifndef TETMF_N1_ZW_PMAJOR
+#define TETMF_N1_ZW_PMAJOR 0
+#endif
+
+template <int O, int RULE = 0, bool SEED = false, typename Tab, typename In>
 __device__ __forceinline__ void element_zw(const Tab& tb, const In& in, double (&Y)[19], bool valid) {
   constexpr int v0 = cube_vertex(O, 0), v1 = cube_vertex(O, 1), v2 = cube_vertex(O, 2), v3 = cube_vertex(O, 3);
   const double a4 = (in.template c<v0, 0>() + in.template c<v1, 0>()) +
@@ -273,9 +305,13 @@ __device__ __forceinline__ void element_zw(const Tab& tb, const In& in, double (
   xe[3] = in.template x<cube_edge(O, 3)>();
   xe[4] = in.template x<cube_edge(O, 4)>();
   xe[5] = in.template x<cube_edge(O, 5)>();
+#if TETMF_N1_ZW_PMAJOR
+  zw_prows<O, 0, SEED>(tb, xe, Bp, Y);
+#else
   double Z[4][3], Z3[4];
   zw_rows<O, 0>(tb, xe, Z, Z3);
-  zw_out<O, 0>(Bp, Z, Z3, Y);
+  zw_out<O, 0, SEED>(Bp, Z, Z3, Y);
+#endif
 }
 
 #ifndef TETMF_N1_ZW
@@ -286,14 +322,14 @@ __device__ __forceinline__ void element_zw(const Tab& tb, const In& in, double (
 // all-zero table (Z = X 0 = 0, so its contribution is exactly 0 for finite
 // inputs): three table bases per step instead of selects on every input.
 // Every cube edge's accumulator is set by its first contribution.
-template <int RULE = 0, typename Tabs, typename In>
+template <int RULE = 0, bool SEED = false, typename Tabs, typename In>
 __device__ __forceinline__ void cube_elements_zw(const Tabs& ts, const In& in, double (&Y)[19]) {
-  element_zw<WU, RULE>(ts.template tab<WU>(), in, Y, true);
-  element_zw<BU, RULE>(ts.template tab<BU>(), in, Y, true);
-  element_zw<BD, RULE>(ts.template tab<BD>(), in, Y, true);
-  element_zw<GU, RULE>(ts.template tab<GU>(), in, Y, true);
-  element_zw<GD, RULE>(ts.template tab<GD>(), in, Y, true);
-  element_zw<WD, RULE>(ts.template tab<WD>(), in, Y, true);
+  element_zw<WU, RULE, SEED>(ts.template tab<WU>(), in, Y, true);
+  element_zw<BU, RULE, SEED>(ts.template tab<BU>(), in, Y, true);
+  element_zw<BD, RULE, SEED>(ts.template tab<BD>(), in, Y, true);
+  element_zw<GU, RULE, SEED>(ts.template tab<GU>(), in, Y, true);
+  element_zw<GD, RULE, SEED>(ts.template tab<GD>(), in, Y, true);
+  element_zw<WD, RULE, SEED>(ts.template tab<WD>(), in, Y, true);
 }
 // one orientation row of a table at a 32-bit shared address; entries are
 // loaded in 16-byte pairs (ld.shared.v2.f64 with an immediate offset; the

@@ -232,7 +232,10 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) probe(const N1GramTable* g, 
 #pragma unroll
     for (int k = 0; k < 19; ++k) Y[k] = Z[k] = 0.0;
     const ProbeIn in{ring + lane + off}, in2{ring + lane + off + kRow};
-    if constexpr (MODE == 0) {
+    if constexpr (MODE == 3) {
+      const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(sm));
+      cube_elements_zw(SmemTabs3{opaque_u32(a), opaque_u32(a), opaque_u32(a)}, in, Z);
+    } else if constexpr (MODE == 0) {
       cube_elements(SmemTabs{sg}, in, Y, true, true, true);
     } else if constexpr (MODE == 1) {
       cube_elements_bp(SmemBp{sm}, in, Y, true, true, true);
@@ -270,7 +273,7 @@ void run(const N1GramTable* g, double* out, int sms) {
   cudaFuncGetAttributes(&fa, probe<WARPS, MINB, MODE>);
   const double flop = 264.0 * 6 * (MODE == 2 ? 2 : 1) * iters * 32.0 * WARPS * blocks;  // SURVEY 8(d) count
   printf("mode %d (%s) warps/CTA %d CTAs/SM %d (%2d warps/SM, %3d regs, spill %zu): %6.2f TFLOP/s algorithmic (%s)\n",
-         MODE, MODE == 0 ? "Gram, 1 cube" : MODE == 1 ? "b', 1 cube" : "b', 2 cubes", WARPS,
+         MODE, MODE == 3 ? "ZW, 1 cube" : MODE == 0 ? "Gram, 1 cube" : MODE == 1 ? "b', 1 cube" : "b', 2 cubes", WARPS,
          MINB, WARPS * MINB, fa.numRegs, fa.localSizeBytes, flop / (ms * 1e-3) / 1e12,
          cudaGetErrorString(cudaGetLastError()));
 }
@@ -286,6 +289,8 @@ int main() {
   cudaMalloc(&g, sizeof(h));
   cudaMalloc(&out, 8);
   cudaMemcpy(g, &h, sizeof(h), cudaMemcpyHostToDevice);
+  run<4, 3, 3>(g, out, sms);
+  run<4, 4, 3>(g, out, sms);
   run<4, 3, 0>(g, out, sms);
   run<4, 4, 0>(g, out, sms);
   run<4, 3, 1>(g, out, sms);
