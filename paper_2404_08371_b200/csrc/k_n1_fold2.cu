@@ -41,6 +41,9 @@ constexpr int kWarps = TETMF_N1F2_WARPS;
 #ifndef TETMF_N1F2_MIN_BLOCKS
 #define TETMF_N1F2_MIN_BLOCKS 2
 #endif
+#ifndef TETMF_N1F2_INTERLEAVE
+#define TETMF_N1F2_INTERLEAVE 0
+#endif
 #ifndef TETMF_N1F2_CHUNK
 #define TETMF_N1F2_CHUNK 32
 #endif
@@ -50,7 +53,7 @@ constexpr int kArrays = 23;               // input arrays per row
 constexpr int kRow = 34;                  // positions per array row
 constexpr int kSlot = kArrays * kRow;     // doubles per ring slot
 constexpr int kRing = 3 * kSlot;          // input ring, doubles per warp
-constexpr int kRmw = 6 * 32;              // pass-1 staging slot, doubles per warp
+constexpr int kRmw = 2 * 6 * 32;          // pass-1 staging, two slots (step parity), doubles per warp
 constexpr int kWarpSmem = kRing + kRmw;
 constexpr int kZeroTab = 6 * kGramRow + 8;         // doubles: zero table offset (+64 B bank phase)
 constexpr int kTabs = kZeroTab + 6 * kGramRow + 8;  // doubles before the warps' rings
@@ -118,7 +121,7 @@ n1_fold2_kernel(const N1GramTable* __restrict__ gram,
   const int lane = threadIdx.x & 31;
   double* ring = dsm + kTabs + (threadIdx.x >> 5) * kWarpSmem;
   for (int i = lane; i < kRing; i += 32) ring[i] = 0.0;  // unfilled positions must read finite
-  double* rmw = ring + kRing + lane;                     // [6][32]
+  double* rmw = ring + kRing + lane;                     // [2][6][32]
   __syncthreads();
   const int warp = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (warp >= ntasks) return;
@@ -219,7 +222,7 @@ n1_fold2_kernel(const N1GramTable* __restrict__ gram,
   // 3 (A's bottom); [3..5] plane z+2 classes 0, 1, 3 (B's top); class 0 at the
   // delayed row in phase 2
   auto stage_rmw = [&](int tn) {
-    double* r = rmw;
+    double* r = rmw + (tn & 1) * 192;
     if (tn < P1) {
       if (tn >= 0 && lane > 0) {
         const double* a = Ym + e0_of(tn) + Xn;
@@ -252,14 +255,29 @@ n1_fold2_kernel(const N1GramTable* __restrict__ gram,
   int slot = ts % 3;
   copy_for(ts - 2, slot == 0 ? 1 : slot == 1 ? 2 : 0);
   copy_for(ts - 1, slot == 0 ? 2 : slot - 1);
-  if (PASS == 1 && t0 == 0) stage_rmw(0);
+  if (PASS == 1) {  // the first writing step's partial sums (an empty group before a halo step)
+    if (t0 == 0)
+      stage_rmw(0);
+    else
+      cp_async_commit();
+  }
 
   // carried sums: A plane z (0, 2, 4), B plane z+1 (0, 2, 4), B plane z+2 (0)
   double a0 = 0.0, a2 = 0.0, a4 = 0.0, b0 = 0.0, b2 = 0.0, b4 = 0.0, bT = 0.0;
   for (int tt = ts; tt < te; ++tt) {
     asm volatile("" ::: "memory");
     copy_for(tt, slot);
-    cp_async_wait1();
+    if constexpr (PASS == 1) {
+      // staging two slots deep: the partial sums step tt + 1 adds to are
+      // requested now and land while this step computes
+      if (tt + 1 < te)
+        stage_rmw(tt + 1);
+      else
+        cp_async_commit();
+      asm volatile("cp.async.wait_group 2;" ::: "memory");  // this step's inputs and staged sums
+    } else {
+      cp_async_wait1();
+    }
     __syncwarp();
     const int sA = slot == 2 ? 0 : slot + 1;
     const int sB = sA == 2 ? 0 : sA + 1;
@@ -275,7 +293,7 @@ n1_fold2_kernel(const N1GramTable* __restrict__ gram,
     const int s = X + y + z;  // anchor sum of A; B's is s + 1
 
     const bool wrt = tt >= t0;  // the halo step only restores the carried sums
-    const double* st = rmw;     // pass 1: staged partial sums (copied at the end of step tt - 1)
+    const double* st = rmw + (tt & 1) * 192;  // pass 1: staged partial sums (requested at step tt - 1)
     auto wr = [&](double* p, int k, double v) {
       if (PASS == 0)
         *p = v;
@@ -286,12 +304,46 @@ n1_fold2_kernel(const N1GramTable* __restrict__ gram,
 
     // ---- cube A = (x, y, z): plane z stores; its top face seeds B
     double YB[19];
+#if TETMF_N1F2_INTERLEAVE == 2
+    // both cubes' elements in one straight-line region (A's stores after B)
+    double YA[19];
+    cube_elements_zw<RULE>(SmemTabs3{opaque_u32(cube && s <= n - 1 ? tab_a : zero_a),
+                                     opaque_u32(cube && s <= n - 2 ? tab_a : zero_a),
+                                     opaque_u32(cube && s <= n - 3 ? tab_a : zero_a)},
+                           FoldIn2<0>{r0, r1, r0 + dq, r1 + dq}, YA);
+    YB[0] = YA[14];
+    YB[1] = YA[15];
+    YB[3] = YA[16];
+    YB[7] = YA[17];
+    YB[10] = YA[18];
+    cube_elements_zw<RULE, true>(SmemTabs3{opaque_u32(cube && s <= n - 2 ? tab_a : zero_a),
+                                           opaque_u32(cube && s <= n - 3 ? tab_a : zero_a),
+                                           opaque_u32(cube && s <= n - 4 ? tab_a : zero_a)},
+                                 FoldIn2<1>{r0, r1, r0 + dq, r1 + dq}, YB);
+    __syncwarp();
+    {
+#elif TETMF_N1F2_INTERLEAVE == 1
+    double YA[19];
+    // A and B element by element (independent accumulators: twice the
+    // independent FP64 chains); A's top face is added to B's bottom after
+    cube_pair_zw<RULE>(SmemTabs3{opaque_u32(cube && s <= n - 1 ? tab_a : zero_a),
+                                 opaque_u32(cube && s <= n - 2 ? tab_a : zero_a),
+                                 opaque_u32(cube && s <= n - 3 ? tab_a : zero_a)},
+                       FoldIn2<0>{r0, r1, r0 + dq, r1 + dq}, YA,
+                       SmemTabs3{opaque_u32(cube && s <= n - 2 ? tab_a : zero_a),
+                                 opaque_u32(cube && s <= n - 3 ? tab_a : zero_a),
+                                 opaque_u32(cube && s <= n - 4 ? tab_a : zero_a)},
+                       FoldIn2<1>{r0, r1, r0 + dq, r1 + dq}, YB);
+    __syncwarp();  // ring slot tt mod 3 is refilled by the next step's copies
+    {
+#else
     {
       double YA[19];
       cube_elements_zw<RULE>(SmemTabs3{opaque_u32(cube && s <= n - 1 ? tab_a : zero_a),
                                        opaque_u32(cube && s <= n - 2 ? tab_a : zero_a),
                                        opaque_u32(cube && s <= n - 3 ? tab_a : zero_a)},
                              FoldIn2<0>{r0, r1, r0 + dq, r1 + dq}, YA);
+#endif
       const double r7 = __shfl_sync(0xffffffffu, YA[7], src);
       const double r8 = __shfl_sync(0xffffffffu, YA[8], src);
       const double r9 = __shfl_sync(0xffffffffu, YA[9], src);
@@ -333,6 +385,16 @@ n1_fold2_kernel(const N1GramTable* __restrict__ gram,
         a2 = YA[2] + r8;
         a4 = YA[4];
       }
+#if TETMF_N1F2_INTERLEAVE == 2
+    }
+#elif TETMF_N1F2_INTERLEAVE == 1
+      YB[0] += YA[14];
+      YB[1] += YA[15];
+      YB[3] += YA[16];
+      YB[7] += YA[17];
+      YB[10] += YA[18];
+    }
+#else
       // B's bottom face starts from A's top face (plane z+1 in-plane edges)
       YB[0] = YA[14];
       YB[1] = YA[15];
@@ -347,6 +409,7 @@ n1_fold2_kernel(const N1GramTable* __restrict__ gram,
                                            opaque_u32(cube && s <= n - 4 ? tab_a : zero_a)},
                                  FoldIn2<1>{r0, r1, r0 + dq, r1 + dq}, YB);
     __syncwarp();  // ring slot tt mod 3 is refilled by the next step's copies
+#endif
     {
       const double r7 = __shfl_sync(0xffffffffu, YB[7], src);
       const double r8 = __shfl_sync(0xffffffffu, YB[8], src);
@@ -405,7 +468,6 @@ n1_fold2_kernel(const N1GramTable* __restrict__ gram,
         bT = YB[14];
       }
     }
-    if (PASS == 1 && tt + 1 < te) stage_rmw(tt + 1);
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
 }

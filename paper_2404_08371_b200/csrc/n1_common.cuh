@@ -185,6 +185,9 @@ __device__ __forceinline__ double zw_term(const double (&Bp)[10], const double (
   const double z = C == 3 ? Z3[P] : Z[P][C < 3 ? C : 0];
   return fma(neg ? -Bp[sym4(A, P)] : Bp[sym4(A, P)], z, acc);
 }
+#ifndef TETMF_N1_ZW_LOCAL
+#define TETMF_N1_ZW_LOCAL 0  // 1: each element sums its terms locally, then adds to the cube accumulator
+#endif
 // element order of cube_elements; a cube edge's first contribution starts its
 // accumulator (no zero-initialised Y)
 constexpr int kCubeOrder[6] = {WU, BU, BD, GU, GD, WD};
@@ -204,7 +207,8 @@ __device__ __forceinline__ void zw_out(const double (&Bp)[10], const double (&Z)
   constexpr bool s = local_edge_ref(O, I).flipped;  // Y_e += s_e y_ab
   constexpr int ce = cube_edge(O, I);
   double acc;
-  if constexpr (touched_before(O, ce) || (SEED && seeded_edge(ce))) {
+  constexpr bool prior = touched_before(O, ce) || (SEED && seeded_edge(ce));
+  if constexpr (prior && !TETMF_N1_ZW_LOCAL) {
     acc = zw_term<s, a, 0, b>(Bp, Z, Z3, Y[ce]);
   } else {
     constexpr bool neg = s != (b == 3);
@@ -217,7 +221,10 @@ __device__ __forceinline__ void zw_out(const double (&Bp)[10], const double (&Z)
   acc = zw_term<!s, b, 2, a>(Bp, Z, Z3, acc);
   acc = zw_term<s, a, 3, b>(Bp, Z, Z3, acc);
   acc = zw_term<!s, b, 3, a>(Bp, Z, Z3, acc);
-  Y[ce] = acc;
+  if constexpr (prior && TETMF_N1_ZW_LOCAL)
+    Y[ce] += acc;  // element-local chain: elements do not wait on each other
+  else
+    Y[ce] = acc;
   if constexpr (I + 1 < 6) zw_out<O, I + 1, SEED>(Bp, Z, Z3, Y);
 }
 template <int O, int P, typename Tab>
@@ -349,6 +356,23 @@ __device__ __forceinline__ unsigned opaque_u32(unsigned v) {
   unsigned r;
   asm("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
   return r;
+}
+// two cubes, element by element (independent accumulators)
+template <int RULE = 0, typename Tabs, typename In0, typename In1>
+__device__ __forceinline__ void cube_pair_zw(const Tabs& ta, const In0& ia, double (&YA)[19], const Tabs& tb,
+                                             const In1& ib, double (&YB)[19]) {
+  element_zw<WU, RULE>(ta.template tab<WU>(), ia, YA, true);
+  element_zw<WU, RULE>(tb.template tab<WU>(), ib, YB, true);
+  element_zw<BU, RULE>(ta.template tab<BU>(), ia, YA, true);
+  element_zw<BU, RULE>(tb.template tab<BU>(), ib, YB, true);
+  element_zw<BD, RULE>(ta.template tab<BD>(), ia, YA, true);
+  element_zw<BD, RULE>(tb.template tab<BD>(), ib, YB, true);
+  element_zw<GU, RULE>(ta.template tab<GU>(), ia, YA, true);
+  element_zw<GU, RULE>(tb.template tab<GU>(), ib, YB, true);
+  element_zw<GD, RULE>(ta.template tab<GD>(), ia, YA, true);
+  element_zw<GD, RULE>(tb.template tab<GD>(), ib, YB, true);
+  element_zw<WD, RULE>(ta.template tab<WD>(), ia, YA, true);
+  element_zw<WD, RULE>(tb.template tab<WD>(), ib, YB, true);
 }
 // three table bases (real or zero table, shared addresses) for the validity
 // classes WU / middle / WD
