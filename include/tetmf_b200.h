@@ -120,6 +120,19 @@ int tetmf_ctx_destroy(tetmf_ctx* ctx);
  * switch never races with an apply still running. To use the legacy default
  * stream pass cudaStreamLegacy ((void*)1). */
 int tetmf_ctx_set_stream(tetmf_ctx* ctx, void* cuda_stream);
+/* Interface exchange of a partitioned context (no effect on one rank):
+ * TETMF_EXCHANGE_SENDRECV (default) packs into a send buffer and moves it with
+ * the transport (grouped ncclSend / ncclRecv, or loopback copies);
+ * TETMF_EXCHANGE_PUT stores every value straight into the peer's receive
+ * window from the pack kernel (NVLink stores through NCCL symmetric windows /
+ * LSA pointers, NCCL device API; plain device pointers between loopback
+ * virtual ranks) followed by a barrier (LSA barrier kernel / host barrier).
+ * Collective; set before the context's first level is used (TETMF_EINVAL
+ * after). Replaces the halo-exchange transport of HyTeG's MPI layer
+ * (PAPER.md:404-405), which the reference does not contain. */
+#define TETMF_EXCHANGE_SENDRECV 0
+#define TETMF_EXCHANGE_PUT 1
+int tetmf_ctx_set_exchange_mode(tetmf_ctx* ctx, int mode);
 int tetmf_ctx_synchronize(tetmf_ctx* ctx);
 int tetmf_ctx_num_macros(const tetmf_ctx* ctx, int* global_count, int* local_count);
 int tetmf_ctx_local_macros(const tetmf_ctx* ctx, int* out /* local_count */);
@@ -260,6 +273,18 @@ int tetmf_plan_slab_units(int num_macros, int level, int nranks, int rank, int* 
 /* the product's pack / combine / local-sum bodies run on host arrays */
 int tetmf_host_local_sum(const int64_t* offsets, const int64_t* copies, int64_t ngroups, double* y);
 int tetmf_host_pack(const double* y, const int64_t* send_index, int64_t nsend, double* send);
+/* put mode (TETMF_EXCHANGE_PUT): where this rank's values start in each
+ * peer's receive buffer, from the group's send-count matrix
+ * counts[src * nranks + dst]; and, per send entry, the target peer slot and
+ * position (the put kernel's addressing) */
+int tetmf_host_put_offsets(int nranks, const int64_t* counts, int rank, int npeers, const int* peers,
+                           int64_t* peer_off);
+int tetmf_host_put_targets(int npeers, const int64_t* send_offsets, const int64_t* peer_off, int64_t* dst_off,
+                           int* dst_peer);
+/* one-GPU check of the NCCL device-API put channel: a 1-rank communicator on
+ * `device`, symmetric window registration, device communicator, `rounds` LSA
+ * barrier kernels (no peers); TETMF_ECOMM with NCCL's message on failure */
+int tetmf_selftest_nccl_put(int device, int rounds);
 int tetmf_host_combine(double* y, const double* recv, const int64_t* group_offsets,
                        const int64_t* group_entries, int64_t ngroups);
 

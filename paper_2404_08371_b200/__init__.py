@@ -31,6 +31,7 @@ FORM_SPACE = {FORM_P1: SPACE_P1, FORM_P1K: SPACE_P1, FORM_N1: SPACE_ND1, FORM_P2
 
 EINVAL, EINTERNAL, EDEVICE, ECOMM = 1, 2, 3, 4
 PARTITION_MACRO, PARTITION_SLAB = 0, 1
+EXCHANGE_SENDRECV, EXCHANGE_PUT = 0, 1
 
 
 class TetmfError(RuntimeError):
@@ -105,6 +106,12 @@ _SIGS = {
     "tetmf_host_local_sum": (ctypes.c_int, [_c_i64p, _c_i64p, ctypes.c_int64, _c_dp]),
     "tetmf_plan_slab_units": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_ip, _c_ip]),
     "tetmf_host_pack": (ctypes.c_int, [_c_dp, _c_i64p, ctypes.c_int64, _c_dp]),
+    "tetmf_host_put_offsets": (ctypes.c_int, [ctypes.c_int, _c_i64p, ctypes.c_int, ctypes.c_int,
+                                              ctypes.POINTER(ctypes.c_int), _c_i64p]),
+    "tetmf_host_put_targets": (ctypes.c_int, [ctypes.c_int, _c_i64p, _c_i64p, _c_i64p,
+                                              ctypes.POINTER(ctypes.c_int)]),
+    "tetmf_selftest_nccl_put": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
+    "tetmf_ctx_set_exchange_mode": (ctypes.c_int, [_c_vp, ctypes.c_int]),
     "tetmf_host_combine": (ctypes.c_int, [_c_dp, _c_dp, _c_i64p, _c_i64p, ctypes.c_int64]),
     "tetmf_measure_fp64_peak": (ctypes.c_int, [_c_vp, ctypes.c_double, _c_dp]),
     "tetmf_measure_fp64_peak2": (ctypes.c_int, [_c_vp, ctypes.c_double, _c_dp, _c_dp]),
@@ -309,6 +316,10 @@ class Context:
             self.close()
         except Exception:
             pass
+
+    def set_exchange_mode(self, mode: int):
+        """EXCHANGE_SENDRECV (default) or EXCHANGE_PUT; before the first level is used."""
+        _check(lib().tetmf_ctx_set_exchange_mode(self._h, int(mode)))
 
     def set_stream(self, stream_ptr: int):
         _check(lib().tetmf_ctx_set_stream(self._h, _c_vp(stream_ptr)))
@@ -612,6 +623,33 @@ def gradient_transpose(nd1: Function, p1: Function, level: int):
 
 def host_local_sum(offsets, copies, y):
     _check(lib().tetmf_host_local_sum(_iptr(offsets), _iptr(copies), offsets.size - 1, _dptr(y)))
+
+
+def host_put_offsets(counts, rank, peers):
+    """where `rank`'s values start in each peer's receive buffer (counts[src, dst])"""
+    counts = np.ascontiguousarray(counts, dtype=np.int64)
+    peers = np.ascontiguousarray(peers, dtype=np.int32)
+    out = np.zeros(max(peers.size, 1), dtype=np.int64)
+    _check(lib().tetmf_host_put_offsets(counts.shape[0], _iptr(counts), int(rank), peers.size,
+                                        peers.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), _iptr(out)))
+    return out[:peers.size]
+
+
+def host_put_targets(send_offsets, peer_off):
+    """per send entry: (position in the target peer's receive buffer, peer slot)"""
+    send_offsets = np.ascontiguousarray(send_offsets, dtype=np.int64)
+    peer_off = np.ascontiguousarray(peer_off, dtype=np.int64)
+    n = int(send_offsets[-1])
+    dst = np.zeros(max(n, 1), dtype=np.int64)
+    slot = np.zeros(max(n, 1), dtype=np.int32)
+    _check(lib().tetmf_host_put_targets(send_offsets.size - 1, _iptr(send_offsets),
+                                        _iptr(peer_off if peer_off.size else np.zeros(1, np.int64)),
+                                        _iptr(dst), slot.ctypes.data_as(ctypes.POINTER(ctypes.c_int))))
+    return dst[:n], slot[:n]
+
+
+def selftest_nccl_put(device=0, rounds=4):
+    _check(lib().tetmf_selftest_nccl_put(int(device), int(rounds)))
 
 
 def host_pack(y, send_index):

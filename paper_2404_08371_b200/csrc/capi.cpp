@@ -183,6 +183,14 @@ int tetmf_ctx_set_stream(tetmf_ctx* ctx, void* cuda_stream) {
   });
 }
 
+int tetmf_ctx_set_exchange_mode(tetmf_ctx* ctx, int mode) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (mode != TETMF_EXCHANGE_SENDRECV && mode != TETMF_EXCHANGE_PUT) fail_arg("exchange mode: 0 (send/recv) or 1 (put)");
+    ctx->impl->set_exchange_put(mode == TETMF_EXCHANGE_PUT);
+  });
+}
+
 int tetmf_ctx_synchronize(tetmf_ctx* ctx) {
   return guard([&] {
     need(ctx, "ctx");
@@ -727,6 +735,52 @@ int tetmf_host_local_sum(const int64_t* offsets, const int64_t* copies, int64_t 
 int tetmf_host_pack(const double* y, const int64_t* send_index, int64_t nsend, double* send) {
   return guard([&] {
     for (int64_t i = 0; i < nsend; ++i) exchange_pack_one(y, send_index, send, i);
+  });
+}
+
+int tetmf_host_put_offsets(int nranks, const int64_t* counts, int rank, int npeers, const int* peers,
+                           int64_t* peer_off) {
+  return guard([&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks || npeers < 0) fail_arg("put offsets: bad rank / sizes");
+    need(counts, "counts");
+    const std::vector<int> pv(peers, peers + npeers);
+    const std::vector<i64> off = put_peer_offsets(nranks, counts, rank, pv);
+    for (int k = 0; k < npeers; ++k) peer_off[k] = off[k];
+  });
+}
+
+int tetmf_host_put_targets(int npeers, const int64_t* send_offsets, const int64_t* peer_off, int64_t* dst_off,
+                           int* dst_peer) {
+  return guard([&] {
+    if (npeers < 0) fail_arg("put targets: npeers < 0");
+    ExchangePlan plan;
+    plan.peers.assign(npeers, 0);
+    plan.send_offsets.assign(send_offsets, send_offsets + npeers + 1);
+    std::vector<i64> off(peer_off, peer_off + npeers), d;
+    std::vector<int> pp;
+    exchange_put_targets(plan, off, d, pp);
+    for (std::size_t i = 0; i < d.size(); ++i) {
+      dst_off[i] = d[i];
+      dst_peer[i] = pp[i];
+    }
+  });
+}
+
+int tetmf_selftest_nccl_put(int device, int rounds) {
+  return guard([&] {
+    TETMF_CUDA(cudaSetDevice(device));
+    char uid[128];
+    nccl_get_unique_id(uid);
+    auto t = make_nccl_transport(1, uid, 0);
+    const std::vector<int> peers;
+    const std::vector<i64> send_off{0}, recv_off{0};
+    auto ch = t->open_put(peers, send_off, recv_off);
+    if (!ch) fail_internal("nccl put self-test: no channel");
+    cudaStream_t s = nullptr;
+    TETMF_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    for (int r = 0; r < rounds; ++r) ch->fence(s);
+    TETMF_CUDA(cudaStreamSynchronize(s));
+    TETMF_CUDA(cudaStreamDestroy(s));
   });
 }
 

@@ -84,6 +84,20 @@ TM_HD void exchange_pack_one(const double* y, const i64* send_index, double* sen
   send[i] = (signed_values && (e & 1)) ? -v : v;
 }
 
+// put mode: entry i goes straight into the receive window of peer slot
+// dst_peer[i] at position dst_off[i] (exchange_put_offsets), same value as the pack
+TM_HD void exchange_put_one(const double* y, const i64* send_index, const i64* dst_off, const int* dst_peer,
+                            double* const* peer_win, i64 i, bool signed_values = true) {
+  const i64 e = send_index[i];
+  const double v = y[e >> 1];
+  peer_win[dst_peer[i]][dst_off[i]] = (signed_values && (e & 1)) ? -v : v;
+}
+
+// per send entry: the peer slot it goes to and its position in that peer's
+// receive buffer (peer_off from put_peer_offsets)
+void exchange_put_targets(const ExchangePlan& plan, const std::vector<i64>& peer_off, std::vector<i64>& dst_off,
+                          std::vector<int>& dst_peer);
+
 // owner = true: ghost update instead of a sum -- every local copy takes the
 // owner copy's value (the first entry: entries are in ascending macro id)
 TM_HD void exchange_combine_one(double* y, const double* recv, const i64* offsets, const i64* entries, i64 g,
@@ -121,7 +135,9 @@ TM_HD void interface_sum_one(double* y, const i64* offsets, const i64* copies, i
 // (NCCL send/recv, or device-to-device copies between loopback virtual ranks).
 class Exchange {
 public:
-  Exchange(ExchangePlan plan, Transport* transport);
+  // put = true: direct-put mode (transport PutChannel: the pack kernel stores
+  // into the peers' receive windows; no send buffer, no send/recv calls)
+  Exchange(ExchangePlan plan, Transport* transport, bool put = false);
   ~Exchange();
   // pack -> send/recv -> combine on `stream` (signed_values = false: ND1
   // orientation signs ignored, for operator diagonals). Collective: every
@@ -140,6 +156,12 @@ private:
   i64* d_group_entries_ = nullptr;
   double* d_send_ = nullptr;
   double* d_recv_ = nullptr;
+  // put mode
+  std::unique_ptr<PutChannel> put_;
+  i64* d_dst_off_ = nullptr;
+  int* d_dst_peer_ = nullptr;
+  double** d_peer_win_ = nullptr;  // [2 parities][peers]: window half bases
+  int parity_ = 0;
 };
 
 } // namespace tetmf

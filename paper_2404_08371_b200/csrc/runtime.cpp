@@ -284,7 +284,7 @@ Context::LevelData& Context::level(Space s, int level) {
     ld->exchange = std::make_unique<Exchange>(
         partition_ == kPartitionSlab ? build_exchange_plan_slab(mesh_, topo_, ld->lay, units, rank_)
                                      : build_exchange_plan(mesh_, topo_, ld->lay, rank_of, rank_),
-        transport_.get());
+        transport_.get(), exchange_put_);
   auto& ref = *ld;
   levels_.emplace(key, std::move(ld));
   return ref;

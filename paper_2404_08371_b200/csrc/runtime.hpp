@@ -31,6 +31,7 @@
 #include "layout.hpp"
 #include "mesh.hpp"
 #include "tables.hpp"
+#include "common.hpp"
 #include "transport.hpp"
 
 namespace tetmf {
@@ -156,8 +157,16 @@ public:
   // NCCL (one process per GPU) or loopback (virtual ranks on one GPU)
   void attach_transport(std::shared_ptr<Transport> t) { transport_ = std::move(t); }
   Transport* transport() const { return transport_.get(); }
+  // interface exchange mode: false = transport send/recv (default), true =
+  // direct put into the peers' receive windows; set before the first level
+  void set_exchange_put(bool put) {
+    if (!levels_.empty()) fail_arg("exchange mode: set it before the context's first level is used");
+    exchange_put_ = put;
+  }
+  bool exchange_put() const { return exchange_put_; }
 
 private:
+  bool exchange_put_ = false;
   MacroMesh mesh_;
   Topology topo_;
   int device_, rank_, nranks_;

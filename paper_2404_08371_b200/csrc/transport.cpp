@@ -1,6 +1,7 @@
 // transport.cpp -- NCCL and loopback transports (transport.hpp).
 #include "transport.hpp"
 
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 #include <string>
@@ -8,6 +9,7 @@
 #include <nccl.h>
 
 #include "common.hpp"
+#include "nccl_put.hpp"
 #include "runtime_check.hpp"
 
 namespace tetmf {
@@ -52,6 +54,12 @@ public:
   void allgather(const double* d_in, double* d_out, int count, cudaStream_t s) override {
     poll_async_error();
     nccl_check(ncclAllGather(d_in, d_out, static_cast<size_t>(count), ncclDouble, comm_, s), "ncclAllGather");
+  }
+
+  std::unique_ptr<PutChannel> open_put(const std::vector<int>& peers, const std::vector<i64>& send_off,
+                                       const std::vector<i64>& recv_off) override {
+    poll_async_error();
+    return nccl_open_put(comm_, rank_, nranks_, peers, send_off, recv_off);
   }
 
   std::string describe() const override {
@@ -162,12 +170,84 @@ private:
   }
 
 public:
+  std::unique_ptr<PutChannel> open_put(const std::vector<int>& peers, const std::vector<i64>& send_off,
+                                       const std::vector<i64>& recv_off) override {
+    std::unique_ptr<PutChannel> ch;
+    guarded([&] { ch = open_put_impl(peers, send_off, recv_off); });
+    return ch;
+  }
+
   std::string describe() const override {
     return "loopback virtual rank " + std::to_string(rank_) + " of " + std::to_string(nranks()) +
            " (device-to-device copies on one GPU)";
   }
 
 private:
+  // the virtual ranks' windows are device buffers of the same GPU; the peers'
+  // stores become visible through stream order: fence = record this rank's
+  // event after its put kernel, host barrier, wait for every peer's event
+  class LoopbackPut final : public PutChannel {
+  public:
+    LoopbackPut(LoopbackTransport* t, std::vector<int> peers) : t_(t), peers_(std::move(peers)) {}
+    ~LoopbackPut() override { cudaFree(local); }
+    void fence(cudaStream_t s) override {
+      t_->guarded([&] {
+        auto& me = t_->hub_->slot(t_->rank_);
+        TETMF_CUDA(cudaEventRecord(me.ready, s));
+        t_->hub_->barrier().wait(t_->hub_->timeout_s);
+        for (int p : peers_) TETMF_CUDA(cudaStreamWaitEvent(s, t_->hub_->slot(p).ready, 0));
+      });
+    }
+
+  private:
+    LoopbackTransport* t_;
+    std::vector<int> peers_;
+  };
+
+  std::unique_ptr<PutChannel> open_put_impl(const std::vector<int>& peers, const std::vector<i64>& send_off,
+                                            const std::vector<i64>& recv_off) {
+    int dev = 0;
+    TETMF_CUDA(cudaGetDevice(&dev));
+    hub_->ensure_events(rank_, dev);
+    auto ch = std::make_unique<LoopbackPut>(this, peers);
+    auto& me = hub_->slot(rank_);
+    me.peers = &peers;
+    me.send_off = &send_off;
+    me.recv_off = &recv_off;
+    me.recv_total = recv_off.empty() ? 0 : recv_off.back();
+    hub_->barrier().wait(hub_->timeout_s);  // every rank's receive layout is published
+    const int P = nranks();
+    std::vector<i64> counts(static_cast<std::size_t>(P) * P, 0);
+    i64 half = 0;
+    for (int q = 0; q < P; ++q) {
+      const auto& qs = hub_->slot(q);
+      half = std::max(half, qs.recv_total);
+      for (std::size_t k = 0; k < qs.peers->size(); ++k)
+        counts[static_cast<std::size_t>(q) * P + (*qs.peers)[k]] = (*qs.send_off)[k + 1] - (*qs.send_off)[k];
+    }
+    ch->half = half;
+    ch->peer_off = put_peer_offsets(P, counts.data(), rank_, peers);
+    // cross-check against the peers' own receive layouts
+    for (std::size_t k = 0; k < peers.size(); ++k) {
+      const auto& ps = hub_->slot(peers[k]);
+      i64 expect = -1;
+      for (std::size_t q = 0; q < ps.peers->size(); ++q)
+        if ((*ps.peers)[q] == rank_) expect = (*ps.recv_off)[q];
+      if (expect != ch->peer_off[k])
+        fail_internal("loopback put: peer " + std::to_string(peers[k]) + " receives rank " + std::to_string(rank_) +
+                      " at " + std::to_string(expect) + ", computed " + std::to_string(ch->peer_off[k]));
+    }
+    if (half > 0) TETMF_CUDA(cudaMalloc(&ch->local, sizeof(double) * 2 * half));
+    me.window = ch->local;
+    hub_->barrier().wait(hub_->timeout_s);  // every window exists
+    for (int p : peers) {
+      if (hub_->slot(p).device != dev) fail_internal("loopback: virtual ranks must share one device");
+      ch->peer_base.push_back(hub_->slot(p).window);
+    }
+    hub_->barrier().wait(hub_->timeout_s);  // the slots may be reused by the next setup
+    return ch;
+  }
+
   void finish(const std::vector<int>& peers, cudaStream_t s) {
     auto& me = hub_->slot(rank_);
     TETMF_CUDA(cudaEventRecord(me.done, s));
@@ -180,6 +260,19 @@ private:
 };
 
 } // namespace
+
+std::vector<i64> put_peer_offsets(int nranks, const i64* counts, int me, const std::vector<int>& peers) {
+  std::vector<i64> off;
+  off.reserve(peers.size());
+  for (int p : peers) {
+    if (p < 0 || p >= nranks || p == me) fail_internal("put_peer_offsets: bad peer rank");
+    i64 o = 0;
+    for (int q = 0; q < me; ++q)
+      if (q != p) o += counts[static_cast<std::size_t>(q) * nranks + p];
+    off.push_back(o);
+  }
+  return off;
+}
 
 std::unique_ptr<Transport> make_nccl_transport(int nranks, const void* unique_id, int rank) {
   return std::make_unique<NcclTransport>(nranks, unique_id, rank);

@@ -47,9 +47,39 @@ struct ExchangeIO {
   double* recv;
 };
 
+// Direct-put channel of one exchange plan (Exchange put mode): every rank
+// owns a receive window of two parity halves (consecutive exchanges alternate
+// halves, so a peer's next puts never land in the half this rank is still
+// combining); the pack kernel stores each value straight into the peer's
+// window (NVLink stores through NCCL LSA pointers, or plain device pointers
+// between loopback virtual ranks), then fence() makes all peers' stores into
+// this rank's window visible on `s`.
+class PutChannel {
+public:
+  virtual ~PutChannel() = default;
+  double* local = nullptr;          // this rank's window: 2 * half doubles
+  i64 half = 0;                     // doubles per parity half (max receive total over the ranks)
+  std::vector<double*> peer_base;   // per plan peer: device address of the peer's window
+  std::vector<i64> peer_off;        // per plan peer: first position of this rank's values in a half
+  virtual void fence(cudaStream_t s) = 0;
+};
+
+// where this rank's values start in each peer's receive buffer: a receive
+// buffer concatenates its peers' contributions in ascending rank order, so
+// for peer p it is the sum of counts[q][p] over ranks q < me
+// (counts[src * nranks + dst] = number of values src sends to dst)
+std::vector<i64> put_peer_offsets(int nranks, const i64* counts, int me, const std::vector<int>& peers);
+
 class Transport {
 public:
   virtual ~Transport() = default;
+  // collective over the group: the put channel of one plan, or nullptr when
+  // the transport cannot store into peer memory
+  virtual std::unique_ptr<PutChannel> open_put(const std::vector<int>& peers, const std::vector<i64>& send_off,
+                                               const std::vector<i64>& recv_off) {
+    (void)peers, (void)send_off, (void)recv_off;
+    return nullptr;
+  }
   virtual int rank() const = 0;
   virtual int nranks() const = 0;
   virtual void exchange(const ExchangeIO& io, cudaStream_t s) = 0;
@@ -94,6 +124,10 @@ public:
     cudaEvent_t ready = nullptr;           // recorded after the rank's send buffer is written
     cudaEvent_t done = nullptr;            // recorded after the rank's copies from its peers
     int device = -1;
+    // put channel setup (open_put): the rank's window and its plan's receive layout
+    double* window = nullptr;
+    i64 recv_total = 0;
+    const std::vector<i64>* recv_off = nullptr;
   };
   Slot& slot(int r) { return slots_[r]; }
   HostBarrier& barrier() { return barrier_; }

@@ -28,7 +28,58 @@ def _free_port():
     return p
 
 
-def _worker(rank, port, mesh, form, level, q):
+def _transfer(tm, plan, y, rank, mode):
+    """The exchange's transfer step on CPU (gloo standing in for the device
+    transport). 'sendrecv': pack into a send buffer, one message per peer
+    (the NCCL send/recv path). 'put': the direct-put addressing of
+    TETMF_EXCHANGE_PUT -- the group's send-count matrix is all-gathered, each
+    rank computes where its values land in every peer's receive buffer
+    (tetmf_host_put_offsets / tetmf_host_put_targets, the put kernel's own
+    addressing) and the receiver only stores them at those positions, which
+    must be exactly the range its own plan reserves for that peer."""
+    send = tm.host_pack(y, plan["send_index"])
+    recv = np.zeros(int(plan["recv_offsets"][-1]))
+    reqs = []
+    if mode == "sendrecv":
+        for i, peer in enumerate(plan["peers"]):
+            so, se = plan["send_offsets"][i], plan["send_offsets"][i + 1]
+            ro, re_ = plan["recv_offsets"][i], plan["recv_offsets"][i + 1]
+            reqs.append(dist.isend(torch.from_numpy(send[so:se].copy()), peer))
+            buf = torch.zeros(int(re_ - ro), dtype=torch.float64)
+            dist.recv(buf, peer)
+            recv[ro:re_] = buf.numpy()
+    else:
+        world = dist.get_world_size()
+        row = torch.zeros(world, dtype=torch.int64)
+        for i, peer in enumerate(plan["peers"]):
+            row[peer] = int(plan["send_offsets"][i + 1] - plan["send_offsets"][i])
+        rows = [torch.zeros(world, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(rows, row)
+        counts = torch.stack(rows).numpy()
+        peer_off = tm.host_put_offsets(counts, rank, plan["peers"])
+        dst, slot = tm.host_put_targets(plan["send_offsets"], peer_off)
+        seen = np.zeros(recv.size, dtype=int)
+        for i, peer in enumerate(plan["peers"]):
+            so, se = plan["send_offsets"][i], plan["send_offsets"][i + 1]
+            assert (slot[so:se] == i).all()
+            reqs.append(dist.isend(torch.from_numpy(dst[so:se].copy()), peer))
+            reqs.append(dist.isend(torch.from_numpy(send[so:se].copy()), peer))
+            ro, re_ = plan["recv_offsets"][i], plan["recv_offsets"][i + 1]
+            pos = torch.zeros(int(re_ - ro), dtype=torch.int64)
+            val = torch.zeros(int(re_ - ro), dtype=torch.float64)
+            dist.recv(pos, peer)
+            dist.recv(val, peer)
+            pos = pos.numpy()
+            assert ((pos >= ro) & (pos < re_)).all(), "a put lands outside the range reserved for its sender"
+            recv[pos] = val.numpy()
+            seen[pos] += 1
+        assert (seen == 1).all()  # every receive position written exactly once
+    for r in reqs:
+        r.wait()
+    return recv
+
+
+def _worker(rank, port, mesh, form, level, q, mode="sendrecv"):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -74,18 +125,7 @@ def _worker(rank, port, mesh, form, level, q):
         off, cp = ctx.local_groups(space, level)
         tm.host_local_sum(off, cp, y)
         plan = ctx.exchange_plan(space, level)
-        send = tm.host_pack(y, plan["send_index"])
-        recv = np.zeros(int(plan["recv_offsets"][-1]))
-        reqs = []
-        for i, peer in enumerate(plan["peers"]):
-            so, se = plan["send_offsets"][i], plan["send_offsets"][i + 1]
-            ro, re_ = plan["recv_offsets"][i], plan["recv_offsets"][i + 1]
-            reqs.append(dist.isend(torch.from_numpy(send[so:se].copy()), peer))
-            buf = torch.zeros(int(re_ - ro), dtype=torch.float64)
-            dist.recv(buf, peer)
-            recv[ro:re_] = buf.numpy()
-        for r in reqs:
-            r.wait()
+        recv = _transfer(tm, plan, y, rank, mode)
         tm.host_combine(y, recv, plan["group_offsets"], plan["group_entries"])
 
         ok = ref_map >= 0
@@ -99,13 +139,14 @@ def _worker(rank, port, mesh, form, level, q):
         q.put((rank, "error: " + traceback.format_exc(), 0, 0))
 
 
+@pytest.mark.parametrize("mode", ["sendrecv", "put"])
 @pytest.mark.parametrize("mesh,form,level", [("cube6", "P1", 3), ("cube6", "N1", 2), ("cubes1x1x2", "P1", 2),
                                              ("cubes1x1x2", "N1", 2)])
-def test_two_rank_exchange(mesh, form, level):
+def test_two_rank_exchange(mesh, form, level, mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, mesh, form, level, q)) for r in range(WORLD)]
+    procs = [ctx.Process(target=_worker, args=(r, port, mesh, form, level, q, mode)) for r in range(WORLD)]
     for p in procs:
         p.start()
     res = [q.get(timeout=240) for _ in range(WORLD)]
@@ -117,7 +158,7 @@ def test_two_rank_exchange(mesh, form, level):
         assert err <= 1e-13, (rank, err)
 
 
-def _slab_worker(rank, world, port, mesh, level, q):
+def _slab_worker(rank, world, port, mesh, level, q, mode="sendrecv"):
     """(macro, z-slab) partition (TETMF_PARTITION_SLAB): every rank stores
     every macro but only its units' planes are computed; copies elsewhere are
     poisoned (NaN) so that any use of a non-owned copy shows."""
@@ -166,18 +207,7 @@ def _slab_worker(rank, world, port, mesh, level, q):
         off, cp = ctx.local_groups(space, level)
         tm.host_local_sum(off, cp, y)
         plan = ctx.exchange_plan(space, level)
-        send = tm.host_pack(y, plan["send_index"])
-        recv = np.zeros(int(plan["recv_offsets"][-1]))
-        reqs = []
-        for i, peer in enumerate(plan["peers"]):
-            so, se = plan["send_offsets"][i], plan["send_offsets"][i + 1]
-            ro, re_ = plan["recv_offsets"][i], plan["recv_offsets"][i + 1]
-            reqs.append(dist.isend(torch.from_numpy(send[so:se].copy()), peer))
-            buf = torch.zeros(int(re_ - ro), dtype=torch.float64)
-            dist.recv(buf, peer)
-            recv[ro:re_] = buf.numpy()
-        for r in reqs:
-            r.wait()
+        recv = _transfer(tm, plan, y, rank, mode)
         tm.host_combine(y, recv, plan["group_offsets"], plan["group_entries"])
         sel = (ref_map >= 0) & own.ravel()
         expect = w_full[ref_map[sel] >> 2]
@@ -189,9 +219,10 @@ def _slab_worker(rank, world, port, mesh, level, q):
         q.put((rank, "error: " + traceback.format_exc(), 0, None))
 
 
+@pytest.mark.parametrize("mode", ["sendrecv", "put"])
 @pytest.mark.parametrize("mesh,level,world", [("cube6", 4, 2), ("cube6", 4, 4), ("cube6", 5, 4),
                                               ("cubes1x1x2", 4, 3)])
-def test_slab_partition_exchange(mesh, level, world):
+def test_slab_partition_exchange(mesh, level, world, mode):
     """Config 4's strong-scaling partition: (macro, z-slab) units, exchange
     of the macro-interface copies across ranks; every owned copy equals the
     full apply and every lattice point is owned by exactly one rank."""
@@ -199,7 +230,7 @@ def test_slab_partition_exchange(mesh, level, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_slab_worker, args=(r, world, port, mesh, level, q)) for r in range(world)]
+    procs = [ctx.Process(target=_slab_worker, args=(r, world, port, mesh, level, q, mode)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]

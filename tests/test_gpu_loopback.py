@@ -236,3 +236,126 @@ def test_owned_reference_slices(tm, mesh, form, level, nranks):
     for c, (_, _, xl, _) in zip(ctxs, out):
         if c.local_macros():
             assert np.array_equal(xl.reshape(-1, ms), xs1[c.local_macros()])
+
+
+def _modes_run(tm, mesh, form, level, nranks, partition, seeds=(42, 43, 44)):
+    """Applies with consecutive seeds (the put mode's window halves alternate)
+    under both exchange modes; the level is created inside the rank threads
+    because opening a put channel is collective."""
+    out = {}
+    for mode in (tm.EXCHANGE_SENDRECV, tm.EXCHANGE_PUT):
+        group = tm.LoopbackGroup(nranks)
+        ctxs = group.contexts(mesh, device=0, partition=partition)
+        for c in ctxs:
+            c.set_exchange_mode(mode)
+
+        def body(r):
+            x, y, op, _ = _setup(tm, ctxs[r], form, level)
+            res = []
+            for sd in seeds:
+                x.fill_seeded(level, sd)
+                op.apply(x, y, level)
+                ctxs[r].synchronize()
+                res.append(y.download(level))
+            return res
+
+        out[mode] = tm.run_ranks(body, nranks)
+        del ctxs, group
+    return out
+
+
+@pytest.mark.parametrize("mesh,form,level,nranks", [("cubes2", "N1", 4, 2), ("cubes2", "N1", 5, 4),
+                                                    ("cubes2", "N1", 4, 8), ("cube6", "P1", 6, 8),
+                                                    ("cubes2", "P1K", 4, 3), ("cube6", "P2V", 3, 4)])
+def test_put_exchange_equals_sendrecv(tm, mesh, form, level, nranks):
+    """TETMF_EXCHANGE_PUT (the pack kernel stores straight into the peers'
+    receive windows; loopback: device pointers, host barrier as the fence)
+    gives the send/recv exchange's results bitwise, apply after apply (each
+    apply uses the other window half), and the single-rank apply's."""
+    out = _modes_run(tm, mesh, form, level, nranks, tm.PARTITION_MACRO)
+    for r in range(nranks):
+        for k in range(3):
+            a, b = out[tm.EXCHANGE_SENDRECV][r][k], out[tm.EXCHANGE_PUT][r][k]
+            if form == "P2V":  # cube kernels scatter with FP64 atomics
+                assert np.allclose(a, b, rtol=1e-13, atol=1e-13 * np.abs(a).max())
+            else:
+                assert np.array_equal(a, b), f"rank {r} apply {k}"
+    # and the same as one rank (seed 42)
+    ctx1, y1, _, ms = _single(tm, mesh, form, level)
+    group = tm.LoopbackGroup(nranks)
+    ctxs = group.contexts(mesh, device=0)
+    for r in range(nranks):
+        mac = ctxs[r].local_macros()
+        got = out[tm.EXCHANGE_PUT][r][0].reshape(-1, ms) if len(mac) else np.zeros((0, ms))
+        for li, m in enumerate(mac):
+            if form == "P2V":
+                assert np.allclose(got[li], y1[m], rtol=1e-13, atol=1e-13 * np.abs(y1).max())
+            else:
+                assert np.array_equal(got[li], y1[m]), f"rank {r} macro {m}"
+
+
+@pytest.mark.parametrize("mesh,level,nranks", [("cube6", 6, 4), ("cube6", 7, 8)])
+def test_put_exchange_slab_partition(tm, mesh, level, nranks):
+    """Config 4's strong-scaling partition with the put exchange: every rank's
+    owned points equal the send/recv exchange's bitwise."""
+    out = _modes_run(tm, mesh, "P1", level, nranks, tm.PARTITION_SLAB)
+    n = 1 << level
+    tet = lambda k: (k + 1) * (k + 2) * (k + 3) // 6
+    ctx1 = tm.Context(mesh, device=0)
+    ms, _ = ctx1.layout(tm.SPACE_P1, level)
+    starts = np.array([tet(n) - tet(n - z) for z in range(n + 1)])
+    zslot = np.searchsorted(starts, np.arange(ms), side="right") - 1
+    real = np.arange(ms) < tet(n)
+    nmac = ctx1.num_macros()[0]
+    for r in range(nranks):
+        for m, za, zb in tm.slab_units(nmac, level, nranks, r):
+            sel = (zslot >= za) & (zslot < zb) & real
+            for k in range(3):
+                a = out[tm.EXCHANGE_SENDRECV][r][k].reshape(nmac, ms)[m][sel]
+                b = out[tm.EXCHANGE_PUT][r][k].reshape(nmac, ms)[m][sel]
+                assert np.array_equal(a, b), f"rank {r} macro {m} apply {k}"
+
+
+def test_put_mode_cg_matches_sendrecv(tm):
+    """The solver over put-mode virtual ranks (applies through the put
+    exchange, inner products through the transport's all-gather)."""
+    res = {}
+    for mode in (tm.EXCHANGE_SENDRECV, tm.EXCHANGE_PUT):
+        group = tm.LoopbackGroup(3)
+        ctxs = group.contexts("cubes2", device=0)
+        for c in ctxs:
+            c.set_exchange_mode(mode)
+
+        def body(r, ctxs=ctxs):
+            x, b, op, _ = _setup(tm, ctxs[r], "P1", 3, seed=5)
+            x.fill_seeded(3, 5, True)
+            op.apply(x, b, 3)
+            b.mask_dirichlet(3)
+            u = tm.Function(ctxs[r], tm.SPACE_P1)
+            it, _, ok = op.cg_solve(b, u, 3, rtol=1e-10, max_iter=500)
+            assert ok
+            return u.download(3), it
+
+        res[mode] = tm.run_ranks(body, 3)
+    for r in range(3):
+        assert res[0][r][1] == res[1][r][1]
+        assert np.array_equal(res[0][r][0], res[1][r][0])
+
+
+def test_exchange_mode_set_before_first_level(tm):
+    group = tm.LoopbackGroup(2)
+    ctx = tm.Context.loopback(group, "cube6", 0, device=0)
+    with pytest.raises(tm.InvalidArgument):
+        ctx.set_exchange_mode(7)
+    ctx.set_exchange_mode(tm.EXCHANGE_SENDRECV)  # (a send/recv exchange opens without the peer)
+    f = tm.Function(ctx, tm.SPACE_P1)
+    f.size(3)
+    with pytest.raises(tm.InvalidArgument, match="before the context's first level"):
+        ctx.set_exchange_mode(tm.EXCHANGE_PUT)
+
+
+def test_nccl_put_channel_selftest(tm):
+    """The NCCL device-API path on one B200: a 1-rank communicator,
+    ncclMemAlloc + symmetric window registration, a device communicator with
+    an LSA barrier, and the LSA barrier kernel (no peers on one GPU)."""
+    tm.selftest_nccl_put(0, rounds=4)
