@@ -341,7 +341,11 @@ def run_gpu(a):
     slab = a.config == "c4" and ws > 1
     ctx = tm.Context(cfg["mesh"], device=local, rank=rank, nranks=ws, nccl_id=nccl_id,
                      partition=tm.PARTITION_SLAB if slab else tm.PARTITION_MACRO)
+    if ws > 1 and a.exchange == "put":
+        ctx.set_exchange_mode(tm.EXCHANGE_PUT)  # before the first level: the put channel opens with it
     comm_info = ctx.transport_info()  # "nccl rank r of N (cuda device d)": the communicator's own rank count
+    if ws > 1:
+        comm_info += f"; interface exchange: {a.exchange}"
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     nmac_global, nmac_local = ctx.num_macros()
@@ -629,6 +633,8 @@ def main():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-fp64-peak", dest="fp64_peak", action="store_false")
     p.add_argument("--variant", type=int, default=0, help="kernel variant for A/B runs (0 = default)")
+    p.add_argument("--exchange", choices=["sendrecv", "put"], default="sendrecv",
+                   help="N > 1: interface exchange by NCCL send/recv or by direct NVLink puts (NCCL device API)")
     p.add_argument("--no-subrecords", dest="subrecords", action="store_false",
                    help="c5 only: skip the c4 / c2l / p2v / c1-c3 sub-records")
     a = p.parse_args()
