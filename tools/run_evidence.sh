@@ -14,6 +14,6 @@ python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-subrecords 
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_c5.csv \
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-subrecords --no-fp64-peak > /dev/null 2>&1
 python bench.py --config c2l --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${TAG}_c2l.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:p1k_walk -s 3 -c 1 -o gpurun_out/${TAG}_k2walk \
+ncu --set full --clock-control none --import-source on -k regex:p1k_cube -s 3 -c 1 -o gpurun_out/${TAG}_k2cube \
     python bench.py --config c2l --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 echo done
