@@ -73,13 +73,6 @@ void build_stencil6_tasks(int nmacros, int n, std::vector<int>& out);
 void launch_p1_stencil6(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
                         int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s,
                         const int* zrange = nullptr);
-// K1 variant 7: persistent double-buffered shared-memory boxes (k_p1_stencil5.cu)
-void build_stencil7_tasks(int nmacros, int n, std::vector<int>& out);
-void launch_p1_stencil7(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
-                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
-// K1 variant 8: variant 7's boxes filled by 16-byte cp.async chunks (k_p1_stencil5.cu)
-void launch_p1_stencil8(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
-                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
 // K1 variant 10: variant 6's boxes in a persistent double-buffered CTA loop (k_p1_stencil5.cu)
 void launch_p1_stencil10(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
                          int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);

@@ -644,216 +644,6 @@ p1_box_kernel(const double* __restrict__ xin, double* __restrict__ yout, const T
   }
 }
 
-// ---------------------------------------------------------------------------
-// Variant 7: persistent, double-buffered version of variant 6. Each CTA loops
-// over boxes (macro, 2*kPairs7 planes, kRows7 rows, kCols7 columns); while
-// its warps walk box k out of one shared-memory stage, the per-row TMA bulk
-// copies of box k+1 land in the other stage (full / empty mbarrier pair per
-// stage), so copy latency is off the critical path. Warp w walks plane pair
-// w / kSegs7, 32-column segment w % kSegs7 of the box; the segment-0 warp of
-// each pair also computes the pair's diagonal points (gathers, L2).
-#ifndef TETMF_P1P_COLS
-#define TETMF_P1P_COLS 64
-#endif
-#ifndef TETMF_P1P_ROWS
-#define TETMF_P1P_ROWS 8
-#endif
-#ifndef TETMF_P1P_PAIRS
-#define TETMF_P1P_PAIRS 2
-#endif
-#ifndef TETMF_P1P_NULL
-#define TETMF_P1P_NULL 0
-#endif
-#ifndef TETMF_P1P_MINB
-#define TETMF_P1P_MINB 0
-#endif
-constexpr int kCols7 = TETMF_P1P_COLS;
-constexpr int kRows7 = TETMF_P1P_ROWS;
-constexpr int kPairs7 = TETMF_P1P_PAIRS;
-constexpr int kSegs7 = kCols7 / 32;
-constexpr int kWarps7 = kPairs7 * kSegs7;
-constexpr int kPlanes7 = 2 * kPairs7 + 2;
-constexpr int kRowsH7 = kRows7 + 2;
-constexpr int kCopies7 = kPlanes7 * kRowsH7;
-constexpr int kPitch7 = kCols7 + 6;
-constexpr int kStage7 = kCopies7 * kPitch7;  // doubles per stage
-static_assert(kCols7 % 32 == 0 && kRows7 <= 16 && kCopies7 <= 32 * kWarps7, "p1 pipe tiling");
-
-
-
-// kAsync = false: per-row TMA bulk copies on full / empty mbarriers (variant 7);
-// kAsync = true: the same box rows as coalesced 16-byte cp.async chunks (one
-// warp per row, lanes over the row), one commit group per box, block-wide
-// barriers around each box (variant 8) -- no TMA engine per-copy cost.
-template <bool kAsync>
-#if TETMF_P1P_MINB > 0
-__global__ void __launch_bounds__(32 * kWarps7, TETMF_P1P_MINB)
-#else
-__global__ void __launch_bounds__(32 * kWarps7)
-#endif
-p1_pipe_kernel(const double* __restrict__ xin, double* __restrict__ yout, const Task5* __restrict__ tasks, int ntasks,
-               i64 stride, int n, const P1DeviceTable* __restrict__ tabs, const MacroDesc* __restrict__ macros) {
-  extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) unsigned long long full[2], empty[2];
-  const int tid = static_cast<int>(threadIdx.x), lane = tid & 31, wid = tid >> 5;
-  if (!kAsync && tid == 0) {
-    for (int i = 0; i < 2; ++i) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[i])), "r"(kCopies7));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[i])), "r"(kWarps7));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  // copy thread tid: (box plane pi, box row ri) of box ti into stage st
-  auto issue = [&](int ti, int st) {
-    const Task5 u = tasks[ti];
-    const int pi = tid / kRowsH7, ri = tid - pi * kRowsH7;
-    const int p = min(max(u.z0 - 1 + pi, 0), n);  // missing planes alias the nearest (zero weights)
-    const int y = u.y0 - 1 + ri;                   // -1 for the halo of block 0: finite neighbours
-    const int m = n - p, x0 = u.pad;
-    unsigned bytes = 0;
-    unsigned long long* bar = &full[st];
-    if (y <= m) {
-      const int rs = rstart32(n, p, y);
-      const int base = (rs + x0 - 2) & ~1;
-      const int g0 = (rs + x0 - 1) & ~1;
-      const int g1 = (rs + min(x0 + kCols7 + 1, m + 2 - y) + 1) & ~1;  // row end + 1 at most
-      if (g1 > g0) {
-        bytes = static_cast<unsigned>(g1 - g0) * 8u;
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                     : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(sm + st * kStage7 + tid * kPitch7 + (g0 - base))),
-            "l"(xin + static_cast<i64>(u.macro) * stride + g0), "r"(bytes), "r"(smem_u32(bar))
-            : "memory");
-      }
-    }
-    if (bytes == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-  };
-  auto issue_async = [&](int ti, int st) {
-    const Task5 u = tasks[ti];
-    for (int j = wid; j < kCopies7; j += kWarps7) {
-      const int pi = j / kRowsH7, ri = j - pi * kRowsH7;
-      const int p = min(max(u.z0 - 1 + pi, 0), n);
-      const int y = u.y0 - 1 + ri;
-      const int m = n - p, x0 = u.pad;
-      if (y > m) continue;
-      const int rs = rstart32(n, p, y);
-      const int base = (rs + x0 - 2) & ~1;
-      const int g0 = (rs + x0 - 1) & ~1;
-      const int g1 = (rs + min(x0 + kCols7 + 1, m + 2 - y) + 1) & ~1;
-      const double* src = xin + static_cast<i64>(u.macro) * stride + g0;
-      const unsigned dst = smem_u32(sm + st * kStage7 + j * kPitch7 + (g0 - base));
-      for (int c = lane; 2 * c < g1 - g0; c += 32)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * c), "l"(src + 2 * c) : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  const int G = static_cast<int>(gridDim.x);
-  if (kAsync) {
-    if (static_cast<int>(blockIdx.x) < ntasks) issue_async(blockIdx.x, 0);
-  } else if (tid < kCopies7 && static_cast<int>(blockIdx.x) < ntasks) {
-    issue(blockIdx.x, 0);
-  }
-  const int pr = wid / kSegs7, sg = wid - pr * kSegs7;
-  int k = 0;
-  for (int ti = static_cast<int>(blockIdx.x); ti < ntasks; ti += G, ++k) {
-    const int st = k & 1;
-    if (kAsync) {
-      // the other stage was released by the barrier that ended box k-1
-      if (ti + G < ntasks) issue_async(ti + G, st ^ 1);
-      else asm volatile("cp.async.commit_group;" ::: "memory");
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-      __syncthreads();
-    } else if (tid < kCopies7 && ti + G < ntasks) {
-      // the other stage is free once every warp released box k-1
-      if (k >= 1) mbar_wait_parity(&empty[st ^ 1], static_cast<unsigned>((k - 1) >> 1) & 1u);
-      issue(ti + G, st ^ 1);
-    }
-    const Task5 t = tasks[ti];
-    const int y0 = t.y0, x0 = t.pad;
-    const int z = t.z0 + 2 * pr;
-    const double* __restrict__ Xm = xin + static_cast<i64>(t.macro) * stride;
-    double* __restrict__ Ym = yout + static_cast<i64>(t.macro) * stride;
-    const double* __restrict__ tab = &tabs[macros[t.macro].group].stencil[0][0];
-    const double* __restrict__ S = sm + st * kStage7;
-    if (!kAsync) mbar_wait_parity(&full[st], static_cast<unsigned>(k >> 1) & 1u);
-    const int xs = x0 + 32 * sg;
-    if (z <= n - y0 && xs <= n - y0 - z) {
-      const int px = xs + lane;
-      double w[15];
-      {
-        const double* __restrict__ wt = tab + (px == 0 ? 16 : 0);
-#pragma unroll
-        for (int q = 0; q < 15; ++q) w[q] = __ldg(wt + q);
-      }
-      const int pl = max(z - 1, 0), pb = min(z + 1, n), pu = min(z + 2, n);
-      constexpr int PL = 0, PA = 1, PB = 2, PU = 3;  // relative to the pair's first box plane 2*pr
-      const int pbase = 2 * pr * kRowsH7 * kPitch7 + 2 - x0 + px;
-      // shared-memory index of column px in box row ri of the row starting at g
-      auto idx = [&](int P, int ri, int g) { return pbase + (P * kRowsH7 + ri) * kPitch7 + ((g + x0) & 1); };
-      int ga = rstart32(n, z, y0), gl = rstart32(n, pl, y0), gb = rstart32(n, pb, y0), gu = rstart32(n, pu, y0);
-      int la = n - z - y0 + 1, ll = n - pl - y0 + 1, lb = n - pb - y0 + 1, lu = n - pu - y0 + 1;
-      const int iam = idx(PA, 0, ga - (la + 1)), ia0 = idx(PA, 1, ga), il0 = idx(PL, 1, gl);
-      const int ibm = idx(PB, 0, gb - (lb + 1)), ib0 = idx(PB, 1, gb), ium = idx(PU, 0, gu - (lu + 1));
-      double Am0 = S[iam], Am1 = S[iam + 1];
-      double A0m = S[ia0 - 1], A00 = S[ia0], A01 = S[ia0 + 1];
-      double L00 = S[il0], L01 = S[il0 + 1];
-      double Bmm = S[ibm - 1], Bm0 = S[ibm], Bm1 = S[ibm + 1];
-      double B0m = S[ib0 - 1], B00 = S[ib0], B01 = S[ib0 + 1];
-      double Umm = S[ium - 1], Um0 = S[ium];
-      int yA = ga + px, yB = rstart32(n, z + 1, y0) + px;  // z + 1 = n + 1: never stored
-      const int s0 = px + y0 + z;
-      const bool zA = z >= 1;
-#pragma unroll
-      for (int r = 0; r < kRows7; ++r) {
-        const int yy = y0 + r;
-        const int gl1 = gl + ll, ga1 = ga + la, gb1 = gb + lb;
-        const int il = idx(PL, r + 2, gl1), ia = idx(PA, r + 2, ga1), ib = idx(PB, r + 2, gb1), iu = idx(PU, r + 1, gu);
-        const double Lp0 = S[il], Lp1 = S[il + 1];
-        const double Apm = S[ia - 1], Ap0 = S[ia], Ap1 = S[ia + 1];
-        const double Bpm = S[ib - 1], Bp0 = S[ib], Bp1 = S[ib + 1];
-        const double U0m = S[iu - 1], U00 = S[iu];
-#if TETMF_P1P_NULL  // A/B floor: same loads and stores, no stencil arithmetic
-        const double fa = A00 + Ap0 + L00 + Lp1 + Am0, fb = B00 + Bp0 + U00 + U0m + Bpm + Bmm;
-#else
-        const double fa = sum15(w, A00, A01, A0m, Ap0, Am0, B00, L00, Am1, Apm, L01, B0m, Lp0, Bm0, Lp1, Bmm);
-        const double fb = sum15(w, B00, B01, B0m, Bp0, Bm0, U00, A00, Bm1, Bpm, A01, U0m, Ap0, Um0, Ap1, Umm);
-#endif
-        if (yy >= 1 && zA && s0 + r <= n - 1) Ym[yA] = fa;
-        if (yy >= 1 && s0 + r + 1 <= n - 1) Ym[yB] = fb;
-        yA += la;
-        yB += la - 1;
-        Am0 = A00; Am1 = A01;
-        A0m = Apm; A00 = Ap0; A01 = Ap1;
-        L00 = Lp0; L01 = Lp1;
-        Bmm = B0m; Bm0 = B00; Bm1 = B01;
-        B0m = Bpm; B00 = Bp0; B01 = Bp1;
-        Umm = U0m; Um0 = U00;
-        gu += lu;
-        gl = gl1; ga = ga1; gb = gb1;
-        --ll; --la; --lb; --lu;
-      }
-    }
-    if (sg == 0) {
-      // diagonal points (x + y + z = n) of the pair's box rows inside the box columns
-      const int zz = z + (lane >> 4), yy = y0 + (lane & 15);
-      if ((lane & 15) < kRows7 && zz >= 1 && zz <= n && yy >= 1 && yy <= n - zz) {
-        const int xx = n - zz - yy;
-        if (xx >= x0 && xx < x0 + kCols7)
-          Ym[lattice_index(n, xx, yy, zz)] = gather_point(Xm, tab + 16 * (8 | (xx == 0 ? 1 : 0)), n, xx, yy, zz);
-      }
-    }
-    if (kAsync) {
-      __syncthreads();
-    } else {
-      __syncwarp();
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
-    }
-  }
-}
-
 // Faces z = 0 and y = 0 (coalesced along x): thread per (macro, face f, point
 // of the face triangle); a point on both is computed by f = 0 (z = 0). Grid:
 // x = points of a face triangle, y = macro * 2 + f. The x = 0 face is walked
@@ -936,56 +726,6 @@ void launch_p1_stencil6(const double* x, double* y, const int* d_tasks, int ntas
 void launch_p1_stencil10(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
                          int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
   launch_p1_box<true>(x, y, d_tasks, ntasks, macro_stride, n, nmacros, d_tables, d_macros, s);
-}
-
-// CTA boxes of variant 7 (macro, z0, y0, x0)
-void build_stencil7_tasks(int nmacros, int n, std::vector<int>& out) {
-  out.clear();
-  for (int li = 0; li < nmacros; ++li)
-    for (int y0 = 0; y0 <= n; y0 += kRows7)
-      for (int z0 = 0; z0 <= n - y0; z0 += 2 * kPairs7)
-        for (int x0 = 0; x0 <= n - y0 - z0; x0 += kCols7) {
-          out.push_back(li);
-          out.push_back(z0);
-          out.push_back(y0);
-          out.push_back(x0);
-        }
-}
-
-template <bool kAsync>
-static void launch_p1_pipe(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
-                           int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
-  if (ntasks == 0) return;
-  if (tet_count(n) + n + 96 >= (i64(1) << 31)) fail_arg("p1 pipe kernel: level too large for 32-bit lattice offsets");
-  const std::size_t smem = 2 * static_cast<std::size_t>(kStage7) * sizeof(double);
-  static int grid_ctas = 0;
-  if (grid_ctas == 0) {
-    TETMF_CUDA(cudaFuncSetAttribute(p1_pipe_kernel<kAsync>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-    int dev = 0, sms = 0, per_sm = 0;
-    TETMF_CUDA(cudaGetDevice(&dev));
-    TETMF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    TETMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p1_pipe_kernel<kAsync>, 32 * kWarps7, smem));
-    grid_ctas = sms * (per_sm > 0 ? per_sm : 1);
-  }
-  const int grid = ntasks < grid_ctas ? ntasks : grid_ctas;
-  p1_pipe_kernel<kAsync><<<static_cast<unsigned>(grid), 32 * kWarps7, smem, s>>>(
-      x, y, reinterpret_cast<const Task5*>(d_tasks), ntasks, macro_stride, n, d_tables, d_macros);
-  check_launch("p1_pipe");
-  const int T = (n + 1) * (n + 2) / 2;
-  p1_face_kernel<<<dim3(static_cast<unsigned>((T + 255) / 256), static_cast<unsigned>(2 * nmacros)), 256, 0, s>>>(
-      x, y, macro_stride, n, d_tables, d_macros);
-  check_launch("p1_face");
-}
-
-void launch_p1_stencil7(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
-                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
-  launch_p1_pipe<false>(x, y, d_tasks, ntasks, macro_stride, n, nmacros, d_tables, d_macros, s);
-}
-
-void launch_p1_stencil8(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
-                        int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
-  launch_p1_pipe<true>(x, y, d_tasks, ntasks, macro_stride, n, nmacros, d_tables, d_macros, s);
 }
 
 void launch_p1_stencil5(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,

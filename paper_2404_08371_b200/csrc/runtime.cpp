@@ -297,9 +297,6 @@ void Context::ensure_p1_variant_tasks(LevelData& ld) {
   build_stencil2_tasks(nm, n, tasks);
   ld.ntasks = static_cast<int>(tasks.size() / 4);
   ld.tasks.upload(tasks.data(), tasks.size(), stream_);
-  build_stencil7_tasks(nm, n, tasks);
-  ld.ntasks7 = static_cast<int>(tasks.size() / 4);
-  ld.tasks7.upload(tasks.data(), tasks.size(), stream_);
   build_stencil5_tasks(nm, n, tasks);
   ld.ntasks5 = static_cast<int>(tasks.size() / 4);
   ld.tasks5.upload(tasks.data(), tasks.size(), stream_);
@@ -554,7 +551,8 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
   }
   if (ctx_->partition() == Context::kPartitionSlab && kernel_variant_ != 0)
     fail_arg("slab partition: the default K1 kernel only");
-  if ((form_ == Form::P1Diffusion && kernel_variant_ >= 2 && kernel_variant_ <= 4) ||
+  if ((form_ == Form::P1Diffusion && ((kernel_variant_ >= 2 && kernel_variant_ <= 4) || kernel_variant_ == 7 ||
+                                      kernel_variant_ == 8 || kernel_variant_ > 10)) ||
       (form_ == Form::N1CurlCurlMass && kernel_variant_ >= 2) || (form_ == Form::P2VDiffusion && kernel_variant_ >= 2) ||
       (form_ == Form::P1KDiffusion && kernel_variant_ >= 4))
     fail_arg("kernel variant " + std::to_string(kernel_variant_) + " does not exist for this form");
@@ -563,12 +561,6 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
     case Form::P1Diffusion:
       if (kernel_variant_ == 1)
         launch_p1_stencil(x, y, ld.macros.get(), nm, ld.lay.macro_stride, ld.lay.n, t.p1.get(), s);
-      else if (kernel_variant_ == 8)
-        launch_p1_stencil8(x, y, ld.tasks7.get(), ld.ntasks7, ld.lay.macro_stride, ld.lay.n, nm, t.p1.get(),
-                           ld.macros.get(), s);
-      else if (kernel_variant_ == 7)
-        launch_p1_stencil7(x, y, ld.tasks7.get(), ld.ntasks7, ld.lay.macro_stride, ld.lay.n, nm, t.p1.get(),
-                           ld.macros.get(), s);
       else if (kernel_variant_ == 6)
         launch_p1_stencil6(x, y, ld.tasks6.get(), ld.ntasks6, ld.lay.macro_stride, ld.lay.n, nm, t.p1.get(),
                            ld.macros.get(), s);

@@ -128,8 +128,6 @@ public:
     int ntasks5 = 0;
     DeviceBuffer<int> tasks6;           // P1: shared-memory box tasks (variant 6)
     int ntasks6 = 0;
-    DeviceBuffer<int> tasks7;           // P1: persistent double-buffered box tasks (variant 7)
-    int ntasks7 = 0;
     bool variant_tasks_built = false;   // P1: the A/B variants' lists (built on first use)
     DeviceBuffer<int> zrange;           // slab partition: per local macro {za, zb} computed here
     DeviceBuffer<int> p1k_tasks;        // P1: row tasks of the P1K gather kernel (K2 round 1, diagonal)
