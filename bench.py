@@ -225,12 +225,26 @@ def roofline(cfg_key, form, local_counts, kern_avg_ms, ms_per_step, fp64_peak):
     sec = kern_avg_ms * 1e-3
     if form in ("N1", "P2V"):
         nd1_local, p1_local = local_counts["nd1_edges"], local_counts["p1_points"]
-        flops = FLOP_PER_ELEM[form] * local_counts["elements"]
+        # F = the cheapest exact formulation's flops, and the
+        # builder's ncu-measured FP64 flop count replaces it when lower
+        # (profiles/r2_flops.json: executed DFMA x 2 + DADD + DMUL per element)
+        f_survey = FLOP_PER_ELEM[form]
+        meas = None
+        try:
+            meas = json.load(open(os.path.join(ROOT, "profiles", "r2_flops.json"))).get(form)
+        except Exception:
+            meas = None
+        f_eff = min(f_survey, meas["flop_per_element"]) if meas else f_survey
+        flops = f_eff * local_counts["elements"]
         # N1: x, y (edges) + alpha, beta (points); P2V: x, k, y (points + edges)
         bytes_alg = 8.0 * ((2 * nd1_local + 2 * p1_local) if form == "N1" else 3 * (nd1_local + p1_local))
         roof = {"bound": "fp64", "achieved": flops / sec / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": (flops / sec / 1e12) / fp64_peak if fp64_peak else None,
-                "flop_per_launch": flops, "flop_per_element": FLOP_PER_ELEM[form],
+                "flop_per_launch": flops, "flop_per_element": f_eff,
+                "flop_per_element_survey": f_survey,
+                "frac_at_survey_F": (f_survey * local_counts["elements"] / sec / 1e12) / fp64_peak if fp64_peak else None,
+                "flop_per_element_measured": meas["flop_per_element"] if meas else None,
+                "flop_measured_source": meas["source"] if meas else None,
                 "peak_source": "measured FP64 DFMA-chain probe on this GPU: best launch of a 4 s window "
                                "(tetmf_measure_fp64_peak2; peak_sustained = its second half)",
                 "hbm": {"achieved": bytes_alg / sec / 1e9, "peak": hbm_peak, "unit": "GB/s",
