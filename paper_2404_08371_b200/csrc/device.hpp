@@ -110,6 +110,14 @@ void launch_p2v_diagonal(const double* k, double* d, const MacroDesc* d_macros, 
                          i64 class_stride, int n, const P2VTable* d_tables, int rule, cudaStream_t s);
 // P2V factored cube kernel (default; k_p2v.cu v2)
 // rule: 0 exact, 1..3 quadrature(rule) (under-integration; forms.cpp:12 "U")
+// P2V default (exact rule): folded cube walk (k_p2v_fold.cu), one layer per
+// task, parity passes
+void build_p2v_fold_tasks(const std::vector<int>& local_macros, int n, int parity, std::vector<int>& out, int chunk);
+void pad_p2v_fold_tasks(std::vector<int>& tasks);
+int p2v_fold_chunk(const std::vector<int>& local_macros, int n, int sms);
+void launch_p2v_fold(const P2VTable* tabs, const MacroDesc* macros, int pass, const double* x, const double* k,
+                     double* y, const int* d_tasks, int ntasks, i64 macro_stride, i64 class_stride, int n,
+                     cudaStream_t s, int chunk);
 void launch_p2v_cubes2(const double* x, const double* k, double* y, const MacroDesc* d_macros, int nmacros,
                        i64 macro_stride, i64 class_stride, int n, const P2VTable* d_tables, int rule,
                        cudaStream_t s);

@@ -235,6 +235,28 @@ Context::LevelData& Context::level(Space s, int level) {
       }
       ld->fold_tasks.upload(merged.data(), merged.size(), stream_);
     }
+  } else if (s == Space::P2) {
+    // P2V fold walk (k_p2v_fold.cu): per pass, every geometry group's tasks
+    // padded to whole CTAs (a CTA stages its group's table)
+    int sms = 148;
+    TETMF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+    std::vector<int> locals(macros_.size()), merged, part;
+    for (std::size_t li = 0; li < macros_.size(); ++li) locals[li] = static_cast<int>(li);
+    ld->fold_chunk = p2v_fold_chunk(locals, n, sms);
+    for (int pass = 0; pass < 2; ++pass) {
+      ld->fold_range[2 * pass] = static_cast<int>(merged.size() / 4);
+      for (int g = 0; g < ngroups_; ++g) {
+        std::vector<int> members;
+        for (std::size_t li = 0; li < macros_.size(); ++li)
+          if (group_[li] == g) members.push_back(static_cast<int>(li));
+        build_p2v_fold_tasks(members, n, pass, part, ld->fold_chunk);
+        if (part.empty()) continue;
+        pad_p2v_fold_tasks(part);
+        merged.insert(merged.end(), part.begin(), part.end());
+      }
+      ld->fold_range[2 * pass + 1] = static_cast<int>(merged.size() / 4) - ld->fold_range[2 * pass];
+    }
+    ld->fold_tasks.upload(merged.data(), merged.size(), stream_);
   }
   {
     // solver slot classes (solver.cu): interior = not in a boundary face plane
@@ -553,7 +575,7 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
     fail_arg("slab partition: the default K1 kernel only");
   if ((form_ == Form::P1Diffusion && ((kernel_variant_ >= 2 && kernel_variant_ <= 4) || kernel_variant_ == 7 ||
                                       kernel_variant_ == 8 || kernel_variant_ > 10)) ||
-      (form_ == Form::N1CurlCurlMass && kernel_variant_ >= 2) || (form_ == Form::P2VDiffusion && kernel_variant_ >= 2) ||
+      (form_ == Form::N1CurlCurlMass && kernel_variant_ >= 2) || (form_ == Form::P2VDiffusion && kernel_variant_ >= 3) ||
       (form_ == Form::P1KDiffusion && kernel_variant_ >= 4))
     fail_arg("kernel variant " + std::to_string(kernel_variant_) + " does not exist for this form");
   if (form_ == Form::P1Diffusion && kernel_variant_ >= 2) ctx_->ensure_p1_variant_tasks(ld);
@@ -609,7 +631,12 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
       if (kernel_variant_ == 1 && rule_index() == 0)
         launch_p2v_cubes(x, coeffs_[0]->data(level), y, ld.macros.get(), nm, ld.lay.macro_stride,
                          ld.lay.class_stride, ld.lay.n, t.p2v.get(), s);
-      else
+      else if (kernel_variant_ == 0 && rule_index() == 0)  // default: fold walk (exact rule)
+        for (int pass = 0; pass < 2; ++pass)
+          launch_p2v_fold(t.p2v.get(), ld.macros.get(), pass, x, coeffs_[0]->data(level), y,
+                          ld.fold_tasks.get() + 4 * ld.fold_range[2 * pass], ld.fold_range[2 * pass + 1],
+                          ld.lay.macro_stride, ld.lay.class_stride, ld.lay.n, s, ld.fold_chunk);
+      else  // variant 2 (the cube kernel), and the quadrature rules 1-3
         launch_p2v_cubes2(x, coeffs_[0]->data(level), y, ld.macros.get(), nm, ld.lay.macro_stride,
                           ld.lay.class_stride, ld.lay.n, t.p2v.get(), rule_index(), s);
       break;

@@ -107,14 +107,28 @@ def test_p2v_jacobi_pcg(tm):
     assert np.abs(got - want).max() <= 1e-8 * np.abs(want).max()
 
 
-@pytest.mark.parametrize("mesh,level", [("cube6", 6), ("cubes2", 5), ("single-tet", 7), ("cubes1x1x2", 4)])
+@pytest.mark.parametrize("mesh,level", [("cube6", 6), ("cubes2", 5), ("single-tet", 7), ("cubes1x1x2", 4),
+                                        ("single-tet", 0), ("single-tet", 1), ("single-tet", 2), ("cube6", 3),
+                                        ("single-tet", 6)])
 def test_p2v_factored_vs_first_version(tm, mesh, level):
-    """A/B at sizes beyond the oracle's reach: the factored cube kernel
-    (variant 0) against the first-version table kernel (variant 1)."""
+    """A/B at sizes beyond the oracle's reach: the fold walk (variant 0),
+    the factored cube kernel (variant 2) and the first-version table kernel
+    (variant 1); every stored value overwritten (scribbled outputs), and the
+    fold walk bitwise repeatable (no atomics: one store per DoF, fixed order)."""
     ctx, k, x, op = _setup(tm, mesh, level, 9)
-    y0, y1 = tm.Function(ctx, tm.SPACE_P2), tm.Function(ctx, tm.SPACE_P2)
-    op.apply(x, y0, level)
-    op.set_variant(1)
-    op.apply(x, y1, level)
-    a, b = y0.download(level), y1.download(level)
-    assert np.abs(a - b).max() <= 1e-13 * np.abs(b).max()
+    outs = {}
+    for v in (0, 2, 1):
+        y = tm.Function(ctx, tm.SPACE_P2)
+        y.fill_seeded(level, 77)
+        op.set_variant(v)
+        op.apply(x, y, level)
+        outs[v] = y.download(level)
+    b = outs[1]
+    assert np.abs(outs[0] - b).max() <= 1e-13 * np.abs(b).max()
+    assert np.abs(outs[2] - b).max() <= 1e-13 * np.abs(b).max()
+    op.set_variant(0)
+    for rep in range(2):
+        y = tm.Function(ctx, tm.SPACE_P2)
+        y.fill_seeded(level, 100 + rep)
+        op.apply(x, y, level)
+        assert np.array_equal(y.download(level), outs[0]), f"launch {rep} differs"
