@@ -41,9 +41,6 @@ constexpr int kWarps = TETMF_N1F2_WARPS;
 #ifndef TETMF_N1F2_MIN_BLOCKS
 #define TETMF_N1F2_MIN_BLOCKS 2
 #endif
-#ifndef TETMF_N1F2_INTERLEAVE
-#define TETMF_N1F2_INTERLEAVE 0
-#endif
 #ifndef TETMF_N1F2_CHUNK
 #define TETMF_N1F2_CHUNK 32
 #endif
@@ -304,46 +301,12 @@ n1_fold2_kernel(const N1GramTable* __restrict__ gram,
 
     // ---- cube A = (x, y, z): plane z stores; its top face seeds B
     double YB[19];
-#if TETMF_N1F2_INTERLEAVE == 2
-    // both cubes' elements in one straight-line region (A's stores after B)
-    double YA[19];
-    cube_elements_zw<RULE>(SmemTabs3{opaque_u32(cube && s <= n - 1 ? tab_a : zero_a),
-                                     opaque_u32(cube && s <= n - 2 ? tab_a : zero_a),
-                                     opaque_u32(cube && s <= n - 3 ? tab_a : zero_a)},
-                           FoldIn2<0>{r0, r1, r0 + dq, r1 + dq}, YA);
-    YB[0] = YA[14];
-    YB[1] = YA[15];
-    YB[3] = YA[16];
-    YB[7] = YA[17];
-    YB[10] = YA[18];
-    cube_elements_zw<RULE, true>(SmemTabs3{opaque_u32(cube && s <= n - 2 ? tab_a : zero_a),
-                                           opaque_u32(cube && s <= n - 3 ? tab_a : zero_a),
-                                           opaque_u32(cube && s <= n - 4 ? tab_a : zero_a)},
-                                 FoldIn2<1>{r0, r1, r0 + dq, r1 + dq}, YB);
-    __syncwarp();
-    {
-#elif TETMF_N1F2_INTERLEAVE == 1
-    double YA[19];
-    // A and B element by element (independent accumulators: twice the
-    // independent FP64 chains); A's top face is added to B's bottom after
-    cube_pair_zw<RULE>(SmemTabs3{opaque_u32(cube && s <= n - 1 ? tab_a : zero_a),
-                                 opaque_u32(cube && s <= n - 2 ? tab_a : zero_a),
-                                 opaque_u32(cube && s <= n - 3 ? tab_a : zero_a)},
-                       FoldIn2<0>{r0, r1, r0 + dq, r1 + dq}, YA,
-                       SmemTabs3{opaque_u32(cube && s <= n - 2 ? tab_a : zero_a),
-                                 opaque_u32(cube && s <= n - 3 ? tab_a : zero_a),
-                                 opaque_u32(cube && s <= n - 4 ? tab_a : zero_a)},
-                       FoldIn2<1>{r0, r1, r0 + dq, r1 + dq}, YB);
-    __syncwarp();  // ring slot tt mod 3 is refilled by the next step's copies
-    {
-#else
     {
       double YA[19];
       cube_elements_zw<RULE>(SmemTabs3{opaque_u32(cube && s <= n - 1 ? tab_a : zero_a),
                                        opaque_u32(cube && s <= n - 2 ? tab_a : zero_a),
                                        opaque_u32(cube && s <= n - 3 ? tab_a : zero_a)},
                              FoldIn2<0>{r0, r1, r0 + dq, r1 + dq}, YA);
-#endif
       const double r7 = __shfl_sync(0xffffffffu, YA[7], src);
       const double r8 = __shfl_sync(0xffffffffu, YA[8], src);
       const double r9 = __shfl_sync(0xffffffffu, YA[9], src);
@@ -385,16 +348,6 @@ n1_fold2_kernel(const N1GramTable* __restrict__ gram,
         a2 = YA[2] + r8;
         a4 = YA[4];
       }
-#if TETMF_N1F2_INTERLEAVE == 2
-    }
-#elif TETMF_N1F2_INTERLEAVE == 1
-      YB[0] += YA[14];
-      YB[1] += YA[15];
-      YB[3] += YA[16];
-      YB[7] += YA[17];
-      YB[10] += YA[18];
-    }
-#else
       // B's bottom face starts from A's top face (plane z+1 in-plane edges)
       YB[0] = YA[14];
       YB[1] = YA[15];
@@ -409,7 +362,6 @@ n1_fold2_kernel(const N1GramTable* __restrict__ gram,
                                            opaque_u32(cube && s <= n - 4 ? tab_a : zero_a)},
                                  FoldIn2<1>{r0, r1, r0 + dq, r1 + dq}, YB);
     __syncwarp();  // ring slot tt mod 3 is refilled by the next step's copies
-#endif
     {
       const double r7 = __shfl_sync(0xffffffffu, YB[7], src);
       const double r8 = __shfl_sync(0xffffffffu, YB[8], src);

@@ -185,9 +185,6 @@ __device__ __forceinline__ double zw_term(const double (&Bp)[10], const double (
   const double z = C == 3 ? Z3[P] : Z[P][C < 3 ? C : 0];
   return fma(neg ? -Bp[sym4(A, P)] : Bp[sym4(A, P)], z, acc);
 }
-#ifndef TETMF_N1_ZW_LOCAL
-#define TETMF_N1_ZW_LOCAL 0  // 1: each element sums its terms locally, then adds to the cube accumulator
-#endif
 // element order of cube_elements; a cube edge's first contribution starts its
 // accumulator (no zero-initialised Y)
 constexpr int kCubeOrder[6] = {WU, BU, BD, GU, GD, WD};
@@ -208,7 +205,7 @@ __device__ __forceinline__ void zw_out(const double (&Bp)[10], const double (&Z)
   constexpr int ce = cube_edge(O, I);
   double acc;
   constexpr bool prior = touched_before(O, ce) || (SEED && seeded_edge(ce));
-  if constexpr (prior && !TETMF_N1_ZW_LOCAL) {
+  if constexpr (prior) {
     acc = zw_term<s, a, 0, b>(Bp, Z, Z3, Y[ce]);
   } else {
     constexpr bool neg = s != (b == 3);
@@ -221,10 +218,7 @@ __device__ __forceinline__ void zw_out(const double (&Bp)[10], const double (&Z)
   acc = zw_term<!s, b, 2, a>(Bp, Z, Z3, acc);
   acc = zw_term<s, a, 3, b>(Bp, Z, Z3, acc);
   acc = zw_term<!s, b, 3, a>(Bp, Z, Z3, acc);
-  if constexpr (prior && TETMF_N1_ZW_LOCAL)
-    Y[ce] += acc;  // element-local chain: elements do not wait on each other
-  else
-    Y[ce] = acc;
+  Y[ce] = acc;
   if constexpr (I + 1 < 6) zw_out<O, I + 1, SEED>(Bp, Z, Z3, Y);
 }
 template <int O, int P, typename Tab>
@@ -235,35 +229,6 @@ __device__ __forceinline__ void zw_rows(const Tab& tb, const double (&xe)[6], do
   Z3[P] = (Z[P][0] + Z[P][1]) + Z[P][2];
   if constexpr (P + 1 < 4) zw_rows<O, P + 1>(tb, xe, Z, Z3);
 }
-
-// p-major order: row P of Z is formed and at once consumed by the six edge
-// outputs (terms B'_aP Z_Pb and B'_bP Z_Pa), so only one Z row is live
-template <int O, int P, int I, bool SEED = false>
-__device__ __forceinline__ void zw_prow_out(const double (&Bp)[10], const double (&Zr)[4], double (&Y)[19]) {
-  constexpr int a = local_edge_vertex(I, 0), b = local_edge_vertex(I, 1);
-  constexpr bool s = local_edge_ref(O, I).flipped;
-  constexpr int ce = cube_edge(O, I);
-  constexpr bool nb = s != (b == 3), na = (!s) != (a == 3);  // Z_P3 = -Zr[3]
-  if constexpr (P == 0 && !touched_before(O, ce) && !(SEED && seeded_edge(ce)))
-    Y[ce] = (nb ? -Bp[sym4(a, P)] : Bp[sym4(a, P)]) * Zr[b];
-  else
-    Y[ce] = fma(nb ? -Bp[sym4(a, P)] : Bp[sym4(a, P)], Zr[b], Y[ce]);
-  Y[ce] = fma(na ? -Bp[sym4(b, P)] : Bp[sym4(b, P)], Zr[a], Y[ce]);
-  if constexpr (I + 1 < 6) zw_prow_out<O, P, I + 1, SEED>(Bp, Zr, Y);
-}
-template <int O, int P, bool SEED, typename Tab>
-__device__ __forceinline__ void zw_prows(const Tab& tb, const double (&xe)[6], const double (&Bp)[10], double (&Y)[19]) {
-  double Zr[4];
-  Zr[0] = zw_z<O, P, 0>(tb, xe);
-  Zr[1] = zw_z<O, P, 1>(tb, xe);
-  Zr[2] = zw_z<O, P, 2>(tb, xe);
-  Zr[3] = (Zr[0] + Zr[1]) + Zr[2];
-  zw_prow_out<O, P, 0, SEED>(Bp, Zr, Y);
-  if constexpr (P + 1 < 4) zw_prows<O, P + 1, SEED>(tb, xe, Bp, Y);
-}
-#ifndef TETMF_N1_ZW_PMAJOR
-#define TETMF_N1_ZW_PMAJOR 0
-#endif
 
 template <int O, int RULE = 0, bool SEED = false, typename Tab, typename In>
 __device__ __forceinline__ void element_zw(const Tab& tb, const In& in, double (&Y)[19], bool valid) {
@@ -312,13 +277,9 @@ __device__ __forceinline__ void element_zw(const Tab& tb, const In& in, double (
   xe[3] = in.template x<cube_edge(O, 3)>();
   xe[4] = in.template x<cube_edge(O, 4)>();
   xe[5] = in.template x<cube_edge(O, 5)>();
-#if TETMF_N1_ZW_PMAJOR
-  zw_prows<O, 0, SEED>(tb, xe, Bp, Y);
-#else
   double Z[4][3], Z3[4];
   zw_rows<O, 0>(tb, xe, Z, Z3);
   zw_out<O, 0, SEED>(Bp, Z, Z3, Y);
-#endif
 }
 
 #ifndef TETMF_N1_ZW
@@ -356,23 +317,6 @@ __device__ __forceinline__ unsigned opaque_u32(unsigned v) {
   unsigned r;
   asm("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
   return r;
-}
-// two cubes, element by element (independent accumulators)
-template <int RULE = 0, typename Tabs, typename In0, typename In1>
-__device__ __forceinline__ void cube_pair_zw(const Tabs& ta, const In0& ia, double (&YA)[19], const Tabs& tb,
-                                             const In1& ib, double (&YB)[19]) {
-  element_zw<WU, RULE>(ta.template tab<WU>(), ia, YA, true);
-  element_zw<WU, RULE>(tb.template tab<WU>(), ib, YB, true);
-  element_zw<BU, RULE>(ta.template tab<BU>(), ia, YA, true);
-  element_zw<BU, RULE>(tb.template tab<BU>(), ib, YB, true);
-  element_zw<BD, RULE>(ta.template tab<BD>(), ia, YA, true);
-  element_zw<BD, RULE>(tb.template tab<BD>(), ib, YB, true);
-  element_zw<GU, RULE>(ta.template tab<GU>(), ia, YA, true);
-  element_zw<GU, RULE>(tb.template tab<GU>(), ib, YB, true);
-  element_zw<GD, RULE>(ta.template tab<GD>(), ia, YA, true);
-  element_zw<GD, RULE>(tb.template tab<GD>(), ib, YB, true);
-  element_zw<WD, RULE>(ta.template tab<WD>(), ia, YA, true);
-  element_zw<WD, RULE>(tb.template tab<WD>(), ib, YB, true);
 }
 // three table bases (real or zero table, shared addresses) for the validity
 // classes WU / middle / WD
