@@ -422,6 +422,56 @@ __device__ __forceinline__ void box_diag6(const Task5& t, int wid, int lane, con
   }
 }
 
+#ifndef TETMF_P1S_DIAG_SMEM
+#define TETMF_P1S_DIAG_SMEM 1  // diagonal points from the landed box (0: global gathers)
+#endif
+
+// The same diagonal points as box_diag6, read from the box in shared memory
+// (row address table rowtab) after the copies landed: the same 15 values
+// (positions past the face read the same global words the gather reads, or
+// 0 where the gather uses 0) and the same sum15 order -- bitwise equal.
+__device__ __forceinline__ void box_diag6_smem(const Task5& t, const unsigned* __restrict__ rowtab, int wid,
+                                               int lane, double* __restrict__ yout, i64 stride, int n,
+                                               const double* __restrict__ tab) {
+  const int y0 = t.y0, x0 = t.pad;
+  const int z = t.z0 + 2 * wid;
+  const int zz = z + (lane >> 4), yy = y0 + (lane & 15);
+  if ((lane & 15) < kRows6 && zz >= 1 && zz <= n && yy >= 1 && yy <= n - zz) {
+    const int xx = n - zz - yy;
+    if (xx >= x0 && xx < x0 + kCols6) {
+      const unsigned* R = rowtab + (2 * wid + 1 + (lane >> 4)) * kRowsH6 + (lane & 15) + 1;  // (zz, yy)
+      const unsigned bx = 8u * static_cast<unsigned>(xx);
+      const unsigned c = R[0] + bx, cm = R[-1] + bx, cp = R[1] + bx;            // rows yy, yy-1, yy+1
+      const unsigned d = R[-kRowsH6] + bx, dp = R[-kRowsH6 + 1] + bx;          // plane zz-1: rows yy, yy+1
+      const unsigned u = R[kRowsH6] + bx, um = R[kRowsH6 - 1] + bx;            // plane zz+1: rows yy, yy-1
+      const bool xm = xx > 0, ym = yy > 0, zm = zz > 0;
+      double v[15];
+      v[0] = lds_at<0>(c);
+      v[1] = 0.0;                           // (+1, 0, 0): past the face
+      v[2] = xm ? lds_at<-8>(c) : 0.0;      // (-1, 0, 0)
+      v[3] = 0.0;                           // (0, +1, 0)
+      v[4] = ym ? lds_at<0>(cm) : 0.0;      // (0, -1, 0)
+      v[5] = 0.0;                           // (0, 0, +1)
+      v[6] = zm ? lds_at<0>(d) : 0.0;       // (0, 0, -1)
+      v[7] = ym ? lds_at<8>(cm) : 0.0;      // (+1, -1, 0)
+      v[8] = xm ? lds_at<-8>(cp) : 0.0;     // (-1, +1, 0)
+      v[9] = zm ? lds_at<8>(d) : 0.0;       // (+1, 0, -1)
+      v[10] = xm ? lds_at<-8>(u) : 0.0;     // (-1, 0, +1)
+      v[11] = zm ? lds_at<0>(dp) : 0.0;     // (0, +1, -1)
+      v[12] = ym ? lds_at<0>(um) : 0.0;     // (0, -1, +1)
+      v[13] = zm ? lds_at<8>(dp) : 0.0;     // (+1, +1, -1): the word after the row, as the gather
+      v[14] = (xm && ym) ? lds_at<-8>(um) : 0.0;  // (-1, -1, +1)
+      const double* __restrict__ wt = tab + 16 * (8 | (xx == 0 ? 1 : 0));
+      double w[15];
+#pragma unroll
+      for (int k = 0; k < 15; ++k) w[k] = __ldg(wt + k);
+      double* __restrict__ Ym = yout + static_cast<i64>(t.macro) * stride;
+      Ym[lattice_index(n, xx, yy, zz)] =
+          sum15(w, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9], v[10], v[11], v[12], v[13], v[14]);
+    }
+  }
+}
+
 // The warp's walk of box t (plane pair z = z0 + 2*wid) out of the stage whose
 // row address table is rowtab; w holds the interior weights on entry.
 __device__ __forceinline__ void box_walk6(const Task5& t, const unsigned* __restrict__ rowtab, double (&w)[15],
@@ -489,7 +539,10 @@ __device__ __forceinline__ void box_walk6(const Task5& t, const unsigned* __rest
       Umm = U0m; Um0 = U00;
     }
   }
-  if (kDiagInWalk) box_diag6(t, wid, lane, xin, yout, stride, n, tab);
+  if (TETMF_P1S_DIAG_SMEM)
+    box_diag6_smem(t, rowtab, wid, lane, yout, stride, n, tab);
+  else if (kDiagInWalk)
+    box_diag6(t, wid, lane, xin, yout, stride, n, tab);
 }
 
 
@@ -603,7 +656,7 @@ p1_box_kernel(const double* __restrict__ xin, double* __restrict__ yout, const T
     double w[15];  // interior weights, loaded while the copies land
 #pragma unroll
     for (int k = 0; k < 15; ++k) w[k] = __ldg(tab + k);
-    if (!kDiagInWalk && !kSingle6) box_diag6(t, wid, lane, xin, yout, stride, n, tab);
+    if (!kDiagInWalk && !kSingle6 && !TETMF_P1S_DIAG_SMEM) box_diag6(t, wid, lane, xin, yout, stride, n, tab);
     mbar_wait_parity(&full[0], 0u);
     if (TETMF_P1S_COPYONLY) return;  // A/B: the box copies alone
     if (kSingle6)
@@ -628,7 +681,8 @@ p1_box_kernel(const double* __restrict__ xin, double* __restrict__ yout, const T
     double w[15];
 #pragma unroll
     for (int q = 0; q < 15; ++q) w[q] = __ldg(tab + q);
-    if (!kDiagInWalk && !kSingle6 && t.z0 + 2 * wid <= n - t.y0) box_diag6(t, wid, lane, xin, yout, stride, n, tab);
+    if (!kDiagInWalk && !kSingle6 && !TETMF_P1S_DIAG_SMEM && t.z0 + 2 * wid <= n - t.y0)
+      box_diag6(t, wid, lane, xin, yout, stride, n, tab);
     // every warp observes the box before releasing it (a released,
     // unobserved phase would alias the stage's next phase)
     mbar_wait_parity(&full[st], static_cast<unsigned>(k >> 1) & 1u);
