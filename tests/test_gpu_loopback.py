@@ -6,8 +6,9 @@ K4 for rank-local interface groups, the exchange pack kernel, the transfer
 (device-to-device copies between the ranks' buffers instead of NCCL
 send/recv), the combine kernel, and the solver's scalar all-gather. The
 results must be bitwise equal to the single-rank apply (every interface sum
-runs in ascending global macro order, exchange.hpp; P2V, whose cube kernels
-scatter with FP64 atomics, to 1e-13), and within 1e-12 of the
+runs in ascending global macro order, exchange.hpp; the P2V apply too -- its
+fold walk has no atomics -- and the P2V operator diagonal, whose kernel
+scatters with FP64 atomics, to 1e-13), and within 1e-12 of the
 reference's FormSystem::apply (oracle/_ref) after reassembly.
 
 Partitions: contiguous macro ranges (runtime.cpp partition_macros); cube6
@@ -86,8 +87,8 @@ def test_virtual_ranks_bitwise_equal_single_rank(tm, mesh, form, level, nranks):
         assert "loopback virtual rank" in c.transport_info()
         if not macros:
             continue
-        if form == "P2V":  # the P2V cube kernels scatter with FP64 atomics: order-dependent rounding
-            assert np.abs(y.reshape(-1, ms) - y1[macros]).max() <= 1e-13 * np.abs(y1).max(), f"rank {c.rank}"
+        if form == "P2V":  # the fold walk apply is atomic-free (bitwise); the diagonal kernel uses atomics
+            assert np.array_equal(y.reshape(-1, ms), y1[macros]), f"rank {c.rank}: apply differs"
             assert np.abs(d.reshape(-1, ms) - d1[macros]).max() <= 1e-13 * np.abs(d1).max(), f"rank {c.rank}"
         else:
             assert np.array_equal(y.reshape(-1, ms), y1[macros]), f"rank {c.rank}: apply differs"
@@ -276,10 +277,7 @@ def test_put_exchange_equals_sendrecv(tm, mesh, form, level, nranks):
     for r in range(nranks):
         for k in range(3):
             a, b = out[tm.EXCHANGE_SENDRECV][r][k], out[tm.EXCHANGE_PUT][r][k]
-            if form == "P2V":  # cube kernels scatter with FP64 atomics
-                assert np.allclose(a, b, rtol=1e-13, atol=1e-13 * np.abs(a).max())
-            else:
-                assert np.array_equal(a, b), f"rank {r} apply {k}"
+            assert np.array_equal(a, b), f"rank {r} apply {k}"
     # and the same as one rank (seed 42)
     ctx1, y1, _, ms = _single(tm, mesh, form, level)
     group = tm.LoopbackGroup(nranks)
@@ -288,10 +286,7 @@ def test_put_exchange_equals_sendrecv(tm, mesh, form, level, nranks):
         mac = ctxs[r].local_macros()
         got = out[tm.EXCHANGE_PUT][r][0].reshape(-1, ms) if len(mac) else np.zeros((0, ms))
         for li, m in enumerate(mac):
-            if form == "P2V":
-                assert np.allclose(got[li], y1[m], rtol=1e-13, atol=1e-13 * np.abs(y1).max())
-            else:
-                assert np.array_equal(got[li], y1[m]), f"rank {r} macro {m}"
+            assert np.array_equal(got[li], y1[m]), f"rank {r} macro {m}"
 
 
 @pytest.mark.parametrize("mesh,level,nranks", [("cube6", 6, 4), ("cube6", 7, 8)])
