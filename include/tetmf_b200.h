@@ -128,7 +128,9 @@ int tetmf_ctx_set_stream(tetmf_ctx* ctx, void* cuda_stream);
  * LSA pointers, NCCL device API; plain device pointers between loopback
  * virtual ranks) followed by a barrier (LSA barrier kernel / host barrier).
  * Collective; set before the context's first level is used (TETMF_EINVAL
- * after). Replaces the halo-exchange transport of HyTeG's MPI layer
+ * after). With NCCL the put windows are registered and deregistered
+ * collectively: every rank creates its levels and destroys the context in
+ * the same order. Replaces the halo-exchange transport of HyTeG's MPI layer
  * (PAPER.md:404-405), which the reference does not contain. */
 #define TETMF_EXCHANGE_SENDRECV 0
 #define TETMF_EXCHANGE_PUT 1
