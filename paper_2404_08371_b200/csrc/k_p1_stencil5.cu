@@ -480,7 +480,6 @@ __device__ __forceinline__ void box_walk6(const Task5& t, const unsigned* __rest
                                           const double* __restrict__ tab) {
   const int y0 = t.y0, x0 = t.pad;
   const int z = t.z0 + 2 * wid;
-  const double* __restrict__ Xm = xin + static_cast<i64>(t.macro) * stride;
   double* __restrict__ Ym = yout + static_cast<i64>(t.macro) * stride;
   // planes L = z-1, A = z, B = z+1, U = z+2 = box planes 2w .. 2w+3
   const unsigned* __restrict__ RL = rowtab + (2 * wid) * kRowsH6;

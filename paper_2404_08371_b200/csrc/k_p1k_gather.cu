@@ -178,7 +178,6 @@ __device__ __forceinline__ void walk_incident(const double (&kv)[27], const KT& 
   constexpr int d = kInc.e[KK].d, o = kInc.e[KK].o, i = kInc.e[KK].i;
   constexpr int dx = d & 1, dy = (d >> 1) & 1, dz = d >> 2;
   constexpr int q0 = kInc.e[KK].q[0], q1 = kInc.e[KK].q[1], q2 = kInc.e[KK].q[2], q3 = kInc.e[KK].q[3];
-  constexpr int qi = kInc.e[KK].q[i];
   const bool valid = (dx == 0 || px >= 1) && (dy == 0 || py >= 1) && (dz == 0 || pz >= 1) &&
                      s - (dx + dy + dz) <= orient_sum_limit(o, n);
   const double ks0 = (kv[q0] + kv[q1]) + (kv[q2] + kv[q3]);

@@ -216,7 +216,7 @@ constexpr int kThreads2 = kStage2 ? 64 : kThreads;  // cubes per CTA (static sha
 
 // cube slots (0..7 vertices, 8..26 edges) touched by the elements valid at
 // anchor-sum class c (0: WU only, 1: + BU BD GU GD, 2: + WD), as bit masks
-constexpr unsigned slot_mask(int cls) {
+[[maybe_unused]] constexpr unsigned slot_mask(int cls) {  // TETMF_P2V_STAGE builds
   unsigned m = 0;
   for (int o = 0; o < 6; ++o) {
     const int need = o == WU ? 0 : o == WD ? 2 : 1;

@@ -494,13 +494,23 @@ void build_p2v_fold_tasks(const std::vector<int>& local_macros, int n, int parit
       const bool paired = k < K && K - 1 - k > k;
       const int nsteps = paired ? 2 * L + 6 - kSeg * K : L - kSeg * k + 1;
       for (int t0 = 0; t0 < nsteps; t0 += chunk)
-        for (int li : local_macros) out.insert(out.end(), {li, z, k, t0});
+        for (int li : local_macros) {
+          out.push_back(li);
+          out.push_back(z);
+          out.push_back(k);
+          out.push_back(t0);
+        }
     }
   }
 }
 
 void pad_p2v_fold_tasks(std::vector<int>& tasks) {
-  while ((tasks.size() / 4) % kWarps) tasks.insert(tasks.end(), {-1, 0, 0, 0});
+  while ((tasks.size() / 4) % kWarps) {
+    tasks.push_back(-1);
+    tasks.push_back(0);
+    tasks.push_back(0);
+    tasks.push_back(0);
+  }
 }
 
 int p2v_fold_chunk(const std::vector<int>& local_macros, int n, int sms) {
