@@ -145,28 +145,48 @@ __device__ __forceinline__ void p2v_element(const GTab<O>& tb, const FoldInP2& i
   g[3] = tb.template get<3>(), g[4] = tb.template get<4>(), g[5] = tb.template get<5>();
   g[6] = tb.template get<6>(), g[7] = tb.template get<7>(), g[8] = tb.template get<8>();
   g[9] = tb.template get<9>();
+  // G has zero row and column sums (sum_p grad lambda_p = 0), so
+  //   W_qr = sum_{p<3} G_qp (U_pr - U_3r)   and   Z_3s = -(Z_0s + Z_1s + Z_2s):
+  // rows 0..2 of W and Z are formed, row 3 of Z is the negated running sum
+  // (104 FP64 instead of 128 for W and Z)
+  double V[3][4];
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) V[p][r] = U[p][r] - U[3][r];
+  double Zs[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    double W[4];
+    double Zq[4];
+    if (q < 3) {
+      double W[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      double a = g[sym4(0, q)] * U[0][r];
+      for (int r = 0; r < 4; ++r) {
+        double a = g[sym4(0, q)] * V[0][r];
+        a = fma(g[sym4(1, q)], V[1][r], a);
+        W[r] = fma(g[sym4(2, q)], V[2][r], a);
+      }
 #pragma unroll
-      for (int p = 1; p < 4; ++p) a = fma(g[sym4(p, q)], U[p][r], a);
-      W[r] = a;
+      for (int s2 = 0; s2 < 4; ++s2) {
+        double zz = W[0] * K[sym4(0, s2)];
+#pragma unroll
+        for (int r = 1; r < 4; ++r) zz = fma(W[r], K[sym4(r, s2)], zz);
+        Zq[s2] = zz;
+        Zs[s2] = q == 0 ? zz : Zs[s2] + zz;
+      }
+    } else {
+#pragma unroll
+      for (int s2 = 0; s2 < 4; ++s2) Zq[s2] = -Zs[s2];
     }
     double v = 0.0;
 #pragma unroll
     for (int s2 = 0; s2 < 4; ++s2) {
-      double zz = W[0] * K[sym4(0, s2)];
-#pragma unroll
-      for (int r = 1; r < 4; ++r) zz = fma(W[r], K[sym4(r, s2)], zz);
       if (s2 == q) {
-        v = fma(3.0, zz, v);
+        v = fma(3.0, Zq[s2], v);
       } else {
-        v -= zz;
+        v -= Zq[s2];
         double& ye = Y[8 + cube_edge(O, local_edge_of(q, s2))];
-        ye = fma(4.0, zz, ye);
+        ye = fma(4.0, Zq[s2], ye);
       }
     }
     Y[cube_vertex(O, q)] += v;
