@@ -301,7 +301,11 @@ __device__ __forceinline__ void cube_elements_zw(const Tabs& ts, const In& in, d
 }
 // one orientation row of a table at a 32-bit shared address; entries are
 // loaded in 16-byte pairs (ld.shared.v2.f64 with an immediate offset; the
-// asm is pure, so the two halves of a pair come from one load)
+// asm is pure, so the two halves of a pair come from one load). Pure asm may
+// be reordered freely, so it must only read memory that no later code writes
+// and that is complete before its address operand exists: the tables are
+// written before the kernel's __syncthreads and never again, and the address
+// (a table-base select) depends on the task loaded after that barrier.
 template <int O>
 struct SmemTabA {
   unsigned a;
