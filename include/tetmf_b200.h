@@ -127,6 +127,12 @@ int tetmf_ctx_set_stream(tetmf_ctx* ctx, void* cuda_stream);
  * window from the pack kernel (NVLink stores through NCCL symmetric windows /
  * LSA pointers, NCCL device API; plain device pointers between loopback
  * virtual ranks) followed by a barrier (LSA barrier kernel / host barrier).
+ * In the (macro, z-slab) partition the P1 -Laplace stencil kernel (the
+ * default K1) issues those stores itself as it computes each shared value --
+ * compute and transfer in one kernel, no pack launch (measured faster there;
+ * with whole-macro ranks the pack kernel measured faster and is used).
+ * TETMF_EXCHANGE_PUT_PACK: always the pack kernel; TETMF_EXCHANGE_PUT_FUSED:
+ * the in-kernel puts in every partition (A/B).
  * Collective; set before the context's first level is used (TETMF_EINVAL
  * after). With NCCL the put windows are registered and deregistered
  * collectively: every rank creates its levels and destroys the context in
@@ -134,6 +140,8 @@ int tetmf_ctx_set_stream(tetmf_ctx* ctx, void* cuda_stream);
  * (PAPER.md:404-405), which the reference does not contain. */
 #define TETMF_EXCHANGE_SENDRECV 0
 #define TETMF_EXCHANGE_PUT 1
+#define TETMF_EXCHANGE_PUT_PACK 2
+#define TETMF_EXCHANGE_PUT_FUSED 3
 int tetmf_ctx_set_exchange_mode(tetmf_ctx* ctx, int mode);
 int tetmf_ctx_synchronize(tetmf_ctx* ctx);
 int tetmf_ctx_num_macros(const tetmf_ctx* ctx, int* global_count, int* local_count);

@@ -31,7 +31,7 @@ FORM_SPACE = {FORM_P1: SPACE_P1, FORM_P1K: SPACE_P1, FORM_N1: SPACE_ND1, FORM_P2
 
 EINVAL, EINTERNAL, EDEVICE, ECOMM = 1, 2, 3, 4
 PARTITION_MACRO, PARTITION_SLAB = 0, 1
-EXCHANGE_SENDRECV, EXCHANGE_PUT = 0, 1
+EXCHANGE_SENDRECV, EXCHANGE_PUT, EXCHANGE_PUT_PACK, EXCHANGE_PUT_FUSED = 0, 1, 2, 3
 
 
 class TetmfError(RuntimeError):
@@ -318,7 +318,10 @@ class Context:
             pass
 
     def set_exchange_mode(self, mode: int):
-        """EXCHANGE_SENDRECV (default) or EXCHANGE_PUT; before the first level is used."""
+        """EXCHANGE_SENDRECV (default), EXCHANGE_PUT (slab partition: the P1
+        stencil kernel issues its puts itself; else the pack kernel),
+        EXCHANGE_PUT_PACK (always the pack kernel) or EXCHANGE_PUT_FUSED
+        (always in-kernel for P1); before the first level is used."""
         _check(lib().tetmf_ctx_set_exchange_mode(self._h, int(mode)))
 
     def set_stream(self, stream_ptr: int):

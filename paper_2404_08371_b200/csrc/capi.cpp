@@ -186,8 +186,12 @@ int tetmf_ctx_set_stream(tetmf_ctx* ctx, void* cuda_stream) {
 int tetmf_ctx_set_exchange_mode(tetmf_ctx* ctx, int mode) {
   return guard([&] {
     need(ctx, "ctx");
-    if (mode != TETMF_EXCHANGE_SENDRECV && mode != TETMF_EXCHANGE_PUT) fail_arg("exchange mode: 0 (send/recv) or 1 (put)");
-    ctx->impl->set_exchange_put(mode == TETMF_EXCHANGE_PUT);
+    if (mode < TETMF_EXCHANGE_SENDRECV || mode > TETMF_EXCHANGE_PUT_FUSED)
+      fail_arg("exchange mode: 0 (send/recv), 1 (put), 2 (put, pack kernel) or 3 (put, in-kernel)");
+    ctx->impl->set_exchange_put(mode != TETMF_EXCHANGE_SENDRECV,
+                                mode == TETMF_EXCHANGE_PUT_PACK    ? Context::kFusedNever
+                                : mode == TETMF_EXCHANGE_PUT_FUSED ? Context::kFusedAlways
+                                                                   : Context::kFusedSlab);
   });
 }
 

@@ -28,6 +28,20 @@ struct MacroDesc {
   double dX[3][3];   // world edge vectors, dX[c][r]
 };
 
+// In-kernel exchange puts (Exchange::fused_begin, exchange.hpp): a kernel that
+// stores y at storage slot j also stores it into every peer receive window
+// entry the exchange would pack slot j into: entries e = first[j],
+// chain[e], ... (-1 ends), each at win[dst[e] >> 48][dst[e] & (2^48 - 1)].
+// The window bases travel in the kernel parameters (no dependent load).
+// first == nullptr: no puts.
+constexpr int kFusedMaxPeers = 16;
+struct FusedPut {
+  const int* first = nullptr;
+  const int* chain = nullptr;
+  const i64* dst = nullptr;
+  double* win[kFusedMaxPeers] = {};
+};
+
 struct CoeffSpec {
   int which;         // 0 alpha = 1+x^2+y^2, 1 beta = 2+sin(pi z), 2 k, 3 constant
   double value;      // for which == 3
@@ -69,10 +83,11 @@ void launch_p1_stencil5(const double* x, double* y, const int* d_tasks, int ntas
 // K1 variant 6: shared-memory boxes filled by per-row TMA bulk copies (k_p1_stencil5.cu)
 void build_stencil6_tasks(int nmacros, int n, std::vector<int>& out);
 // zrange (optional, slab partition): per local macro {za, zb}, the planes this
-// rank computes (the task list holds only boxes of those planes)
+// rank computes (the task list holds only boxes of those planes); fp (optional,
+// put-mode exchange): the kernel also issues the exchange's puts of the values it stores
 void launch_p1_stencil6(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
                         int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s,
-                        const int* zrange = nullptr);
+                        const int* zrange = nullptr, const FusedPut& fp = FusedPut{});
 // K1 variant 10: variant 6's boxes in a persistent double-buffered CTA loop (k_p1_stencil5.cu)
 void launch_p1_stencil10(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
                          int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);

@@ -72,6 +72,63 @@ Exchange::~Exchange() {
   cudaFree(d_dst_off_);
   cudaFree(d_dst_peer_);
   cudaFree(d_peer_win_);
+  cudaFree(d_first_);
+  cudaFree(d_chain_);
+  cudaFree(d_dst_);
+}
+
+bool Exchange::fusable() const {
+  if (!put_ || plan_.peers.size() > static_cast<std::size_t>(kFusedMaxPeers)) return false;
+  for (i64 e : plan_.send_index)
+    if (e & 1) return false;
+  return true;
+}
+
+FusedPut Exchange::fused_begin(i64 storage_size) {
+  if (!fusable()) fail_internal("exchange: fused put without a put channel or with signed entries");
+  if (first_size_ != storage_size) {
+    const i64 ns = plan_.send_total();
+    if (ns >= (i64(1) << 31)) fail_arg("exchange: too many send entries for the fused put");
+    std::vector<int> first(static_cast<std::size_t>(storage_size), -1), chain(static_cast<std::size_t>(ns), -1);
+    for (i64 e = ns - 1; e >= 0; --e) {
+      const i64 j = plan_.send_index[e] >> 1;
+      if (j < 0 || j >= storage_size) fail_internal("exchange: send slot outside the level buffer");
+      chain[e] = first[j];
+      first[j] = static_cast<int>(e);
+    }
+    std::vector<i64> dst(static_cast<std::size_t>(ns)), off;
+    std::vector<int> peer;
+    exchange_put_targets(plan_, put_->peer_off, off, peer);
+    for (i64 e = 0; e < ns; ++e) {
+      if (off[e] >= (i64(1) << 48)) fail_arg("exchange: window too large for the fused put");
+      dst[e] = (static_cast<i64>(peer[e]) << 48) | off[e];
+    }
+    cudaFree(d_first_);
+    cudaFree(d_chain_);
+    cudaFree(d_dst_);
+    d_first_ = upload(first);
+    d_chain_ = upload(chain);
+    d_dst_ = upload(dst);
+    first_size_ = storage_size;
+  }
+  FusedPut fp;
+  fp.first = d_first_;
+  fp.chain = d_chain_;
+  fp.dst = d_dst_;
+  for (std::size_t k = 0; k < plan_.peers.size(); ++k) fp.win[k] = put_->peer_base[k] + parity_ * put_->half;
+  return fp;
+}
+
+void Exchange::fused_finish(double* y, cudaStream_t stream) {
+  const int par = parity_;
+  parity_ ^= 1;
+  put_->fence(stream);
+  const i64 ng = plan_.num_groups();
+  if (ng > 0) {
+    combine_kernel<<<static_cast<unsigned>((ng + 255) / 256), 256, 0, stream>>>(
+        y, put_->local + par * put_->half, d_group_offsets_, d_group_entries_, ng, true, false);
+    check_launch("exchange_combine");
+  }
 }
 
 void exchange_put_targets(const ExchangePlan& plan, const std::vector<i64>& peer_off, std::vector<i64>& dst_off,

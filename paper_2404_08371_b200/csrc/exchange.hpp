@@ -24,6 +24,7 @@
 #include "lattice.hpp"
 #include "layout.hpp"
 #include "mesh.hpp"
+#include "device.hpp"
 #include "transport.hpp"
 
 namespace tetmf {
@@ -147,6 +148,17 @@ public:
   void broadcast_owner(double* y, cudaStream_t stream);
   const ExchangePlan& plan() const { return plan_; }
 
+  // Fused put (put mode, unsigned send entries): the producing kernel stores
+  // every sent value straight into the peers' windows (FusedPut) while it
+  // computes y, and fused_finish() does what run() does after its put
+  // kernel: fence, combine, flip the window half. fused_begin() returns the
+  // targets of the current half; storage_size = doubles of the level buffer
+  // (the slot map is built on the first call). No put channel or a signed
+  // entry: fusable() is false and the caller uses run().
+  bool fusable() const;
+  FusedPut fused_begin(i64 storage_size);
+  void fused_finish(double* y, cudaStream_t stream);
+
 private:
   void run_mode(double* y, cudaStream_t stream, bool signed_values, bool owner);
   ExchangePlan plan_;
@@ -162,6 +174,11 @@ private:
   int* d_dst_peer_ = nullptr;
   double** d_peer_win_ = nullptr;  // [2 parities][peers]: window half bases
   int parity_ = 0;
+  // fused put: per storage slot the first send entry, per entry the next of the same slot
+  int* d_first_ = nullptr;
+  int* d_chain_ = nullptr;
+  i64* d_dst_ = nullptr;  // per entry: (peer slot << 48) | offset in the window half
+  i64 first_size_ = -1;
 };
 
 } // namespace tetmf

@@ -116,13 +116,26 @@ __device__ __forceinline__ double gather_point(const double* __restrict__ X, con
   return sum15(w, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9], v[10], v[11], v[12], v[13], v[14]);
 }
 
+// Fused exchange put (FusedPut, device.hpp): the value just stored at slot
+// j of the level buffer also goes to every peer window entry it is sent to.
+// Only storage slots on a macro face can be shared, so the callers test
+// this at their face stores (x = 0 lanes, diagonal and face points).
+__device__ __forceinline__ void put_slot(const FusedPut* fp, i64 j, double v) {
+  if (!fp) return;
+  for (int e = fp->first[j]; e >= 0; e = fp->chain[e]) {
+    const i64 d = fp->dst[e];
+    fp->win[d >> 48][d & ((i64(1) << 48) - 1)] = v;
+  }
+}
+
 // Point q of face f (0: z = 0, 1: y = 0, the z = 0 edge excluded) of macro
 // li: the triangle a + b <= n enumerated b-major (row b starts at
 // S(b) = b(2n+3-b)/2); x = a, and y (f = 0) or z (f = 1) = b.
 __device__ __forceinline__ void face_point(const double* __restrict__ xin, double* __restrict__ yout, i64 stride,
                                            int n, const P1DeviceTable* __restrict__ tabs,
                                            const MacroDesc* __restrict__ macros, int li, int f, int q,
-                                           const int2* __restrict__ zrange = nullptr) {
+                                           const int2* __restrict__ zrange = nullptr,
+                                           const FusedPut* fp = nullptr) {
   const float c = 2.0f * n + 3.0f;
   int b = static_cast<int>((c - sqrtf(fmaxf(c * c - 8.0f * q, 0.0f))) * 0.5f);
   b = min(max(b, 0), n);
@@ -135,7 +148,10 @@ __device__ __forceinline__ void face_point(const double* __restrict__ xin, doubl
   const int type = (x == 0 ? 1 : 0) | (y == 0 ? 2 : 0) | (z == 0 ? 4 : 0) | (x + y + z == n ? 8 : 0);
   const double* __restrict__ X = xin + static_cast<i64>(li) * stride;
   const double* __restrict__ wt = &tabs[macros[li].group].stencil[type][0];
-  yout[static_cast<i64>(li) * stride + lattice_index(n, x, y, z)] = gather_point(X, wt, n, x, y, z);
+  const i64 j = static_cast<i64>(li) * stride + lattice_index(n, x, y, z);
+  const double v = gather_point(X, wt, n, x, y, z);
+  yout[j] = v;
+  put_slot(fp, j, v);
 }
 
 #if TETMF_P1F_MINB > 0
@@ -409,7 +425,7 @@ constexpr bool kDiagInWalk = !TETMF_P1S_DIAG_EARLY;
 // copies.
 __device__ __forceinline__ void box_diag6(const Task5& t, int wid, int lane, const double* __restrict__ xin,
                                           double* __restrict__ yout, i64 stride, int n,
-                                          const double* __restrict__ tab) {
+                                          const double* __restrict__ tab, const FusedPut* fp) {
   const int y0 = t.y0, x0 = t.pad;
   const int z = t.z0 + 2 * wid;
   const double* __restrict__ Xm = xin + static_cast<i64>(t.macro) * stride;
@@ -417,8 +433,11 @@ __device__ __forceinline__ void box_diag6(const Task5& t, int wid, int lane, con
   const int zz = z + (lane >> 4), yy = y0 + (lane & 15);
   if ((lane & 15) < kRows6 && zz >= 1 && zz <= n && yy >= 1 && yy <= n - zz) {
     const int xx = n - zz - yy;
-    if (xx >= x0 && xx < x0 + kCols6)
-      Ym[lattice_index(n, xx, yy, zz)] = gather_point(Xm, tab + 16 * (8 | (xx == 0 ? 1 : 0)), n, xx, yy, zz);
+    if (xx >= x0 && xx < x0 + kCols6) {
+      const double v = gather_point(Xm, tab + 16 * (8 | (xx == 0 ? 1 : 0)), n, xx, yy, zz);
+      Ym[lattice_index(n, xx, yy, zz)] = v;
+      put_slot(fp, static_cast<i64>(t.macro) * stride + lattice_index(n, xx, yy, zz), v);
+    }
   }
 }
 
@@ -432,7 +451,7 @@ __device__ __forceinline__ void box_diag6(const Task5& t, int wid, int lane, con
 // 0 where the gather uses 0) and the same sum15 order -- bitwise equal.
 __device__ __forceinline__ void box_diag6_smem(const Task5& t, const unsigned* __restrict__ rowtab, int wid,
                                                int lane, double* __restrict__ yout, i64 stride, int n,
-                                               const double* __restrict__ tab) {
+                                               const double* __restrict__ tab, const FusedPut* fp) {
   const int y0 = t.y0, x0 = t.pad;
   const int z = t.z0 + 2 * wid;
   const int zz = z + (lane >> 4), yy = y0 + (lane & 15);
@@ -466,9 +485,29 @@ __device__ __forceinline__ void box_diag6_smem(const Task5& t, const unsigned* _
 #pragma unroll
       for (int k = 0; k < 15; ++k) w[k] = __ldg(wt + k);
       double* __restrict__ Ym = yout + static_cast<i64>(t.macro) * stride;
-      Ym[lattice_index(n, xx, yy, zz)] =
+      const double f =
           sum15(w, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9], v[10], v[11], v[12], v[13], v[14]);
+      Ym[lattice_index(n, xx, yy, zz)] = f;
+      put_slot(fp, static_cast<i64>(t.macro) * stride + lattice_index(n, xx, yy, zz), f);
     }
+  }
+}
+
+// Fused put of the walk's x = 0 column (the only shared slots the walk
+// stores): after the walk, lane l < planes * kRows6 takes row l % kRows6 of
+// plane z + l / kRows6 -- the slots lane 0 stored (the walk's store
+// conditions), read back after __syncwarp, so the index loads of all rows
+// are in flight at once instead of one per row inside the walk.
+__device__ __forceinline__ void x0_column_puts(const Task5& t, const FusedPut* fp, int lane, int z, int planes,
+                                               double* __restrict__ yout, i64 stride, int n) {
+  static_assert(2 * kRows6 <= 32, "one lane per row of the plane pair");
+  __syncwarp();  // lane 0's stores are visible to the warp
+  const int pl = lane / kRows6, r = lane - pl * kRows6;
+  const int ystart = t.y0 == 0 ? 1 : 0;
+  const int rlast = pl == 0 ? (z >= 1 ? n - 1 - (t.y0 + z) : -1) : n - 2 - (t.y0 + z);
+  if (pl < planes && r >= ystart && r <= rlast) {
+    const i64 j = static_cast<i64>(t.macro) * stride + lattice_index(n, 0, t.y0 + r, z + pl);
+    put_slot(fp, j, yout[j]);
   }
 }
 
@@ -477,7 +516,7 @@ __device__ __forceinline__ void box_diag6_smem(const Task5& t, const unsigned* _
 __device__ __forceinline__ void box_walk6(const Task5& t, const unsigned* __restrict__ rowtab, double (&w)[15],
                                           int wid, int lane, const double* __restrict__ xin,
                                           double* __restrict__ yout, i64 stride, int n,
-                                          const double* __restrict__ tab) {
+                                          const double* __restrict__ tab, const FusedPut* fp) {
   const int y0 = t.y0, x0 = t.pad;
   const int z = t.z0 + 2 * wid;
   double* __restrict__ Ym = yout + static_cast<i64>(t.macro) * stride;
@@ -538,10 +577,11 @@ __device__ __forceinline__ void box_walk6(const Task5& t, const unsigned* __rest
       Umm = U0m; Um0 = U00;
     }
   }
+  if (fp && x0 == 0) x0_column_puts(t, fp, lane, z, 2, yout, stride, n);
   if (TETMF_P1S_DIAG_SMEM)
-    box_diag6_smem(t, rowtab, wid, lane, yout, stride, n, tab);
+    box_diag6_smem(t, rowtab, wid, lane, yout, stride, n, tab, fp);
   else if (kDiagInWalk)
-    box_diag6(t, wid, lane, xin, yout, stride, n, tab);
+    box_diag6(t, wid, lane, xin, yout, stride, n, tab, fp);
 }
 
 
@@ -551,7 +591,7 @@ __device__ __forceinline__ void box_walk6(const Task5& t, const unsigned* __rest
 __device__ __forceinline__ void box_walk6_single(const Task5& t, const unsigned* __restrict__ rowtab,
                                                  double (&w)[15], int wid, int lane, const double* __restrict__ xin,
                                                  double* __restrict__ yout, i64 stride, int n,
-                                                 const double* __restrict__ tab) {
+                                                 const double* __restrict__ tab, const FusedPut* fp) {
   const int y0 = t.y0, x0 = t.pad;
   const int z = t.z0 + wid;
   const double* __restrict__ Xm = xin + static_cast<i64>(t.macro) * stride;
@@ -596,11 +636,15 @@ __device__ __forceinline__ void box_walk6_single(const Task5& t, const unsigned*
       Umm = U0m; Um0 = U00;
     }
   }
+  if (fp && x0 == 0) x0_column_puts(t, fp, lane, z, 1, yout, stride, n);
   const int yy = y0 + lane;
   if (lane < kRows6 && z >= 1 && yy >= 1 && yy <= n - z) {
     const int xx = n - z - yy;
-    if (xx >= x0 && xx < x0 + kCols6)
-      Ym[lattice_index(n, xx, yy, z)] = gather_point(Xm, tab + 16 * (8 | (xx == 0 ? 1 : 0)), n, xx, yy, z);
+    if (xx >= x0 && xx < x0 + kCols6) {
+      const double v = gather_point(Xm, tab + 16 * (8 | (xx == 0 ? 1 : 0)), n, xx, yy, z);
+      Ym[lattice_index(n, xx, yy, z)] = v;
+      put_slot(fp, static_cast<i64>(t.macro) * stride + lattice_index(n, xx, yy, z), v);
+    }
   }
 }
 
@@ -609,7 +653,7 @@ __device__ __forceinline__ void box_walk6_single(const Task5& t, const unsigned*
 // persistent CTA double-buffers two boxes (full / empty mbarrier per stage):
 // the copies of box k+1 land while the warps walk box k. Face CTAs (faces
 // z = 0, y = 0) follow the boxes in the same launch.
-template <bool kPersistent>
+template <bool kPersistent, bool kFused>
 #if TETMF_P1S_MINB > 0
 __global__ void __launch_bounds__(32 * kWarps6, TETMF_P1S_MINB)
 #else
@@ -617,7 +661,8 @@ __global__ void __launch_bounds__(32 * kWarps6)
 #endif
 p1_box_kernel(const double* __restrict__ xin, double* __restrict__ yout, const Task5* __restrict__ tasks, int ntasks,
               int nboxctas, int nmacros, i64 stride, int n, const P1DeviceTable* __restrict__ tabs,
-              const MacroDesc* __restrict__ macros, const int2* __restrict__ zrange) {
+              const MacroDesc* __restrict__ macros, const int2* __restrict__ zrange, const FusedPut fput) {
+  const FusedPut* fp = kFused ? &fput : nullptr;  // kFused: the exchange's puts from the store sites
   if (static_cast<int>(blockIdx.x) >= nboxctas) {
     // face CTAs after the boxes (same launch, they fill the tail): faces z = 0
     // and y = 0 of every macro, one point per thread
@@ -625,7 +670,7 @@ p1_box_kernel(const double* __restrict__ xin, double* __restrict__ yout, const T
     const int gid = (static_cast<int>(blockIdx.x) - nboxctas) * static_cast<int>(blockDim.x) + static_cast<int>(threadIdx.x);
     const int li = gid / (2 * T), rem = gid - li * 2 * T;
     if (li < nmacros)
-      face_point(xin, yout, stride, n, tabs, macros, li, rem >= T ? 1 : 0, rem >= T ? rem - T : rem, zrange);
+      face_point(xin, yout, stride, n, tabs, macros, li, rem >= T ? 1 : 0, rem >= T ? rem - T : rem, zrange, fp);
     return;
   }
   extern __shared__ __align__(128) double sm[];
@@ -655,13 +700,13 @@ p1_box_kernel(const double* __restrict__ xin, double* __restrict__ yout, const T
     double w[15];  // interior weights, loaded while the copies land
 #pragma unroll
     for (int k = 0; k < 15; ++k) w[k] = __ldg(tab + k);
-    if (!kDiagInWalk && !kSingle6 && !TETMF_P1S_DIAG_SMEM) box_diag6(t, wid, lane, xin, yout, stride, n, tab);
+    if (!kDiagInWalk && !kSingle6 && !TETMF_P1S_DIAG_SMEM) box_diag6(t, wid, lane, xin, yout, stride, n, tab, fp);
     mbar_wait_parity(&full[0], 0u);
     if (TETMF_P1S_COPYONLY) return;  // A/B: the box copies alone
     if (kSingle6)
-      box_walk6_single(t, rowaddr[0], w, wid, lane, xin, yout, stride, n, tab);
+      box_walk6_single(t, rowaddr[0], w, wid, lane, xin, yout, stride, n, tab, fp);
     else
-      box_walk6(t, rowaddr[0], w, wid, lane, xin, yout, stride, n, tab);
+      box_walk6(t, rowaddr[0], w, wid, lane, xin, yout, stride, n, tab, fp);
     return;
   }
   const int G = nboxctas;
@@ -681,16 +726,16 @@ p1_box_kernel(const double* __restrict__ xin, double* __restrict__ yout, const T
 #pragma unroll
     for (int q = 0; q < 15; ++q) w[q] = __ldg(tab + q);
     if (!kDiagInWalk && !kSingle6 && !TETMF_P1S_DIAG_SMEM && t.z0 + 2 * wid <= n - t.y0)
-      box_diag6(t, wid, lane, xin, yout, stride, n, tab);
+      box_diag6(t, wid, lane, xin, yout, stride, n, tab, fp);
     // every warp observes the box before releasing it (a released,
     // unobserved phase would alias the stage's next phase)
     mbar_wait_parity(&full[st], static_cast<unsigned>(k >> 1) & 1u);
     const int z = t.z0 + (kSingle6 ? wid : 2 * wid);
     if (z <= n - t.y0 && t.pad <= n - t.y0 - z) {
       if (kSingle6)
-        box_walk6_single(t, rowaddr[st], w, wid, lane, xin, yout, stride, n, tab);
+        box_walk6_single(t, rowaddr[st], w, wid, lane, xin, yout, stride, n, tab, fp);
       else
-        box_walk6(t, rowaddr[st], w, wid, lane, xin, yout, stride, n, tab);
+        box_walk6(t, rowaddr[st], w, wid, lane, xin, yout, stride, n, tab, fp);
     }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
@@ -741,10 +786,10 @@ void build_stencil6_tasks(int nmacros, int n, std::vector<int>& out) {
         }
 }
 
-template <bool kPersistent>
+template <bool kPersistent, bool kFused>
 static void launch_p1_box(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
                           int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s,
-                          const int* zrange = nullptr) {
+                          const int* zrange = nullptr, const FusedPut& fp = FusedPut{}) {
   if (ntasks == 0 && !zrange) return;
   if (tet_count(n) + n + 96 >= (i64(1) << 31)) fail_arg("p1 box kernel: level too large for 32-bit lattice offsets");
   // per stage: the box rows + a margin (in slab mode lanes past the short rows
@@ -752,33 +797,36 @@ static void launch_p1_box(const double* x, double* y, const int* d_tasks, int nt
   const std::size_t smem = (kPersistent ? 2 : 1) * (static_cast<std::size_t>(kCopies6) * kPitch6 + 96) * sizeof(double);
   static int box_ctas = 0;
   if (box_ctas == 0) {
-    TETMF_CUDA(cudaFuncSetAttribute(p1_box_kernel<kPersistent>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TETMF_CUDA(cudaFuncSetAttribute(p1_box_kernel<kPersistent, kFused>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
     int dev = 0, sms = 0, per_sm = 0;
     TETMF_CUDA(cudaGetDevice(&dev));
     TETMF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    TETMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p1_box_kernel<kPersistent>, 32 * kWarps6, smem));
+    TETMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p1_box_kernel<kPersistent, kFused>, 32 * kWarps6, smem));
     box_ctas = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int nbox = kPersistent ? (ntasks < box_ctas ? ntasks : box_ctas) : ntasks;
   // boxes, then the face CTAs (faces z = 0 and y = 0) in the same launch
   const int T = (n + 1) * (n + 2) / 2;
   const int face_ctas = (2 * T * nmacros + 32 * kWarps6 - 1) / (32 * kWarps6);
-  p1_box_kernel<kPersistent><<<static_cast<unsigned>(nbox + face_ctas), 32 * kWarps6, smem, s>>>(
+  p1_box_kernel<kPersistent, kFused><<<static_cast<unsigned>(nbox + face_ctas), 32 * kWarps6, smem, s>>>(
       x, y, reinterpret_cast<const Task5*>(d_tasks), ntasks, nbox, nmacros, macro_stride, n, d_tables, d_macros,
-      reinterpret_cast<const int2*>(zrange));
+      reinterpret_cast<const int2*>(zrange), fp);
   check_launch("p1_box");
 }
 
 void launch_p1_stencil6(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
                         int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s,
-                        const int* zrange) {
-  launch_p1_box<false>(x, y, d_tasks, ntasks, macro_stride, n, nmacros, d_tables, d_macros, s, zrange);
+                        const int* zrange, const FusedPut& fp) {
+  if (fp.first)
+    launch_p1_box<false, true>(x, y, d_tasks, ntasks, macro_stride, n, nmacros, d_tables, d_macros, s, zrange, fp);
+  else
+    launch_p1_box<false, false>(x, y, d_tasks, ntasks, macro_stride, n, nmacros, d_tables, d_macros, s, zrange);
 }
 
 void launch_p1_stencil10(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,
                          int nmacros, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
-  launch_p1_box<true>(x, y, d_tasks, ntasks, macro_stride, n, nmacros, d_tables, d_macros, s);
+  launch_p1_box<true, false>(x, y, d_tasks, ntasks, macro_stride, n, nmacros, d_tables, d_macros, s);
 }
 
 void launch_p1_stencil5(const double* x, double* y, const int* d_tasks, int ntasks, i64 macro_stride, int n,

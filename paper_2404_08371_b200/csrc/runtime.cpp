@@ -579,6 +579,10 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
       (form_ == Form::P1KDiffusion && kernel_variant_ >= 4))
     fail_arg("kernel variant " + std::to_string(kernel_variant_) + " does not exist for this form");
   if (form_ == Form::P1Diffusion && kernel_variant_ >= 2) ctx_->ensure_p1_variant_tasks(ld);
+  // put mode: the default K1 kernel stores the exchange's values into the
+  // peers' windows itself (Exchange::fused_begin); the rest use the pack kernel
+  const bool fused = form_ == Form::P1Diffusion && kernel_variant_ == 0 && ld.exchange && ctx_->exchange_fused() &&
+                     ld.exchange->fusable();
   switch (form_) {
     case Form::P1Diffusion:
       if (kernel_variant_ == 1)
@@ -597,7 +601,8 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
                            ld.macros.get(), s);
       else
         launch_p1_stencil6(x, y, ld.tasks6.get(), ld.ntasks6, ld.lay.macro_stride, ld.lay.n, nm, t.p1.get(),
-                           ld.macros.get(), s, ld.zrange.get());
+                           ld.macros.get(), s, ld.zrange.get(),
+                           fused ? ld.exchange->fused_begin(static_cast<i64>(nm) * ld.lay.macro_stride) : FusedPut{});
       break;
     case Form::P1KDiffusion:
       if (kernel_variant_ == 1)
@@ -651,7 +656,10 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
   }
   if (ld.exchange) {
     NvtxRange r("tetmf exchange");
-    ld.exchange->run(y, s);
+    if (fused)
+      ld.exchange->fused_finish(y, s);
+    else
+      ld.exchange->run(y, s);
   }
 }
 

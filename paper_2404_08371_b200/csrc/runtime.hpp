@@ -156,15 +156,24 @@ public:
   void attach_transport(std::shared_ptr<Transport> t) { transport_ = std::move(t); }
   Transport* transport() const { return transport_.get(); }
   // interface exchange mode: false = transport send/recv (default), true =
-  // direct put into the peers' receive windows; set before the first level
-  void set_exchange_put(bool put) {
+  // direct put into the peers' receive windows; fused (put only): whether the
+  // P1 stencil kernel issues the puts itself (kFusedNever, kFusedSlab: in the
+  // slab partition, where it measured faster than the pack kernel,
+  // kFusedAlways); set before the first level
+  enum FusedPolicy { kFusedNever = 0, kFusedSlab = 1, kFusedAlways = 2 };
+  void set_exchange_put(bool put, FusedPolicy fused = kFusedSlab) {
     if (!levels_.empty()) fail_arg("exchange mode: set it before the context's first level is used");
     exchange_put_ = put;
+    exchange_fused_ = put ? fused : kFusedNever;
   }
   bool exchange_put() const { return exchange_put_; }
+  bool exchange_fused() const {
+    return exchange_fused_ == kFusedAlways || (exchange_fused_ == kFusedSlab && partition_ == kPartitionSlab);
+  }
 
 private:
   bool exchange_put_ = false;
+  FusedPolicy exchange_fused_ = kFusedNever;
   MacroMesh mesh_;
   Topology topo_;
   int device_, rank_, nranks_;

@@ -244,7 +244,7 @@ def _modes_run(tm, mesh, form, level, nranks, partition, seeds=(42, 43, 44)):
     under both exchange modes; the level is created inside the rank threads
     because opening a put channel is collective."""
     out = {}
-    for mode in (tm.EXCHANGE_SENDRECV, tm.EXCHANGE_PUT):
+    for mode in (tm.EXCHANGE_SENDRECV, tm.EXCHANGE_PUT, tm.EXCHANGE_PUT_PACK, tm.EXCHANGE_PUT_FUSED):
         group = tm.LoopbackGroup(nranks)
         ctxs = group.contexts(mesh, device=0, partition=partition)
         for c in ctxs:
@@ -267,17 +267,21 @@ def _modes_run(tm, mesh, form, level, nranks, partition, seeds=(42, 43, 44)):
 
 @pytest.mark.parametrize("mesh,form,level,nranks", [("cubes2", "N1", 4, 2), ("cubes2", "N1", 5, 4),
                                                     ("cubes2", "N1", 4, 8), ("cube6", "P1", 6, 8),
-                                                    ("cubes2", "P1K", 4, 3), ("cube6", "P2V", 3, 4)])
+                                                    ("cubes2", "P1K", 4, 3), ("cube6", "P2V", 3, 4),
+                                                    ("cubes2", "P1", 5, 3)])
 def test_put_exchange_equals_sendrecv(tm, mesh, form, level, nranks):
     """TETMF_EXCHANGE_PUT (the pack kernel stores straight into the peers'
-    receive windows; loopback: device pointers, host barrier as the fence)
+    receive windows; TETMF_EXCHANGE_PUT_FUSED, P1: the K1 stencil kernel
+    stores each shared value as it computes it; loopback: device pointers,
+    host barrier as the fence)
     gives the send/recv exchange's results bitwise, apply after apply (each
     apply uses the other window half), and the single-rank apply's."""
     out = _modes_run(tm, mesh, form, level, nranks, tm.PARTITION_MACRO)
     for r in range(nranks):
         for k in range(3):
-            a, b = out[tm.EXCHANGE_SENDRECV][r][k], out[tm.EXCHANGE_PUT][r][k]
-            assert np.array_equal(a, b), f"rank {r} apply {k}"
+            a = out[tm.EXCHANGE_SENDRECV][r][k]
+            for mode in (tm.EXCHANGE_PUT, tm.EXCHANGE_PUT_PACK, tm.EXCHANGE_PUT_FUSED):
+                assert np.array_equal(a, out[mode][r][k]), f"mode {mode} rank {r} apply {k}"
     # and the same as one rank (seed 42)
     ctx1, y1, _, ms = _single(tm, mesh, form, level)
     group = tm.LoopbackGroup(nranks)
@@ -307,8 +311,9 @@ def test_put_exchange_slab_partition(tm, mesh, level, nranks):
             sel = (zslot >= za) & (zslot < zb) & real
             for k in range(3):
                 a = out[tm.EXCHANGE_SENDRECV][r][k].reshape(nmac, ms)[m][sel]
-                b = out[tm.EXCHANGE_PUT][r][k].reshape(nmac, ms)[m][sel]
-                assert np.array_equal(a, b), f"rank {r} macro {m} apply {k}"
+                for mode in (tm.EXCHANGE_PUT, tm.EXCHANGE_PUT_PACK, tm.EXCHANGE_PUT_FUSED):
+                    b = out[mode][r][k].reshape(nmac, ms)[m][sel]
+                    assert np.array_equal(a, b), f"mode {mode} rank {r} macro {m} apply {k}"
 
 
 def test_put_mode_cg_matches_sendrecv(tm):
