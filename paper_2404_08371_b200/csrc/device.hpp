@@ -102,9 +102,10 @@ void launch_n1_fold(const N1GramTable* gram, const MacroDesc* macros, int pass, 
                     i64 class_stride, i64 coeff_stride, int n, int rule, cudaStream_t s, int chunk);
 int n1_kernel_mode();
 // K2 default: cube walk with per-cube edge weights (k_p1k_cube.cu)
-void build_p1k_cube_tasks(int nmacros, int n, std::vector<int>& out);
+void build_p1k_cube_tasks(int nmacros, int n, std::vector<int>& out, int chunk);
+int p1k_cube_chunk(int nmacros, int n, int sms);  // rows = layers per task (16, 8 or 4 by task count)
 void launch_p1k_cube(const double* x, const double* k, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
-                     int n, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s);
+                     int n, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s, int chunk);
 // K2 variant 3 (round-2 first kernel): the gather walked along y with register windows (k_p1k_gather.cu)
 void build_p1k_walk_tasks(int nmacros, int n, std::vector<int>& out);
 void launch_p1k_walk(const double* x, const double* k, double* y, const int* d_tasks, int ntasks, i64 macro_stride,

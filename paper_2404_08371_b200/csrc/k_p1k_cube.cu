@@ -42,6 +42,8 @@
 // neighbouring rows / planes of the same buffer).
 // Tasks are taken dynamically by the warps of one resident wave, heaviest
 // first (the list is sorted by step count).
+#include <cstdlib>
+
 #include "device.hpp"
 #include "runtime_check.hpp"
 
@@ -202,7 +204,7 @@ __device__ __forceinline__ void cube_kbar(const double (&kv)[NC], int s, int n, 
 __global__ void __launch_bounds__(32 * kCWarps, TETMF_P1KC_MINB)
 p1k_cube_kernel(const double* __restrict__ x, const double* __restrict__ kc, double* __restrict__ y,
                 const CubeTask* __restrict__ tasks, int ntasks, i64 stride, int n,
-                const P1DeviceTable* __restrict__ tabs, const MacroDesc* __restrict__ macros) {
+                const P1DeviceTable* __restrict__ tabs, const MacroDesc* __restrict__ macros, int chunk) {
   __shared__ __align__(16) double sT[kCWarps][36];
   __shared__ double sP[kCWarps][kRows][32];
   __shared__ double sRing[kCWarps][kSlots][kWin][32];  // [warp][slot][window entry][lane]
@@ -235,10 +237,10 @@ p1k_cube_kernel(const double* __restrict__ x, const double* __restrict__ kc, dou
     double* yl = y + static_cast<i64>(t.macro) * stride + px;
     asm volatile("" : "+l"(xl), "+l"(kl), "+l"(yl));
     const int r0 = t.y0 == 0 ? 0 : -1;  // halo row unless the chunk starts at y = 0
-    const int zs = t.z0 > 0 ? t.z0 - 1 : 0, ze = min(t.z0 + kLayers - 1, n);
+    const int zs = t.z0 > 0 ? t.z0 - 1 : 0, ze = min(t.z0 + chunk - 1, n);
     for (int z = zs; z <= ze;) {
       const bool two = kPair && z + 1 <= ze;
-      const int rend = min(kRows - 1, n - z - t.x0 - t.y0);  // last row with a stored vertex
+      const int rend = min(chunk - 1, n - z - t.x0 - t.y0);  // last row with a stored vertex
       if (rend < 0) break;                                  // and none in the layers above
       const bool store0 = z >= t.z0, store1 = z + 1 >= t.z0;
       int len[kPl];  // row-0 lengths of planes z, z + 1 (, z + 2)
@@ -310,7 +312,7 @@ p1k_cube_kernel(const double* __restrict__ x, const double* __restrict__ kc, dou
 #pragma unroll
         for (int q = 0; q < NC; ++q) c[q] = 0.0;
         c[0] = R0;                                     // (x, y, z): layer z - 1 and row y - 1 so far
-        c[2] = r + 1 < kRows ? P[32 * (r + 1)] : 0.0;  // (x, y + 1, z): layer z - 1
+        c[2] = r + 1 < chunk ? P[32 * (r + 1)] : 0.0;  // (x, y + 1, z): layer z - 1
         if constexpr (TWO) {
           c[4] = R1;  // (x, y, z + 1): row y - 1 so far
           c[8] = Pn;  // (x, y, z + 2): row y - 1
@@ -391,8 +393,8 @@ p1k_cube_kernel(const double* __restrict__ x, const double* __restrict__ kc, dou
 }
 
 // rows of layer z the task walks (0 if none)
-int task_steps(int n, int x0, int y0, int z) {
-  const int rend = std::min(kRows - 1, n - z - x0 - y0);
+int task_steps(int n, int x0, int y0, int z, int chunk) {
+  const int rend = std::min(chunk - 1, n - z - x0 - y0);
   return rend < 0 ? 0 : rend - (y0 == 0 ? 0 : -1) + 1;
 }
 
@@ -400,18 +402,19 @@ int task_steps(int n, int x0, int y0, int z) {
 
 // one task per (macro, layer chunk, row chunk, 31-column segment) with a
 // stored vertex; heaviest first (the grid's tail then holds the short tasks)
-void build_p1k_cube_tasks(int nmacros, int n, std::vector<int>& out) {
+void build_p1k_cube_tasks(int nmacros, int n, std::vector<int>& out, int chunk) {
+  if (chunk < 1 || chunk > kRows || chunk > kLayers) fail_internal("p1k_cube: chunk out of range");
   struct T {
     int m, x0, y0, z0;
     long cost;
   };
   std::vector<T> ts;
   for (int m = 0; m < nmacros; ++m)
-    for (int z0 = 0; z0 <= n; z0 += kLayers)
-      for (int y0 = 0; y0 <= n - z0; y0 += kRows)
+    for (int z0 = 0; z0 <= n; z0 += chunk)
+      for (int y0 = 0; y0 <= n - z0; y0 += chunk)
         for (int x0 = 0; x0 <= n - z0 - y0; x0 += kSeg) {
           long cost = 0;
-          for (int z = z0 > 0 ? z0 - 1 : 0; z <= std::min(z0 + kLayers - 1, n); ++z) cost += task_steps(n, x0, y0, z);
+          for (int z = z0 > 0 ? z0 - 1 : 0; z <= std::min(z0 + chunk - 1, n); ++z) cost += task_steps(n, x0, y0, z, chunk);
           ts.push_back({m, x0, y0, z0, cost});
         }
   std::stable_sort(ts.begin(), ts.end(), [](const T& a, const T& b) { return a.cost > b.cost; });
@@ -421,9 +424,32 @@ void build_p1k_cube_tasks(int nmacros, int n, std::vector<int>& out) {
   out.insert(out.end(), {0, 0});  // the kernel's task counters (reset by the kernel after each launch)
 }
 
+// rows = layers per task: 16 when that gives every resident warp (8 per SM)
+// two tasks, 8 when that gives it one, else 4. On a small lattice the 16 x 16
+// tasks are fewer than the warps of one wave and each is a serial walk of
+// ~140 steps: config 2 (one macro at L7, 95 / 305 / 1087 tasks) runs 73 /
+// 29 / 21 us with 16 / 8 / 4; cube6 L7 76 / 57 / 70 us; cube6 L8 265 / 306 /
+// 423 us (tools/k2_chunk.py). Results differ by rounding between task sizes
+// (the order a vertex's cube contributions are summed in follows the tasks).
+int p1k_cube_chunk(int nmacros, int n, int sms) {
+  if (const char* e = std::getenv("TETMF_P1KC_CHUNK")) {  // tuning sweeps (tools/k2_chunk.py)
+    const int c = std::atoi(e);
+    if (c >= 1 && c <= std::min(kRows, kLayers)) return c;
+  }
+  std::vector<int> t;
+  int chunk = std::min(kRows, kLayers);
+  while (chunk > 4) {
+    build_p1k_cube_tasks(nmacros, n, t, chunk);
+    if (static_cast<long long>(t.size() / 4) >= static_cast<long long>(chunk) * sms) break;
+    chunk /= 2;
+  }
+  return chunk;
+}
+
 void launch_p1k_cube(const double* x, const double* k, double* y, const int* d_tasks, int ntasks, i64 macro_stride,
-                     int n, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s) {
+                     int n, const P1DeviceTable* d_tables, const MacroDesc* d_macros, cudaStream_t s, int chunk) {
   if (ntasks == 0) return;
+  if (chunk < 1 || chunk > kRows || chunk > kLayers) fail_internal("p1k_cube: chunk out of range");
   // one wave of resident CTAs (the warps take the tasks dynamically)
   static int resident = 0;
   if (resident == 0) {
@@ -438,7 +464,7 @@ void launch_p1k_cube(const double* x, const double* k, double* y, const int* d_t
   }
   const unsigned grid = static_cast<unsigned>(std::min((ntasks + kCWarps - 1) / kCWarps, resident));
   p1k_cube_kernel<<<grid, 32 * kCWarps, 0, s>>>(x, k, y, reinterpret_cast<const CubeTask*>(d_tasks), ntasks,
-                                                macro_stride, n, d_tables, d_macros);
+                                                macro_stride, n, d_tables, d_macros, chunk);
   check_launch("p1k_cube");
 }
 

@@ -190,7 +190,15 @@ Context::LevelData& Context::level(Space s, int level) {
     build_p1k_walk_tasks(static_cast<int>(macros_.size()), n, tasks);
     ld->np1k_walk = static_cast<int>(tasks.size() / 4);
     ld->p1k_walk.upload(tasks.data(), tasks.size(), stream_);
-    build_p1k_cube_tasks(static_cast<int>(macros_.size()), n, tasks);
+    {
+      int sms = 148;
+      TETMF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+      // from the mesh's macro count, not this rank's share: the task size sets
+      // the summation order, and a partitioned apply stays bitwise equal to
+      // the single-rank one
+      ld->p1k_chunk = p1k_cube_chunk(mesh_.num_tets(), n, sms);
+    }
+    build_p1k_cube_tasks(static_cast<int>(macros_.size()), n, tasks, ld->p1k_chunk);
     ld->np1k_cube = static_cast<int>(tasks.size() / 4);
     ld->p1k_cube.upload(tasks.data(), tasks.size(), stream_);
   } else if (s == Space::ND1) {
@@ -616,7 +624,7 @@ void Operator::kernel_apply(const double* x, double* y, int level) {
                         ld.lay.n, t.p1.get(), ld.macros.get(), s);
       else
         launch_p1k_cube(x, coeffs_[0]->data(level), y, ld.p1k_cube.get(), ld.np1k_cube, ld.lay.macro_stride,
-                        ld.lay.n, t.p1.get(), ld.macros.get(), s);
+                        ld.lay.n, t.p1.get(), ld.macros.get(), s, ld.p1k_chunk);
       break;
     case Form::N1CurlCurlMass: {
       auto& cl = ctx_->level(Space::P1, level);

@@ -134,6 +134,7 @@ public:
     int np1k_walk = 0;
     DeviceBuffer<int> p1k_walk;         // P1: column-walk tasks of the P1K walk kernel (K2 variant 3)
     int np1k_cube = 0;
+    int p1k_chunk = 16;                 // rows = layers per cube-walk task (p1k_cube_chunk)
     DeviceBuffer<int> p1k_cube;         // P1: cube-walk tasks of the P1K cube kernel (K2 default)
     int np1k_tasks = 0;
     // solver (solver.hpp): per local macro, [support mask] -> {bit 0 interior,
