@@ -24,6 +24,8 @@
 // Ring arrays (per row): 0..6 x plane z classes 0..6; 7..13 x plane z+1
 // classes 0..6; 14, 15, 16 x plane z+2 classes 0, 1, 3; 17, 18, 19 alpha
 // planes z, z+1, z+2; 20, 21, 22 beta planes z, z+1, z+2.
+#include <cstdlib>
+
 #include "device.hpp"
 #include "n1_common.cuh"
 #include "runtime_check.hpp"
@@ -460,13 +462,25 @@ void pad_n1_fold2_tasks(std::vector<int>& tasks) {
 }
 
 int n1_fold2_chunk(const std::vector<int>& local_macros, int n, int sms) {
-  std::vector<int> t;
-  int chunk = kChunk;
-  while (chunk > 8) {
-    build_n1_fold2_tasks(local_macros, n, 0, t, chunk);
-    if (static_cast<long long>(t.size() / 4) >= 4LL * 10 * sms) break;
-    chunk /= 2;
+  if (const char* e = std::getenv("TETMF_N1F2_CHUNK_STEPS")) {  // tuning sweeps (tools/k3_chunk.py)
+    const int c = std::atoi(e);
+    if (c >= 1) return c;
   }
+  // 32 steps per task while that leaves every resident warp (8 per SM) five
+  // tasks; on small lattices shorter tasks (each pays one halo step) down to
+  // 2 steps: a task is a serial walk and the kernel ends with its longest one.
+  // Measured (tools/k3_chunk.py, profiles/r2_k3_chunk_sweep.txt; bitwise equal
+  // for every length): config 3 (one macro at L6) 72 us at 8 steps, 46 at 4,
+  // 33 at 2; cube6 L6 75 / 70 / 77; 48 macros at L5 102 / 94 / 108.
+  std::vector<int> t;
+  auto count = [&](int c) {
+    build_n1_fold2_tasks(local_macros, n, 0, t, c);
+    return static_cast<long long>(t.size() / 4);
+  };
+  int chunk = kChunk;
+  while (chunk > 8 && count(chunk) < 4LL * 10 * sms) chunk /= 2;
+  if (chunk == 8 && count(8) < 2LL * 8 * sms) chunk = 4;
+  if (chunk == 4 && count(4) < 4LL * sms) chunk = 2;
   return chunk;
 }
 

@@ -36,6 +36,8 @@
 // Ring arrays (per row): 0..6 x edges plane z classes 0..6; 7, 8, 9 x edges
 // plane z+1 classes 0, 1, 3; 10, 11 x vertices planes z, z+1; 12..23 the same
 // for k.
+#include <cstdlib>
+
 #include "device.hpp"
 #include "n1_common.cuh"
 #include "p2v_common.cuh"
@@ -534,13 +536,23 @@ void pad_p2v_fold_tasks(std::vector<int>& tasks) {
 }
 
 int p2v_fold_chunk(const std::vector<int>& local_macros, int n, int sms) {
-  std::vector<int> t;
-  int chunk = kChunk;
-  while (chunk > 8) {
-    build_p2v_fold_tasks(local_macros, n, 0, t, chunk);
-    if (static_cast<long long>(t.size() / 4) >= 4LL * 8 * sms) break;
-    chunk /= 2;
+  if (const char* e = std::getenv("TETMF_P2VF_CHUNK_STEPS")) {  // tuning sweeps (tools/k3_chunk.py --p2v)
+    const int c = std::atoi(e);
+    if (c >= 1) return c;
   }
+  // as n1_fold2_chunk: shorter tasks on small lattices, down to 2 steps
+  // (tools/k3_chunk.py --p2v, profiles/r2_p2v_chunk_sweep.txt; bitwise equal
+  // for every length): one macro at L6 58 us at 8 steps, 39 at 4, 37 at 2;
+  // cube6 L4 51 / 36 / 28; one macro at L7 88 / 88 / 92
+  std::vector<int> t;
+  auto count = [&](int c) {
+    build_p2v_fold_tasks(local_macros, n, 0, t, c);
+    return static_cast<long long>(t.size() / 4);
+  };
+  int chunk = kChunk;
+  while (chunk > 8 && count(chunk) < 4LL * 8 * sms) chunk /= 2;
+  if (chunk == 8 && count(8) < 6LL * sms) chunk = 4;
+  if (chunk == 4 && count(4) < 3LL * sms) chunk = 2;
   return chunk;
 }
 
