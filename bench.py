@@ -299,22 +299,46 @@ def sub_record(tm, torch, key, steps, warmup, device, fp64_peak):
     for _ in range(warmup):
         op.apply(x, y, level)
     torch.cuda.synchronize()
+    # Pass 1 (the value): no events between the kernels of an apply. Events
+    # there cost ~8 us per apply at config 4 and keep the kernels' programmatic
+    # dependent launches (K1 / K4, runtime_check.hpp) from overlapping. Inputs
+    # larger than L2: the steps run back to back inside one event bracket, as a
+    # solver issues them. Inputs that fit: one bracket per step, L2 flushed
+    # outside it.
+    if flush is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(steps):
+            op.apply(x, y, level)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+    else:
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for i in range(steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            op.apply(x, y, level)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        ms = sum(s.elapsed_time(e) for s, e in ev) / steps
+    # Pass 2 (the roofline's kernel time): the same steps with the library's
+    # events around the element kernel of every apply
     op.profile(True)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     for i in range(steps):
         if flush is not None:
             flush.zero_()
-        ev[i][0].record(stream)
         op.apply(x, y, level)
-        ev[i][1].record(stream)
     torch.cuda.synchronize()
     kern_ms, kern_n = op.kernel_stats()
     op.profile(False)
-    ms = sum(s.elapsed_time(e) for s, e in ev) / steps
     n_unique = unique_dofs(cfg["mesh"], form, level)
     rec = {"workload": cfg["name"], "mesh": cfg["mesh"], "level": level, "form": form, "dofs": n_unique,
            "value": n_unique / (ms * 1e-3) / 1e9, "unit": "GDoF/s", "ms_per_step": ms, "steps": steps,
            "l2": "inputs > 126 MB L2" if flush is None else "L2 flushed between steps",
+           "timing": ("one CUDA-event bracket around the steps, applies back to back" if flush is None else
+                      "one CUDA-event bracket per step") + "; kernel_ms from a second pass of the same steps with "
+                     "events around the element kernel",
            "roofline": roofline(key, form, lattice_counts(nmac, level, form), kern_ms / max(kern_n, 1), ms,
                                 fp64_peak)}
     del op, x, y, ctx
@@ -493,6 +517,9 @@ def run_gpu(a):
                        "parallelism": (f"(macro, z-slab) partition over {ws} GPU(s)" if slab else
                                        f"macro partition over {ws} GPU(s)"), "comm": comm_info,
                        "l2": "inputs > 126 MB L2" if flush is None else "L2 flushed between steps",
+           "timing": ("one CUDA-event bracket around the steps, applies back to back" if flush is None else
+                      "one CUDA-event bracket per step") + "; kernel_ms from a second pass of the same steps with "
+                     "events around the element kernel",
                        "setup_s": round(t_setup, 2)},
             "roofline": roof, "clocks": clk.summary(), "gpu_launches": launches,
             "e2e": e2e, "cpu_baseline": cpu,

@@ -663,7 +663,14 @@ p1_box_kernel(const double* __restrict__ xin, double* __restrict__ yout, const T
               int nboxctas, int nmacros, i64 stride, int n, const P1DeviceTable* __restrict__ tabs,
               const MacroDesc* __restrict__ macros, const int2* __restrict__ zrange, const FusedPut fput) {
   const FusedPut* fp = kFused ? &fput : nullptr;  // kFused: the exchange's puts from the store sites
+  // Early trigger only where the next kernel on the stream is another K1 (one
+  // macro: no K4), whose CTAs then set up their barriers during this grid's
+  // tail (config 1: 6.2 -> 4.5 us per apply). With K4 next it is left to the
+  // grid's end: K4 CTAs made resident early and parked in pdl_wait() measured
+  // slower (config 4: 90.1 -> 94.6 us per apply).
+  if (nmacros == 1) pdl_launch_dependents();
   if (static_cast<int>(blockIdx.x) >= nboxctas) {
+    pdl_wait();
     // face CTAs after the boxes (same launch, they fill the tail): faces z = 0
     // and y = 0 of every macro, one point per thread
     const int T = (n + 1) * (n + 2) / 2;
@@ -688,6 +695,7 @@ p1_box_kernel(const double* __restrict__ xin, double* __restrict__ yout, const T
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_wait();  // x and y are the previous grid's (K4 of the last apply, a solver kernel): barriers set up meanwhile
   __syncthreads();
   constexpr int kStage6 = kCopies6 * kPitch6 + 96;  // doubles per stage (+ slab-mode overread margin)
   if (!kPersistent) {
@@ -809,9 +817,9 @@ static void launch_p1_box(const double* x, double* y, const int* d_tasks, int nt
   // boxes, then the face CTAs (faces z = 0 and y = 0) in the same launch
   const int T = (n + 1) * (n + 2) / 2;
   const int face_ctas = (2 * T * nmacros + 32 * kWarps6 - 1) / (32 * kWarps6);
-  p1_box_kernel<kPersistent, kFused><<<static_cast<unsigned>(nbox + face_ctas), 32 * kWarps6, smem, s>>>(
-      x, y, reinterpret_cast<const Task5*>(d_tasks), ntasks, nbox, nmacros, macro_stride, n, d_tables, d_macros,
-      reinterpret_cast<const int2*>(zrange), fp);
+  TETMF_CUDA(launch_pdl(kPdlK1, p1_box_kernel<kPersistent, kFused>, dim3(static_cast<unsigned>(nbox + face_ctas)),
+                        dim3(32 * kWarps6), smem, s, x, y, reinterpret_cast<const Task5*>(d_tasks), ntasks, nbox,
+                        nmacros, macro_stride, n, d_tables, d_macros, reinterpret_cast<const int2*>(zrange), fp));
   check_launch("p1_box");
 }
 
